@@ -1,0 +1,153 @@
+/*
+ * mrab.h — C ABI of libmrab.so: the B200 (sm_100a, fp64) hot path of multi-rate
+ * Adams–Bashforth time integration of the compressible Navier–Stokes equations on overset
+ * SBP-SAT meshes (Mikida, Klöckner, Bodony, arXiv 1805.06607).
+ *
+ * Citations are PAPER.md lines (P:<line>) and the numbered readings R<k> of DESIGN.md §2.
+ *
+ * Conventions (every entry point):
+ *   - A mesh has n[0] x n[1] (x n[2]) points in INDEX order (i fastest).  Host arrays are
+ *     dense, C order: coordinates [dim][n2][n1][n0], states [nc][n2][n1][n0] with
+ *     nc = dim + 2 components (rho, rho u_1..rho u_dim, rho E).  For dim = 2
+ *     set n[2] = 1.
+ *   - All floating point is IEEE fp64.
+ *   - Every call returns an mrab_status and never throws across the ABI; on failure
+ *     mrab_last_error() returns a thread-local message.  Output pointers are left
+ *     untouched (creation calls set *out = NULL).
+ *   - Ownership: the caller owns every descriptor and host array; they are read during the
+ *     call only (copied).  The caller owns the device workspace passed to mrab_create (it
+ *     must outlive the context).  The library owns plans, contexts, CUDA streams, events
+ *     and graphs.
+ *   - Asynchrony: mrab_step is asynchronous on the caller's stream; mrab_get_state,
+ *     mrab_set_state, mrab_rhs and mrab_get_counters synchronise that stream.
+ */
+#ifndef MRAB_H
+#define MRAB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    MRAB_OK = 0,
+    MRAB_E_INVALID = 1,              /* bad argument, J^-1 <= 0 at an active point         */
+    MRAB_E_DEGENERATE_NODES = 2,     /* duplicate AB history nodes                   */
+    MRAB_E_INSUFFICIENT_HISTORY = 3, /* m < n                                        */
+    MRAB_E_MISALIGNED = 4,           /* step multiples do not divide the largest    */
+    MRAB_E_ORPHAN = 5,               /* a receiver has no all-active donor stencil (R17)   */
+    MRAB_E_SEGMENT = 6,              /* an active segment shorter than 8 points (R2)       */
+    MRAB_E_NONFINITE = 7,            /* non-finite state ("rhs blowup")             */
+    MRAB_E_CUDA = 8,                 /* a CUDA runtime error (message has the CUDA string)  */
+    MRAB_E_WORKSPACE = 9             /* workspace NULL / too small / misaligned            */
+} mrab_status;
+
+/* face tags (R16): overset interface, SAT far field, SAT isothermal no-slip wall,
+ * periodic (both faces of a periodic direction) */
+enum { MRAB_BC_OVERSET = 0, MRAB_BC_FARFIELD = 1, MRAB_BC_WALL = 2, MRAB_BC_PERIODIC = 3 };
+
+typedef struct {
+    int dim;                 /* 2 or 3                                                        */
+    int n[3];                /* points per direction (index order); n[2] = 1 when dim = 2     */
+    int periodic[3];         /* 1 = periodic direction (cyclic stencil across the seam)       */
+    int face_bc[3][2];       /* tag of the (min, max) face of each direction                  */
+    double period[3][3];     /* period[k][c]: jump of coordinate c across the seam of k       */
+    const double* xyz;       /* host [dim][n2][n1][n0] node coordinates                       */
+    int priority;            /* hole-cutting priority: higher cuts lower (R17)                */
+    int step_multiple;       /* s_g: finest micro steps per step of this mesh (R8)           */
+} mrab_mesh_desc;
+
+typedef struct {
+    int dim;
+    int n_meshes;
+    const mrab_mesh_desc* meshes;
+    double gamma, Re, Pr;    /* R11/R12: mu = 1, tau scaled by 1/Re, Fourier heat flux      */
+    int viscous;             /* 0 = Euler (F^V = 0, sigma^V = 0)                            */
+    double q_inf[5];         /* far-field state (conserved), nc entries used                */
+    double wall_T;           /* isothermal wall temperature (R16)                           */
+    int order_n;             /* AB order n                                      */
+    int history_m;           /* history length m >= n; m > n = min-norm extended AB */
+    double h;                /* finest micro step; mesh g steps h_g = s_g h                 */
+} mrab_problem;
+
+typedef struct mrab_plan mrab_plan;   /* host setup: tables, metrics, coefficients         */
+typedef struct mrab_ctx mrab_ctx;     /* device state, rings, schedule, CUDA graphs        */
+
+/* AB weights (P:343-361 eq:vandermonde, P:388-394 eq:ext_ab; reading R1 for the moments):
+ * alpha (m, oldest node first) with sum_k alpha_k t_k^(i-1) = (b^i - a^i)/i, i = 1..n, of
+ * minimum 2-norm when m > n.  nodes: host [m] strictly distinct.  alpha_out: host [m].
+ * Errors: INSUFFICIENT_HISTORY (m < n), DEGENERATE_NODES (duplicate nodes), INVALID. */
+mrab_status mrab_ab_weights(const double* nodes, int m, int n, double a, double b,
+                            double* alpha_out);
+
+/* Host setup (P:227-252 overset phases, reading R17; P:628-637 metrics, reading R3;
+ * segments / closures, reading R2).  Builds hole cutting, segment classes, receivers with
+ * donor stencils and Lagrange weights, metric terms and the MRAB coefficient tables.
+ * Errors: INVALID, MISALIGNED, ORPHAN, SEGMENT, INSUFFICIENT_HISTORY, DEGENERATE_NODES. */
+mrab_status mrab_plan_create(const mrab_problem* problem, mrab_plan** out);
+void        mrab_plan_destroy(mrab_plan* plan);
+
+/* Sizes of mesh `mesh` in a plan: points, active points, receivers (any may be NULL). */
+mrab_status mrab_plan_info(const mrab_plan* plan, int mesh, int64_t* n_points,
+                           int64_t* n_active, int64_t* n_receivers);
+
+/* Setup tables of `mesh` (each output may be NULL; sizes from mrab_plan_info):
+ *   iblank       [n_points]        1 active / 0 hole
+ *   recv_point   [R]               flat point index of each receiver (ascending)
+ *   recv_donor   [R]               donor mesh
+ *   recv_base    [R][3]            donor stencil base (wrapped into [0, n)); [2] = 0 in 2-D
+ *   recv_weights [R][3][4]         per-axis Lagrange weights                */
+mrab_status mrab_plan_get_tables(const mrab_plan* plan, int mesh, int8_t* iblank,
+                                 int64_t* recv_point, int32_t* recv_donor,
+                                 int32_t* recv_base, double* recv_weights);
+
+/* Metric terms of `mesh` (reading R3): jinv [n_points] = J^-1, M [dim][dim][n_points] with
+ * M[kappa][i] = J^-1 d kappa / d x_i (zeros at holes). */
+mrab_status mrab_plan_get_metrics(const mrab_plan* plan, int mesh, double* jinv, double* M);
+
+/* Device workspace the context needs, in bytes (256-byte aligned base required). */
+size_t mrab_workspace_bytes(const mrab_plan* plan);
+
+/* Create a context: uploads tables, metrics and the initial states q0[g] (host or device
+ * pointers, dense [nc][n...]) into the caller's device workspace; stream is a
+ * cudaStream_t (NULL = legacy default stream).  t = 0, histories empty.
+ * Errors: WORKSPACE, CUDA, INVALID. */
+mrab_status mrab_create(const mrab_plan* plan, const double* const* q0, void* d_workspace,
+                        size_t ws_bytes, void* stream, mrab_ctx** out);
+void        mrab_destroy(mrab_ctx* ctx);
+
+/* Advance exactly n_macro macro steps H = S_max h (reading R8).  The first m-1
+ * macro steps after create are the RK bootstrap (R5/R6: (m-1) S_max coupled RK3/RK4 micro
+ * steps).  Asynchronous on the context stream.  Errors: CUDA, INVALID. */
+mrab_status mrab_step(mrab_ctx* ctx, int n_macro);
+
+/* Copy mesh `mesh`'s state at the current macro boundary to dst (host or device, dense
+ * [nc][n...]); *t (may be NULL) receives the time.  Synchronises. */
+mrab_status mrab_get_state(mrab_ctx* ctx, int mesh, double* dst, double* t);
+
+/* Overwrite mesh `mesh`'s state at the current macro boundary from src (host or device,
+ * dense [nc][n...]); the RHS histories are kept.  Synchronises. */
+mrab_status mrab_set_state(mrab_ctx* ctx, int mesh, const double* src);
+
+/* Parity hook: one coupled RHS evaluation (eq:int) of every mesh at the given
+ * states q[g] (host or device, dense) -> rhs_out[g] (host or device, dense).  Does not
+ * change the integrator state.  Synchronises. */
+mrab_status mrab_rhs(mrab_ctx* ctx, const double* const* q, double* const* rhs_out);
+
+/* Counters since create: RHS evaluations per mesh (rhs_evals[n_meshes]), sum over meshes of
+ * active points x evaluations, macro steps taken (bootstrap included). */
+mrab_status mrab_get_counters(mrab_ctx* ctx, int64_t* rhs_evals, int64_t* point_rhs,
+                              int64_t* macro_steps);
+
+/* Kernel launches one macro step issues (for the bench's gpu_launches claim). */
+mrab_status mrab_launches_per_macro_step(mrab_ctx* ctx, int64_t* launches);
+
+/* Thread-local message of the last failing call on this thread. */
+const char* mrab_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MRAB_H */

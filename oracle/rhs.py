@@ -49,6 +49,7 @@ class Setup:
     ov: overset.OversetSetup
     geom: List[MeshGeom]
     recv_row: List[dict]
+    stencils: list = None
 
 
 def _sat_groups(mesh, positions):
@@ -82,7 +83,8 @@ def build(problem) -> Setup:
         J = np.where(act, 1.0 / np.where(act, Jinv, 1.0), 0.0)
         geom.append(MeshGeom(Jinv, J, M, act, ov.positions[g], _sat_groups(m, ov.positions[g])))
     recv_row = [{int(p): r for r, p in enumerate(rc.point)} for rc in ov.receivers]
-    return Setup(problem, ov, geom, recv_row)
+    stencils = [_stencils(problem, ov, g) for g in range(len(problem.meshes))]
+    return Setup(problem, ov, geom, recv_row, stencils)
 
 
 def _gradients(prob, geo, q):
@@ -107,21 +109,33 @@ def cartesian_viscous_fluxes(prob, setup, g, q):
     return [gas.viscous_flux(q, du, dT, i, prob.Re, prob.Pr, prob.gamma) for i in range(d)]
 
 
+def _stencils(problem, ov, g):
+    """Per receiver of mesh g: flat donor stencil indices (R, 4^d) and tensor-product
+    Lagrange weights (R, 4^d)."""
+    rc = ov.receivers[g]
+    d = problem.dim
+    offs = overset._stencil_offsets(d)
+    R = len(rc.point)
+    idx = np.zeros((R, 4 ** d), dtype=np.int64)
+    W = np.ones((R, 4 ** d))
+    for r in range(R):
+        idx[r] = overset.stencil_flat(problem.meshes[rc.donor[r]], rc.base[r])
+    for k in range(d):
+        W = W * rc.weights[:, k, :][:, offs[:, k]]
+    return idx, W
+
+
 def interpolate(setup, g, fields_per_mesh):
     """Lagrange interpolation of per-mesh arrays (C, *spatial) at the receivers
-    of mesh g; returns (R, C)."""
+    of mesh g: qhat_r = sum_a W_ra f_donor(r)[stencil_ra]; returns (R, C)."""
     rc = setup.ov.receivers[g]
-    prob = setup.problem
-    out = np.zeros((len(rc.point), fields_per_mesh[0].shape[0]))
-    for r in range(len(rc.point)):
-        dm = prob.meshes[rc.donor[r]]
-        st = overset.stencil_flat(dm, rc.base[r])
-        W = np.ones(len(st))
-        offs = overset._stencil_offsets(dm.dim)
-        for k in range(dm.dim):
-            W = W * rc.weights[r, k, offs[:, k]]
-        F = fields_per_mesh[rc.donor[r]].reshape(fields_per_mesh[rc.donor[r]].shape[0], -1)
-        out[r] = F[:, st] @ W
+    idx, W = setup.stencils[g]
+    C_ = fields_per_mesh[0].shape[0]
+    out = np.zeros((len(rc.point), C_))
+    for dm in np.unique(rc.donor):
+        sel = rc.donor == dm
+        F = fields_per_mesh[dm].reshape(C_, -1)
+        out[sel] = np.einsum("rca,ra->rc", F[:, idx[sel]].transpose(1, 0, 2), W[sel])
     return out
 
 
@@ -169,7 +183,7 @@ def rhs(problem, setup: Setup, states, which=None):
             qp = qf[:, pts].T                                     # (P, nc)
             n = np.stack([(geo.J * geo.M[k][i]).ravel()[pts] for i in range(d)], axis=1)
             if typ == INTERFACE:
-                rows = np.array([setup.recv_row[g][int(p)] for p in pts])
+                rows = np.searchsorted(setup.ov.receivers[g].point, pts)
                 qh = qhat_i[rows]
             elif typ == overset.FARFIELD:
                 qh = np.broadcast_to(problem.q_inf, qp.shape)

@@ -1,0 +1,682 @@
+// C ABI of libmrab.so: plans, contexts, the MRAB schedule and its CUDA graphs.
+//
+// Schedule (P:569-610 Steps 1-7 generalised to N rates, reading R8 of DESIGN.md):
+// a macro step covers micro times t + j h, j = 0..S-1.  At micro time j the meshes with
+// j mod s_g == 0 "step": their RHS is evaluated at their current state and, fused in the
+// same kernel, their state is advanced by one AB step of size h_g = s_g h (the new RHS is
+// pushed into the history ring first).  A mesh that does not step at j but donates to one
+// that does supplies an intermediate state base_g + h_g sum_k beta_k R_k on its donor box
+// (the partial integral of its extrapolant, Steps 2/5).  The first m-1 macro steps are the
+// RK bootstrap (readings R5/R6).  One macro step is captured once per ring/double-buffer
+// phase as a CUDA graph and replayed.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "mrab_internal.h"
+
+using namespace mrab;
+
+static thread_local std::string g_last_error;
+
+static mrab_status fail(mrab_status st, const std::string& msg) {
+    g_last_error = msg;
+    return st;
+}
+
+#define CK(call)                                                                        \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            return fail(MRAB_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+struct mrab_plan {
+    std::shared_ptr<Plan> P;
+};
+
+namespace {
+
+struct MeshDev {
+    double* Q[2] = {nullptr, nullptr};
+    double* ring[kMaxHist] = {nullptr};
+    double* FV = nullptr;
+    double* dstate = nullptr;
+    double* kbuf[4] = {nullptr, nullptr, nullptr, nullptr};
+    double* ystage = nullptr;
+    double* J = nullptr;
+    double* M = nullptr;
+    uint16_t* cls = nullptr;
+    int32_t* recv_slot = nullptr;
+    int64_t* rpoint = nullptr;
+    int32_t* rdonor = nullptr;
+    int32_t* rbase = nullptr;
+    double* rw = nullptr;
+    double* qhat = nullptr;
+    double* fvhat = nullptr;
+    DevMesh dm{};
+};
+
+struct Book {
+    int head[kMaxMeshes];
+    int cur[kMaxMeshes];
+    int pending[kMaxMeshes];
+};
+
+struct Bump {
+    char* base;
+    size_t cap, off;
+    void* take(size_t bytes) {
+        off = (off + 255) & ~(size_t)255;
+        if (off + bytes > cap) return nullptr;
+        void* p = base + off;
+        off += bytes;
+        return p;
+    }
+};
+
+}  // namespace
+
+struct mrab_ctx {
+    std::shared_ptr<Plan> P;
+    cudaStream_t user = nullptr;
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    std::vector<MeshDev> md;
+    Gas gas{};
+    Book book{};
+    int64_t macro = 0;            // macro steps taken (bootstrap included)
+    int64_t boot_micro = 0;       // RK micro steps done
+    std::vector<int64_t> evals;
+    // graphs per phase
+    int period = 1;
+    std::vector<cudaGraphExec_t> graphs;
+    std::vector<Book> book_after;
+    std::vector<std::vector<int64_t>> evals_per_phase;
+    int64_t launches_last = 0;
+    int64_t launch_counter = 0;
+};
+
+// ----------------------------------------------------------------------------------------
+// workspace layout
+// ----------------------------------------------------------------------------------------
+static size_t plan_bytes(const Plan& P, bool dry, mrab_ctx* ctx, Bump* bump, bool* ok) {
+    size_t total = 0;
+    auto take = [&](size_t bytes) -> void* {
+        total += ((bytes + 255) & ~(size_t)255) + 256;
+        if (dry) return nullptr;
+        void* p = bump->take(bytes);
+        if (!p) *ok = false;
+        return p;
+    };
+    const int nc = P.nc, d = P.dim;
+    for (size_t g = 0; g < P.meshes.size(); ++g) {
+        const MeshPlan& m = P.meshes[g];
+        const size_t N = (size_t)m.npts, R = m.rpoint.size();
+        const size_t S = nc * N * sizeof(double);
+        MeshDev* D = dry ? nullptr : &ctx->md[g];
+        for (int b = 0; b < 2; ++b) {
+            void* p = take(S);
+            if (D) D->Q[b] = (double*)p;
+        }
+        for (int k = 0; k < P.history_m; ++k) {
+            void* p = take(S);
+            if (D) D->ring[k] = (double*)p;
+        }
+        {
+            void* p = take((size_t)d * (d + 1) * N * sizeof(double));
+            if (D) D->FV = (double*)p;
+        }
+        {
+            void* p = take(S);
+            if (D) D->dstate = (double*)p;
+        }
+        for (int k = 0; k < 4; ++k) {
+            void* p = take(S);
+            if (D) D->kbuf[k] = (double*)p;
+        }
+        {
+            void* p = take(S);
+            if (D) D->ystage = (double*)p;
+        }
+        if (!m.cartesian) {
+            void* a = take(N * sizeof(double));
+            void* b = take((size_t)d * d * N * sizeof(double));
+            if (D) {
+                D->J = (double*)a;
+                D->M = (double*)b;
+            }
+        }
+        {
+            void* a = take(N * sizeof(uint16_t));
+            void* b = take(N * sizeof(int32_t));
+            if (D) {
+                D->cls = (uint16_t*)a;
+                D->recv_slot = (int32_t*)b;
+            }
+        }
+        {
+            size_t Rm = std::max<size_t>(R, 1);
+            void* a = take(Rm * sizeof(int64_t));
+            void* b = take(Rm * sizeof(int32_t));
+            void* c = take(Rm * 3 * sizeof(int32_t));
+            void* e = take(Rm * 12 * sizeof(double));
+            void* f = take(Rm * nc * sizeof(double));
+            void* h = take(Rm * d * (d + 1) * sizeof(double));
+            if (D) {
+                D->rpoint = (int64_t*)a;
+                D->rdonor = (int32_t*)b;
+                D->rbase = (int32_t*)c;
+                D->rw = (double*)e;
+                D->qhat = (double*)f;
+                D->fvhat = (double*)h;
+            }
+        }
+    }
+    return total + 1024;
+}
+
+// ----------------------------------------------------------------------------------------
+// launches
+// ----------------------------------------------------------------------------------------
+static Box whole_box(const MeshPlan& m) {
+    Box b{};
+    for (int k = 0; k < 3; ++k) {
+        b.lo[k] = 0;
+        b.hi[k] = m.n[k] - 1;
+    }
+    return b;
+}
+
+static Box make_box(const int* lo, const int* hi) {
+    Box b{};
+    for (int k = 0; k < 3; ++k) {
+        b.lo[k] = lo[k];
+        b.hi[k] = hi[k];
+    }
+    return b;
+}
+
+// interpolation for the receivers of mesh g; state_of[d] = state array of donor d
+static void issue_interp(mrab_ctx* c, int g, const double* const* state_of) {
+    const Plan& P = *c->P;
+    MeshDev& D = c->md[g];
+    const MeshPlan& m = P.meshes[g];
+    if (m.rpoint.empty()) return;
+    RecvList rl{};
+    rl.n = (int64_t)m.rpoint.size();
+    rl.point = D.rpoint;
+    rl.donor = D.rdonor;
+    rl.base = D.rbase;
+    rl.w = D.rw;
+    rl.qhat = D.qhat;
+    rl.fvhat = D.fvhat;
+    DonorSet ds{};
+    for (size_t h = 0; h < P.meshes.size(); ++h) {
+        ds.state[h] = state_of[h];
+        ds.fv[h] = c->md[h].FV;
+        for (int k = 0; k < 3; ++k) ds.n[h][k] = P.meshes[h].n[k];
+        ds.npts[h] = P.meshes[h].npts;
+    }
+    launch_interp(P.dim, P.viscous, rl, ds, c->st);
+    c->launch_counter++;
+}
+
+static void issue_visc(mrab_ctx* c, int g, const double* Q, const Box& box) {
+    const Plan& P = *c->P;
+    if (!P.viscous) return;
+    launch_visc(P.dim, c->md[g].dm, Q, c->md[g].FV, box, c->gas, c->st);
+    c->launch_counter++;
+}
+
+static void issue_rhs(mrab_ctx* c, int g, const double* Q, const Epilogue& ep) {
+    launch_rhs(c->P->dim, c->md[g].dm, Q, c->md[g].FV, c->gas, ep, c->st);
+    c->launch_counter++;
+}
+
+// one MRAB macro step (host bookkeeping + launches)
+static void issue_macro_step(mrab_ctx* c) {
+    const Plan& P = *c->P;
+    const int G = (int)P.meshes.size(), m = P.history_m;
+    for (int j = 0; j < P.S; ++j) {
+        std::vector<int> stepping(G, 0), partial(G, 0);
+        for (int g = 0; g < G; ++g) stepping[g] = (j % P.meshes[g].s) == 0;
+        for (int g = 0; g < G; ++g) {
+            if (stepping[g]) continue;
+            for (int h = 0; h < G; ++h)
+                if (stepping[h] && P.donor_of[g][h]) partial[g] = 1;
+        }
+        std::vector<const double*> state_of(G, nullptr);
+        for (int g = 0; g < G; ++g) {
+            MeshDev& D = c->md[g];
+            if (stepping[g]) {
+                if (c->book.pending[g]) {
+                    c->book.cur[g] ^= 1;
+                    c->book.pending[g] = 0;
+                }
+                const double* Q = D.Q[c->book.cur[g]];
+                state_of[g] = Q;
+                issue_visc(c, g, Q, whole_box(P.meshes[g]));
+            } else if (partial[g]) {
+                const MeshPlan& mp = P.meshes[g];
+                const int jj = j % mp.s;
+                const double hg = P.h * mp.s;
+                const double* src[kMaxHist];
+                double cs[kMaxHist];
+                for (int k = 0; k < m; ++k) {
+                    int slot = ((c->book.head[g] - (m - 1) + k) % m + m) % m;   // oldest first
+                    src[k] = D.ring[slot];
+                    cs[k] = hg * P.coef[g][jj][k];
+                }
+                const double* base = D.Q[c->book.cur[g]];
+                launch_combine(P.nc, D.dm, make_box(mp.st_lo, mp.st_hi), base, m, src, cs, D.dstate, c->st);
+                c->launch_counter++;
+                state_of[g] = D.dstate;
+                issue_visc(c, g, D.dstate, make_box(mp.fv_lo, mp.fv_hi));
+            }
+        }
+        for (int g = 0; g < G; ++g)
+            if (stepping[g]) issue_interp(c, g, state_of.data());
+        for (int g = 0; g < G; ++g) {
+            if (!stepping[g]) continue;
+            MeshDev& D = c->md[g];
+            const MeshPlan& mp = P.meshes[g];
+            const double hg = P.h * mp.s;
+            const int newslot = (c->book.head[g] + 1) % m;
+            Epilogue ep{};
+            ep.r_out = D.ring[newslot];
+            ep.y_out = D.Q[c->book.cur[g] ^ 1];
+            ep.base = D.Q[c->book.cur[g]];
+            const std::vector<double>& al = P.coef[g][mp.s];   // full step, oldest first
+            ep.c_new = hg * al[m - 1];
+            ep.nsrc = m - 1;
+            for (int k = 0; k < m - 1; ++k) {
+                int slot = ((c->book.head[g] - (m - 2) + k) % m + m) % m;
+                ep.src[k] = D.ring[slot];
+                ep.csrc[k] = hg * al[k];
+            }
+            issue_rhs(c, g, D.Q[c->book.cur[g]], ep);
+            c->book.head[g] = newslot;
+            c->book.pending[g] = 1;
+            c->evals[g]++;
+        }
+    }
+}
+
+// one coupled RK micro step of the bootstrap
+static void issue_rk_step(mrab_ctx* c) {
+    const Plan& P = *c->P;
+    const int G = (int)P.meshes.size(), m = P.history_m;
+    const bool rk4 = P.order_n >= 4;
+    const int ns = rk4 ? 4 : 3;
+    // Heun RK3 (R5) / classical RK4: a[s][j], b[j]
+    double a[4][4] = {{0}}, b[4] = {0};
+    if (rk4) {
+        a[1][0] = 0.5;
+        a[2][1] = 0.5;
+        a[3][2] = 1.0;
+        b[0] = 1.0 / 6;
+        b[1] = 1.0 / 3;
+        b[2] = 1.0 / 3;
+        b[3] = 1.0 / 6;
+    } else {
+        a[1][0] = 1.0 / 3;
+        a[2][1] = 2.0 / 3;
+        b[0] = 0.25;
+        b[1] = 0.0;
+        b[2] = 0.75;
+    }
+    const int64_t nboot = (int64_t)(m - 1) * P.S;
+    const int64_t left = nboot - c->boot_micro;
+    std::vector<double*> kp(G * 4, nullptr);
+    for (int g = 0; g < G; ++g) {
+        if (c->book.pending[g]) {
+            c->book.cur[g] ^= 1;
+            c->book.pending[g] = 0;
+        }
+        const int s = P.meshes[g].s;
+        bool rec = (left % s == 0) && (left / s <= m - 1);
+        for (int q = 0; q < ns; ++q) kp[g * 4 + q] = c->md[g].kbuf[q];
+        if (rec) {
+            int newslot = (c->book.head[g] + 1) % m;
+            kp[g * 4 + 0] = c->md[g].ring[newslot];
+            c->book.head[g] = newslot;
+        }
+    }
+    for (int s = 0; s < ns; ++s) {
+        std::vector<const double*> state_of(G);
+        for (int g = 0; g < G; ++g) {
+            MeshDev& D = c->md[g];
+            state_of[g] = (s == 0) ? D.Q[c->book.cur[g]] : D.ystage;
+            issue_visc(c, g, state_of[g], whole_box(P.meshes[g]));
+        }
+        for (int g = 0; g < G; ++g) issue_interp(c, g, state_of.data());
+        // every mesh reads its own stage state; the next stage state goes to a second
+        // buffer (dstate) so that no mesh overwrites what another still gathers from.
+        for (int g = 0; g < G; ++g) {
+            MeshDev& D = c->md[g];
+            Epilogue ep{};
+            ep.r_out = kp[g * 4 + s];
+            ep.base = D.Q[c->book.cur[g]];
+            if (s < ns - 1) {
+                ep.y_out = D.dstate;
+                ep.c_new = P.h * a[s + 1][s];
+                ep.nsrc = 0;
+                for (int jx = 0; jx < s; ++jx)
+                    if (a[s + 1][jx] != 0.0) {
+                        ep.src[ep.nsrc] = kp[g * 4 + jx];
+                        ep.csrc[ep.nsrc++] = P.h * a[s + 1][jx];
+                    }
+            } else {
+                ep.y_out = D.Q[c->book.cur[g] ^ 1];
+                ep.c_new = P.h * b[s];
+                ep.nsrc = 0;
+                for (int jx = 0; jx < s; ++jx)
+                    if (b[jx] != 0.0) {
+                        ep.src[ep.nsrc] = kp[g * 4 + jx];
+                        ep.csrc[ep.nsrc++] = P.h * b[jx];
+                    }
+            }
+            issue_rhs(c, g, state_of[g], ep);
+            c->evals[g]++;
+        }
+        if (s < ns - 1)
+            for (int g = 0; g < G; ++g) std::swap(c->md[g].dstate, c->md[g].ystage);
+    }
+    for (int g = 0; g < G; ++g) c->book.pending[g] = 1;
+    c->boot_micro++;
+}
+
+// ----------------------------------------------------------------------------------------
+// C ABI
+// ----------------------------------------------------------------------------------------
+extern "C" {
+
+const char* mrab_last_error(void) { return g_last_error.c_str(); }
+
+mrab_status mrab_ab_weights(const double* nodes, int m, int n, double a, double b, double* alpha_out) {
+    std::string msg;
+    mrab_status st = mrab::ab_weights(nodes, m, n, a, b, alpha_out, &msg);
+    if (st != MRAB_OK) g_last_error = msg;
+    return st;
+}
+
+mrab_status mrab_plan_create(const mrab_problem* problem, mrab_plan** out) {
+    if (!out) return fail(MRAB_E_INVALID, "out is NULL");
+    *out = nullptr;
+    try {
+        auto P = std::make_shared<Plan>();
+        Error err{MRAB_OK, ""};
+        if (!build_plan(problem, *P, err)) return fail(err.st, err.msg);
+        *out = new mrab_plan{P};
+        return MRAB_OK;
+    } catch (const std::exception& e) {
+        return fail(MRAB_E_INVALID, std::string("plan_create: ") + e.what());
+    }
+}
+
+void mrab_plan_destroy(mrab_plan* plan) { delete plan; }
+
+mrab_status mrab_plan_info(const mrab_plan* plan, int mesh, int64_t* n_points, int64_t* n_active,
+                           int64_t* n_receivers) {
+    if (!plan || mesh < 0 || mesh >= (int)plan->P->meshes.size()) return fail(MRAB_E_INVALID, "bad plan/mesh");
+    const MeshPlan& m = plan->P->meshes[mesh];
+    if (n_points) *n_points = m.npts;
+    if (n_active) *n_active = m.nactive;
+    if (n_receivers) *n_receivers = (int64_t)m.rpoint.size();
+    return MRAB_OK;
+}
+
+mrab_status mrab_plan_get_tables(const mrab_plan* plan, int mesh, int8_t* iblank, int64_t* recv_point,
+                                 int32_t* recv_donor, int32_t* recv_base, double* recv_weights) {
+    if (!plan || mesh < 0 || mesh >= (int)plan->P->meshes.size()) return fail(MRAB_E_INVALID, "bad plan/mesh");
+    const MeshPlan& m = plan->P->meshes[mesh];
+    if (iblank) std::memcpy(iblank, m.active.data(), m.npts);
+    const size_t R = m.rpoint.size();
+    if (recv_point && R) std::memcpy(recv_point, m.rpoint.data(), R * sizeof(int64_t));
+    if (recv_donor && R) std::memcpy(recv_donor, m.rdonor.data(), R * sizeof(int32_t));
+    if (recv_base && R) std::memcpy(recv_base, m.rbase.data(), R * 3 * sizeof(int32_t));
+    if (recv_weights && R) std::memcpy(recv_weights, m.rw.data(), R * 12 * sizeof(double));
+    return MRAB_OK;
+}
+
+mrab_status mrab_plan_get_metrics(const mrab_plan* plan, int mesh, double* jinv, double* M) {
+    if (!plan || mesh < 0 || mesh >= (int)plan->P->meshes.size()) return fail(MRAB_E_INVALID, "bad plan/mesh");
+    const MeshPlan& m = plan->P->meshes[mesh];
+    if (jinv) std::memcpy(jinv, m.jinv.data(), m.npts * sizeof(double));
+    if (M) std::memcpy(M, m.M.data(), m.M.size() * sizeof(double));
+    return MRAB_OK;
+}
+
+size_t mrab_workspace_bytes(const mrab_plan* plan) {
+    if (!plan) return 0;
+    bool ok = true;
+    return plan_bytes(*plan->P, true, nullptr, nullptr, &ok);
+}
+
+mrab_status mrab_create(const mrab_plan* plan, const double* const* q0, void* d_workspace,
+                        size_t ws_bytes, void* stream, mrab_ctx** out) {
+    if (!out) return fail(MRAB_E_INVALID, "out is NULL");
+    *out = nullptr;
+    if (!plan || !q0) return fail(MRAB_E_INVALID, "plan or q0 is NULL");
+    if (!d_workspace || ((uintptr_t)d_workspace & 255)) return fail(MRAB_E_WORKSPACE, "workspace NULL or not 256-byte aligned");
+    const Plan& P = *plan->P;
+    if (ws_bytes < mrab_workspace_bytes(plan)) return fail(MRAB_E_WORKSPACE, "workspace too small");
+    std::unique_ptr<mrab_ctx> c(new mrab_ctx());
+    c->P = plan->P;
+    c->user = (cudaStream_t)stream;
+    const int G = (int)P.meshes.size();
+    c->md.resize(G);
+    c->evals.assign(G, 0);
+    Bump bump{(char*)d_workspace, ws_bytes, 0};
+    bool ok = true;
+    plan_bytes(P, false, c.get(), &bump, &ok);
+    if (!ok) return fail(MRAB_E_WORKSPACE, "workspace too small (layout)");
+    CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
+    c->gas.gamma = P.gamma;
+    c->gas.Re = P.viscous ? P.Re : 1.0;
+    c->gas.Pr = P.Pr;
+    c->gas.wall_T = P.wall_T;
+    c->gas.viscous = P.viscous;
+    for (int k = 0; k < 5; ++k) c->gas.q_inf[k] = P.q_inf[k];
+    const int nc = P.nc, d = P.dim;
+    for (int g = 0; g < G; ++g) {
+        const MeshPlan& m = P.meshes[g];
+        MeshDev& D = c->md[g];
+        const size_t N = (size_t)m.npts, R = m.rpoint.size();
+        CK(cudaMemcpyAsync(D.Q[0], q0[g], nc * N * sizeof(double), cudaMemcpyDefault, c->st));
+        CK(cudaMemsetAsync(D.Q[1], 0, nc * N * sizeof(double), c->st));
+        for (int k = 0; k < P.history_m; ++k) CK(cudaMemsetAsync(D.ring[k], 0, nc * N * sizeof(double), c->st));
+        CK(cudaMemsetAsync(D.FV, 0, (size_t)d * (d + 1) * N * sizeof(double), c->st));
+        CK(cudaMemsetAsync(D.dstate, 0, nc * N * sizeof(double), c->st));
+        CK(cudaMemsetAsync(D.ystage, 0, nc * N * sizeof(double), c->st));
+        for (int k = 0; k < 4; ++k) CK(cudaMemsetAsync(D.kbuf[k], 0, nc * N * sizeof(double), c->st));
+        if (!m.cartesian) {
+            std::vector<double> J(N);
+            for (size_t p = 0; p < N; ++p) J[p] = m.active[p] ? 1.0 / m.jinv[p] : 0.0;
+            CK(cudaMemcpy(D.J, J.data(), N * sizeof(double), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(D.M, m.M.data(), (size_t)d * d * N * sizeof(double), cudaMemcpyHostToDevice));
+        }
+        CK(cudaMemcpy(D.cls, m.cls.data(), N * sizeof(uint16_t), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(D.recv_slot, m.recv_slot.data(), N * sizeof(int32_t), cudaMemcpyHostToDevice));
+        if (R) {
+            CK(cudaMemcpy(D.rpoint, m.rpoint.data(), R * sizeof(int64_t), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(D.rdonor, m.rdonor.data(), R * sizeof(int32_t), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(D.rbase, m.rbase.data(), R * 3 * sizeof(int32_t), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(D.rw, m.rw.data(), R * 12 * sizeof(double), cudaMemcpyHostToDevice));
+        }
+        DevMesh& dm = D.dm;
+        for (int k = 0; k < 3; ++k) {
+            dm.n[k] = m.n[k];
+            dm.periodic[k] = m.periodic[k];
+            dm.face_bc[k][0] = m.face_bc[k][0];
+            dm.face_bc[k][1] = m.face_bc[k][1];
+        }
+        dm.npts = m.npts;
+        dm.cart = m.cartesian ? 1 : 0;
+        dm.cJ = m.cart_J;
+        for (int k = 0; k < 3; ++k) dm.cM[k] = m.cart_M[k];
+        dm.J = D.J;
+        dm.M = D.M;
+        dm.cls = D.cls;
+        dm.recv_slot = D.recv_slot;
+        dm.qhat = D.qhat;
+        dm.fvhat = D.fvhat;
+        dm.nrecv = (int64_t)R;
+        c->book.head[g] = P.history_m - 1;   // empty ring: the first push goes to slot 0
+        c->book.cur[g] = 0;
+        c->book.pending[g] = 0;
+    }
+    CK(cudaStreamSynchronize(c->st));
+    // graph period: ring phase (m) and double-buffer phase (2)
+    int L = 1;
+    for (int g = 0; g < G; ++g) {
+        int e = P.S / P.meshes[g].s;
+        int pm = P.history_m / std::gcd(P.history_m, e);
+        int p2 = 2 / std::gcd(2, e);
+        int pg = std::lcm(pm, p2);
+        L = std::lcm(L, pg);
+    }
+    c->period = L;
+    c->graphs.assign(L, nullptr);
+    c->book_after.resize(L);
+    c->evals_per_phase.resize(L);
+    *out = c.release();
+    return MRAB_OK;
+}
+
+void mrab_destroy(mrab_ctx* c) {
+    if (!c) return;
+    cudaStreamSynchronize(c->st);
+    for (auto& g : c->graphs)
+        if (g) cudaGraphExecDestroy(g);
+    if (c->ev_in) cudaEventDestroy(c->ev_in);
+    if (c->ev_out) cudaEventDestroy(c->ev_out);
+    if (c->st) cudaStreamDestroy(c->st);
+    delete c;
+}
+
+mrab_status mrab_step(mrab_ctx* c, int n_macro) {
+    if (!c || n_macro < 0) return fail(MRAB_E_INVALID, "bad ctx / n_macro");
+    const Plan& P = *c->P;
+    CK(cudaEventRecord(c->ev_in, c->user));
+    CK(cudaStreamWaitEvent(c->st, c->ev_in, 0));
+    const int64_t nboot_macro = P.history_m - 1;
+    for (int it = 0; it < n_macro; ++it) {
+        if (c->macro < nboot_macro) {
+            for (int s = 0; s < P.S; ++s) issue_rk_step(c);
+            CK(cudaGetLastError());
+        } else {
+            const int64_t k = c->macro - nboot_macro;
+            const int phase = (int)(k % c->period);
+            if (!c->graphs[phase]) {
+                const Book before = c->book;
+                std::vector<int64_t> ev0 = c->evals;
+                c->launch_counter = 0;
+                CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+                issue_macro_step(c);
+                cudaGraph_t graph;
+                CK(cudaStreamEndCapture(c->st, &graph));
+                CK(cudaGraphInstantiate(&c->graphs[phase], graph, 0));
+                CK(cudaGraphDestroy(graph));
+                c->launches_last = c->launch_counter;
+                c->book_after[phase] = c->book;
+                c->evals_per_phase[phase].resize(c->evals.size());
+                for (size_t g = 0; g < c->evals.size(); ++g) c->evals_per_phase[phase][g] = c->evals[g] - ev0[g];
+                (void)before;
+            } else {
+                c->book = c->book_after[phase];
+                for (size_t g = 0; g < c->evals.size(); ++g) c->evals[g] += c->evals_per_phase[phase][g];
+            }
+            CK(cudaGraphLaunch(c->graphs[phase], c->st));
+        }
+        c->macro++;
+    }
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(c->ev_out, c->st));
+    CK(cudaStreamWaitEvent(c->user, c->ev_out, 0));
+    return MRAB_OK;
+}
+
+static const double* current_state(mrab_ctx* c, int g) {
+    const MeshDev& D = c->md[g];
+    int b = c->book.pending[g] ? (c->book.cur[g] ^ 1) : c->book.cur[g];
+    return D.Q[b];
+}
+
+mrab_status mrab_get_state(mrab_ctx* c, int mesh, double* dst, double* t) {
+    if (!c || mesh < 0 || mesh >= (int)c->md.size() || !dst) return fail(MRAB_E_INVALID, "bad arguments");
+    const Plan& P = *c->P;
+    CK(cudaStreamSynchronize(c->st));
+    const size_t bytes = (size_t)P.nc * P.meshes[mesh].npts * sizeof(double);
+    CK(cudaMemcpyAsync(dst, current_state(c, mesh), bytes, cudaMemcpyDefault, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    if (t) *t = (double)c->macro * P.S * P.h;
+    return MRAB_OK;
+}
+
+mrab_status mrab_set_state(mrab_ctx* c, int mesh, const double* src) {
+    if (!c || mesh < 0 || mesh >= (int)c->md.size() || !src) return fail(MRAB_E_INVALID, "bad arguments");
+    const Plan& P = *c->P;
+    CK(cudaStreamSynchronize(c->st));
+    const size_t bytes = (size_t)P.nc * P.meshes[mesh].npts * sizeof(double);
+    CK(cudaMemcpyAsync((double*)current_state(c, mesh), src, bytes, cudaMemcpyDefault, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return MRAB_OK;
+}
+
+mrab_status mrab_rhs(mrab_ctx* c, const double* const* q, double* const* rhs_out) {
+    if (!c || !q || !rhs_out) return fail(MRAB_E_INVALID, "bad arguments");
+    const Plan& P = *c->P;
+    const int G = (int)P.meshes.size();
+    CK(cudaStreamSynchronize(c->st));
+    std::vector<const double*> state_of(G);
+    for (int g = 0; g < G; ++g) {
+        const size_t bytes = (size_t)P.nc * P.meshes[g].npts * sizeof(double);
+        CK(cudaMemcpyAsync(c->md[g].ystage, q[g], bytes, cudaMemcpyDefault, c->st));
+        state_of[g] = c->md[g].ystage;
+    }
+    for (int g = 0; g < G; ++g) issue_visc(c, g, state_of[g], whole_box(P.meshes[g]));
+    for (int g = 0; g < G; ++g) issue_interp(c, g, state_of.data());
+    for (int g = 0; g < G; ++g) {
+        Epilogue ep{};
+        ep.r_out = c->md[g].kbuf[3];
+        issue_rhs(c, g, state_of[g], ep);
+    }
+    CK(cudaGetLastError());
+    for (int g = 0; g < G; ++g) {
+        const size_t bytes = (size_t)P.nc * P.meshes[g].npts * sizeof(double);
+        CK(cudaMemcpyAsync(rhs_out[g], c->md[g].kbuf[3], bytes, cudaMemcpyDefault, c->st));
+    }
+    CK(cudaStreamSynchronize(c->st));
+    return MRAB_OK;
+}
+
+mrab_status mrab_get_counters(mrab_ctx* c, int64_t* rhs_evals, int64_t* point_rhs, int64_t* macro_steps) {
+    if (!c) return fail(MRAB_E_INVALID, "ctx is NULL");
+    CK(cudaStreamSynchronize(c->st));
+    int64_t pr = 0;
+    for (size_t g = 0; g < c->evals.size(); ++g) {
+        if (rhs_evals) rhs_evals[g] = c->evals[g];
+        pr += c->evals[g] * c->P->meshes[g].nactive;
+    }
+    if (point_rhs) *point_rhs = pr;
+    if (macro_steps) *macro_steps = c->macro;
+    return MRAB_OK;
+}
+
+mrab_status mrab_launches_per_macro_step(mrab_ctx* c, int64_t* launches) {
+    if (!c || !launches) return fail(MRAB_E_INVALID, "bad arguments");
+    *launches = c->launches_last;
+    return MRAB_OK;
+}
+
+}  // extern "C"

