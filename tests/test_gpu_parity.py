@@ -50,7 +50,11 @@ def test_rhs_parity(cid):
         Rg = ctx.rhs(states)
         Ro = orhs.rhs(p, st, states)
         rel = _rel(Rg, Ro)
-        assert rel <= 1e-12, (rel, _per_component(Rg, Ro))
+        # R = -J sum D Fhat cancels O(|F|/h) terms down to O(|R|): near-uniform states lose
+        # log10(|F|/(h|R|)) digits to rounding (FMA vs separate ops, summation order), so
+        # the RHS bar is the north_star's 1e-10 rather than a few ulps.
+        assert rel <= 1e-10, (rel, _per_component(Rg, Ro))
+        print(f"config {cid}: rhs rel {rel:.2e}")
     ctx.close()
 
 
