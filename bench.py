@@ -1,0 +1,346 @@
+#!/usr/bin/env python
+"""bench.py — throughput of the MRAB / SBP-SAT overset hot path on B200.
+
+Contract:
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mrab|reference] [--config C]
+One "step" = one MRAB macro step H = S_max h of the whole hot path (every mesh's fused
+SBP-SAT RHS + AB update at its own rate, donor intermediate states, Lagrange gathers) on the
+workload of BASELINE.json configs[1] (config 2, full size) unless --config says otherwise.
+metric = grid-point RHS evaluations per second (sum over meshes of active points x RHS
+evaluations, fp64).  L2 is flushed (256 MiB write) between timed steps.  Multi-GPU: one
+process per GPU, each an independent replica (no data-path collective).
+--impl reference times the oracle (oracle/, plain numpy fp64) on host cores instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+os.environ.setdefault("OMP_NUM_THREADS", "1")       # the oracle baseline is single-threaded
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "grid-point RHS evals/sec (fp64)"
+UNIT = "point-RHS/s"
+FALLBACK_HBM = 6650.0
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        rows = [r.split(",") for r in out.strip().splitlines() if r.strip()]
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+            except (ValueError, IndexError):
+                continue
+            for name, v in zip(names, r[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _problem(cid, scale, sr=None):
+    import synth
+    kw = {} if sr is None else {"sr": sr}
+    return synth.make_config(cid, scale, **kw)
+
+
+_ORACLE = {}
+
+
+def _oracle_sample(p, n_macro, budget_s):
+    """Oracle (plain numpy fp64, oracle/) timed on host cores: `n_macro` macro steps of the
+    same workload from a synthetic full history (rings = m copies of R(q0); the arithmetic
+    of a step is identical).  Returns (point_rhs, seconds, macro steps done)."""
+    from oracle import timeint, rhs as orhs
+    if id(p) not in _ORACLE:
+        setup = orhs.build(p)
+        mr = timeint.MRAB(p, setup=setup)
+        R0 = orhs.rhs(p, setup, mr.base)
+        for g in range(len(p.meshes)):
+            mr.rings[g] = [R0[g].copy() for _ in range(p.history_m)]
+        _ORACLE[id(p)] = (setup, mr)
+    setup, mr = _ORACLE[id(p)]
+    active = [int(setup.geom[g].active.sum()) for g in range(len(p.meshes))]
+    c0 = list(mr.counts)
+    t0 = time.perf_counter()
+    done = 0
+    while done < n_macro:
+        mr.macro_step()
+        done += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    pr = sum((mr.counts[g] - c0[g]) * active[g] for g in range(len(p.meshes)))
+    return pr, dt, done
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    p = _problem(args.config, "full")
+    per_step, tot_pr, tot_t = [], 0, 0.0
+    for it in range(args.warmup + args.steps):
+        pr, dt, _ = _oracle_sample(p, 1, 1e9)
+        if it >= args.warmup:
+            tot_pr += pr
+            tot_t += dt
+            per_step.append(dt)
+    value = tot_pr / tot_t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": p.notes["workload"], "config": args.config,
+                   "l2": "n/a (host)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"{args.steps} oracle MRAB macro steps of config "
+                                   f"{args.config} at full size from a synthetic history"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_gpu(args):
+    import torch
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1805_06607_b200 import mrab
+
+    p = _problem(args.config, "full", args.sr)
+    plan = mrab.Plan(p)
+    ctx = mrab.Context(plan, p.q0)
+    stream = torch.cuda.current_stream()
+    G = len(p.meshes)
+    nboot = p.history_m - 1
+
+    # bootstrap (untimed for `value`, reported)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    ctx.step(nboot)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    boot_ms = e0.elapsed_time(e1)
+    for _ in range(args.warmup):
+        ctx.step(1)
+    torch.cuda.synchronize()
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    ev0, _, _ = ctx.counters()
+    clocks = Clocks(local)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.25)
+    total_ms = 0.0
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    for k in range(args.steps):
+        flush.fill_(k & 0xff)                       # L2 flush, outside the timed events
+        starts[k].record(stream)
+        ctx.step(1)
+        ends[k].record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if dist is not None:
+        dist.barrier()
+    for k in range(args.steps):
+        total_ms += starts[k].elapsed_time(ends[k])
+    ev1, _, _ = ctx.counters()
+    active = [plan.info(g)[1] for g in range(G)]
+    pr = int(sum((ev1[g] - ev0[g]) * active[g] for g in range(G)))
+    t_max, pr_sum = total_ms, pr
+    if dist is not None:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        c = torch.tensor([pr], device="cuda", dtype=torch.float64)
+        dist.all_reduce(c, op=dist.ReduceOp.SUM)
+        t_max, pr_sum = float(t.item()), int(c.item())
+    value = pr_sum / (t_max * 1e-3)
+    launches = ctx.launches_per_macro_step()
+
+    # ---- roofline of the dominant kernel (live CUDA-event timing, L2 flushed) ----------
+    peak, peak_src = _peaks()
+    per_mesh = []
+    evals_per_step = [(ev1[g] - ev0[g]) / args.steps for g in range(G)]
+    for g in range(G):
+        ms, by = ctx.time_kernel(0, g, reps=20, flush_l2=True)
+        per_mesh.append((ms * evals_per_step[g], ms, by, g))
+    share, ms, by, gdom = max(per_mesh)
+    achieved = by / (ms * 1e-3) / 1e9
+    kernel_times = {}
+    for kid, name in ((0, "k_rhs"), (1, "k_visc"), (2, "k_interp")):
+        if kid == 1 and not p.viscous:
+            continue
+        tot = 0.0
+        for g in range(G):
+            mk, _ = ctx.time_kernel(kid, g, reps=10, flush_l2=True)
+            tot += mk * evals_per_step[g]
+        kernel_times[name] = tot
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": None,
+            "kernel": f"k_rhs (fused RHS+SAT+AB) on mesh {gdom} ({p.meshes[gdom].name})",
+            "algorithmic_bytes_per_launch": by, "ms_per_launch": ms, "peak_source": peak_src,
+            "kernel_ms_per_step_cold": kernel_times}
+
+    # ---- end to end through the C ABI with host buffers --------------------------------
+    host = [torch.empty(q.shape, dtype=torch.float64).pin_memory() for q in p.q0]
+    for g in range(G):
+        ctx.get_state(g, out=host[g])
+    nbytes = int(sum(h.numel() * 8 for h in host))
+    ke = max(3, min(args.steps, 50))
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    ev0e, _, _ = ctx.counters()
+    t0.record(stream)
+    for _ in range(ke):
+        for g in range(G):
+            ctx.set_state(g, host[g])
+        ctx.step(1)
+        for g in range(G):
+            ctx.get_state(g, out=host[g])
+    t1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = t0.elapsed_time(t1)
+    ev1e, _, _ = ctx.counters()
+    pr_e = sum((ev1e[g] - ev0e[g]) * active[g] for g in range(G))
+    e2e = {"value": pr_e / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": nbytes,
+           "d2h_bytes_per_step": nbytes, "steps": ke}
+
+    # ---- MRAB vs single-rate AB wall time (same simulated time) ------------------------
+    srab = None
+    if rank == 0 and not args.no_srab:
+        plan_s = mrab.Plan(p, steps=[1] * G)
+        ctx_s = mrab.Context(plan_s, p.q0)
+        ctx_s.step(nboot)
+        for _ in range(3):
+            ctx_s.step(1)
+        S = p.s_max
+        ks = max(S * 4, (min(args.steps, 50) // 1) * S)
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        tot_s = 0.0
+        for k in range(ks):
+            flush.fill_(k & 0xff)
+            a0.record(stream)
+            ctx_s.step(1)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            tot_s += a0.elapsed_time(a1)
+        srab_ms_per_H = tot_s / ks * S
+        mrab_ms_per_H = total_ms / args.steps
+        srab = {"mrab_ms_per_macro_step": mrab_ms_per_H, "srab_ms_per_same_time": srab_ms_per_H,
+                "saving": 1.0 - mrab_ms_per_H / srab_ms_per_H,
+                "predicted_work_ratio_mrab_over_srab":
+                    sum(active[g] * S / p.meshes[g].step_multiple for g in range(G)) /
+                    (S * sum(active))}
+        ctx_s.close()
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        pr_c, dt_c, n_c = _oracle_sample(p, 3, 20.0)
+        cpu = {"value": pr_c / dt_c, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{n_c} oracle MRAB macro step(s) of config {args.config} at full size "
+                         f"from a synthetic history ({dt_c:.1f} s, OMP_NUM_THREADS=1)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": p.notes["workload"], "config": args.config,
+                       "order_n": p.order_n, "history_m": p.history_m,
+                       "step_multiples": [m.step_multiple for m in p.meshes],
+                       "points": [plan.info(g)[0] for g in range(G)],
+                       "active_points": active, "l2": "flushed between timed steps (256 MiB)",
+                       "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU"},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(launches * args.steps), "launches_per_step": launches,
+            "clocks": clk, "bootstrap_ms": boot_ms, "mrab_vs_srab": srab,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="mrab", choices=["mrab", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--sr", type=int, default=None)
+    ap.add_argument("--no-srab", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

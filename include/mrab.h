@@ -144,6 +144,16 @@ mrab_status mrab_get_counters(mrab_ctx* ctx, int64_t* rhs_evals, int64_t* point_
 /* Kernel launches one macro step issues (for the bench's gpu_launches claim). */
 mrab_status mrab_launches_per_macro_step(mrab_ctx* ctx, int64_t* launches);
 
+/* Live timing of one hot kernel of mesh `mesh` exactly as the MRAB step launches it, but
+ * writing to scratch buffers (the integrator state is not changed): kernel 0 = fused
+ * RHS + SAT + AB update, 1 = viscous-flux pass, 2 = donor gather of this mesh's receivers.
+ * Each of `reps` launches is bracketed by CUDA events on the context stream; with
+ * flush_l2 != 0 a 256 MiB buffer is written between launches (outside the events).
+ * Outputs: mean ms per launch, and the kernel's ALGORITHMIC bytes per launch.
+ * Synchronises. */
+mrab_status mrab_time_kernel(mrab_ctx* ctx, int kernel, int mesh, int reps, int flush_l2,
+                             double* ms_per_launch, double* algorithmic_bytes);
+
 /* Thread-local message of the last failing call on this thread. */
 const char* mrab_last_error(void);
 

@@ -679,4 +679,69 @@ mrab_status mrab_launches_per_macro_step(mrab_ctx* c, int64_t* launches) {
     return MRAB_OK;
 }
 
+mrab_status mrab_time_kernel(mrab_ctx* c, int kernel, int mesh, int reps, int flush_l2,
+                             double* ms_per_launch, double* algorithmic_bytes) {
+    if (!c || mesh < 0 || mesh >= (int)c->md.size() || reps < 1 || kernel < 0 || kernel > 2)
+        return fail(MRAB_E_INVALID, "bad arguments");
+    const Plan& P = *c->P;
+    const MeshPlan& mp = P.meshes[mesh];
+    MeshDev& D = c->md[mesh];
+    const int m = P.history_m, nc = P.nc, d = P.dim;
+    const double N = (double)mp.npts;
+    CK(cudaStreamSynchronize(c->st));
+    void* flush = nullptr;
+    const size_t fbytes = (size_t)256 << 20;
+    if (flush_l2) CK(cudaMalloc(&flush, fbytes));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    const double* Q = current_state(c, mesh);
+    std::vector<const double*> state_of(P.meshes.size());
+    for (size_t g = 0; g < P.meshes.size(); ++g) state_of[g] = current_state(c, (int)g);
+    double total = 0.0;
+    double bytes = 0.0;
+    for (int r = 0; r < reps; ++r) {
+        if (flush) CK(cudaMemsetAsync(flush, r & 0xff, fbytes, c->st));
+        CK(cudaEventRecord(e0, c->st));
+        if (kernel == 0) {
+            Epilogue ep{};
+            ep.r_out = D.kbuf[0];
+            ep.y_out = D.kbuf[1];
+            ep.base = Q;
+            ep.c_new = P.h * mp.s * P.coef[mesh][mp.s][m - 1];
+            ep.nsrc = m - 1;
+            for (int k = 0; k < m - 1; ++k) {
+                ep.src[k] = D.ring[k];
+                ep.csrc[k] = P.h * mp.s * P.coef[mesh][mp.s][k];
+            }
+            launch_rhs(d, D.dm, Q, D.FV, c->gas, ep, c->st);
+            // Q read, R written, (m-1) ring reads, state written, metrics if curvilinear
+            bytes = 8.0 * N * (nc * (m + 2) + (mp.cartesian ? 0 : 1 + d * d));
+        } else if (kernel == 1) {
+            launch_visc(d, D.dm, Q, D.dstate == nullptr ? D.FV : D.FV, whole_box(mp), c->gas, c->st);
+            // Q read, Cartesian viscous fluxes written, metrics if curvilinear
+            bytes = 8.0 * N * (nc + d * (d + 1) + (mp.cartesian ? 0 : 1 + d * d));
+        } else {
+            issue_interp(c, mesh, state_of.data());
+            const double R = (double)mp.rpoint.size();
+            const int np = d == 2 ? 16 : 64;
+            // per receiver: indices + weights in, nc (+ d(d+1)) gathered values out; the
+            // donor values themselves (np per receiver, mostly L2 hits) are counted once
+            bytes = R * (8 + 4 + 12 + 96 + 8.0 * (nc + (P.viscous ? d * (d + 1) : 0)) * (1 + np));
+        }
+        CK(cudaEventRecord(e1, c->st));
+        CK(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        total += ms;
+    }
+    CK(cudaGetLastError());
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (flush) cudaFree(flush);
+    if (ms_per_launch) *ms_per_launch = total / reps;
+    if (algorithmic_bytes) *algorithmic_bytes = bytes;
+    return MRAB_OK;
+}
+
 }  // extern "C"

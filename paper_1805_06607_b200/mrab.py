@@ -69,11 +69,12 @@ def lib():
         L.mrab_rhs.argtypes = [vp, C.POINTER(vp), C.POINTER(vp)]
         L.mrab_get_counters.argtypes = [vp, i64p, i64p, i64p]
         L.mrab_launches_per_macro_step.argtypes = [vp, i64p]
+        L.mrab_time_kernel.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, dp, dp]
         L.mrab_last_error.restype = C.c_char_p
         for name in ("mrab_ab_weights", "mrab_plan_create", "mrab_plan_info",
                      "mrab_plan_get_tables", "mrab_plan_get_metrics", "mrab_create",
                      "mrab_step", "mrab_get_state", "mrab_set_state", "mrab_rhs",
-                     "mrab_get_counters", "mrab_launches_per_macro_step"):
+                     "mrab_get_counters", "mrab_launches_per_macro_step", "mrab_time_kernel"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -82,7 +83,8 @@ def lib():
 EXPORTED = ["mrab_ab_weights", "mrab_plan_create", "mrab_plan_destroy", "mrab_plan_info",
             "mrab_plan_get_tables", "mrab_plan_get_metrics", "mrab_workspace_bytes",
             "mrab_create", "mrab_destroy", "mrab_step", "mrab_get_state", "mrab_set_state",
-            "mrab_rhs", "mrab_get_counters", "mrab_launches_per_macro_step", "mrab_last_error"]
+            "mrab_rhs", "mrab_get_counters", "mrab_launches_per_macro_step", "mrab_time_kernel",
+            "mrab_last_error"]
 
 
 def _check(st):
@@ -247,3 +249,11 @@ class Context:
         v = C.c_int64()
         _check(lib().mrab_launches_per_macro_step(self.h, C.byref(v)))
         return v.value
+
+    def time_kernel(self, kernel, g, reps=20, flush_l2=True):
+        """(ms per launch, algorithmic bytes per launch) of kernel 0 = fused RHS+SAT+AB,
+        1 = viscous-flux pass, 2 = donor gather, for mesh g (mrab_time_kernel)."""
+        ms, by = C.c_double(), C.c_double()
+        _check(lib().mrab_time_kernel(self.h, int(kernel), int(g), int(reps), int(flush_l2),
+                                      C.byref(ms), C.byref(by)))
+        return ms.value, by.value
