@@ -183,7 +183,15 @@ def run_gpu(args):
         ctx.step(1)
     torch.cuda.synchronize()
 
+    # L2 flush between timed steps: write 256 MiB, then read another 256 MiB so the L2 holds
+    # clean lines of an unrelated buffer (a write-only flush would leave ~126 MB of dirty
+    # lines whose write-back would be charged to the next timed step).
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    scrub = torch.ones(32 << 20, dtype=torch.float64, device="cuda")
+
+    def l2_flush(k):
+        flush.fill_(k & 0xff)
+        scrub.sum()
     ev0, _, _ = ctx.counters()
     clocks = Clocks(local)
     if dist is not None:
@@ -195,7 +203,7 @@ def run_gpu(args):
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     for k in range(args.steps):
-        flush.fill_(k & 0xff)                       # L2 flush, outside the timed events
+        l2_flush(k)                                 # outside the timed events
         starts[k].record(stream)
         ctx.step(1)
         ends[k].record(stream)
@@ -281,7 +289,7 @@ def run_gpu(args):
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         tot_s = 0.0
         for k in range(ks):
-            flush.fill_(k & 0xff)
+            l2_flush(k)
             a0.record(stream)
             ctx_s.step(1)
             a1.record(stream)
@@ -331,7 +339,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="mrab", choices=["mrab", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--sr", type=int, default=None)
     ap.add_argument("--no-srab", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

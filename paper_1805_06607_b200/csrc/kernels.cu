@@ -11,25 +11,9 @@
 
 #include "kernels.cuh"
 #include "mrab_internal.h"
+#include "stencil_table.cuh"
 
 namespace mrab {
-
-// SBP 2-4 diagonal-norm rows by class code (0 hole, 1 interior, 2..5 left r, 6..9 right r)
-__constant__ int c_nst[10] = {0, 4, 4, 2, 4, 4, 4, 2, 4, 4};
-__constant__ int c_off[10][4] = {{0, 0, 0, 0},   {-2, -1, 1, 2}, {0, 1, 2, 3},  {-1, 1, 0, 0},
-                                 {-2, -1, 1, 2}, {-3, -1, 1, 2}, {0, -1, -2, -3}, {1, -1, 0, 0},
-                                 {2, 1, -1, -2}, {3, 1, -1, -2}};
-__constant__ double c_cf[10][4] = {
-    {0, 0, 0, 0},
-    {1.0 / 12, -2.0 / 3, 2.0 / 3, -1.0 / 12},
-    {-24.0 / 17, 59.0 / 34, -4.0 / 17, -3.0 / 34},
-    {-0.5, 0.5, 0, 0},
-    {4.0 / 43, -59.0 / 86, 59.0 / 86, -4.0 / 43},
-    {3.0 / 98, -59.0 / 98, 32.0 / 49, -4.0 / 49},
-    {24.0 / 17, -59.0 / 34, 4.0 / 17, 3.0 / 34},
-    {0.5, -0.5, 0, 0},
-    {-4.0 / 43, 59.0 / 86, -59.0 / 86, 4.0 / 43},
-    {-3.0 / 98, 59.0 / 98, -32.0 / 49, 4.0 / 49}};
 
 void upload_stencil_rows() {}
 
@@ -431,8 +415,15 @@ void launch_visc(int dim, const DevMesh& m, const double* Q, double* FV, const B
     }
 }
 
+void launch_rhs2d(const DevMesh& m, const double* Q, const Gas& g, const Epilogue& ep,
+                  const DonorSet& ds, cudaStream_t st);
+
 void launch_rhs(int dim, const DevMesh& m, const double* Q, const double* FV, const Gas& gas,
-                const Epilogue& ep, cudaStream_t st) {
+                const Epilogue& ep, const DonorSet& ds, cudaStream_t st) {
+    if (dim == 2) {
+        launch_rhs2d(m, Q, gas, ep, ds, st);
+        return;
+    }
     unsigned nb = blocks_for(m.npts, 256);
 #define MRAB_RHS(D, V, C) k_rhs<D, V, C><<<nb, 256, 0, st>>>(m, Q, FV, gas, ep)
     if (dim == 2) {
@@ -464,6 +455,20 @@ void launch_combine(int nc, const DevMesh& m, const Box& box, const double* base
                   (box.hi[2] - box.lo[2] + 1);
     if (tot <= 0) return;
     k_combine<<<blocks_for(tot, 256), 256, 0, st>>>(nc, m.npts, m.n[0], m.n[1], box, a, out);
+}
+
+__global__ void k_scrub_read(const double4* __restrict__ b, size_t n, double* sink) {
+    double acc = 0.0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        double4 v = b[i];
+        acc += v.x + v.y + v.z + v.w;
+    }
+    if (acc == 12345.678) *sink = acc;   // keeps the loads alive, never true for scrub data
+}
+
+void launch_l2_scrub(void* a, void* b, size_t bytes, int tag, cudaStream_t st) {
+    cudaMemsetAsync(a, tag & 0xff, bytes, st);
+    k_scrub_read<<<148 * 8, 256, 0, st>>>((const double4*)b, bytes / sizeof(double4), (double*)a);
 }
 
 void launch_interp(int dim, int viscous, const RecvList& rl, const DonorSet& ds, cudaStream_t st) {

@@ -22,12 +22,17 @@ struct DevMesh {
     const double* qhat;        // [nc][R] interpolated donor state at this mesh's receivers
     const double* fvhat;       // [d][d+1][R] interpolated donor Cartesian viscous fluxes
     int64_t nrecv;
+    const int32_t* rdonor;     // [R] donor mesh of each receiver
+    const int32_t* rbase;      // [R][3] donor stencil base
+    const double* rw;          // [R][3][4] per-axis Lagrange weights
 };
 
 struct Gas {
     double gamma, Re, Pr, wall_T;
     double q_inf[5];
     int viscous;
+    // host-precomputed: 1/Re, mu/(Re Pr (gamma-1)), gamma-1, 1/(gamma-1), 1/gamma
+    double iRe, kT, gm1, igm1, igamma;
 };
 
 // y_out = base + c_new * R + sum_k csrc[k] * src[k]  (all [nc][npts]); r_out = R
@@ -64,13 +69,50 @@ struct DonorSet {             // per donor mesh: where to read state / viscous f
     int64_t npts[8];
 };
 
+// State of every mesh at one evaluation time as a linear combination
+// state_h = base_h + sum_k c_hk src_hk (nsrc = 0: the base itself).  Used to form donor
+// intermediate states on the fly (MRAB Steps 2/5).
+struct SrcSet {
+    const double* base[8];
+    const double* src[8][6];
+    double c[8][6];
+    int nsrc[8];
+};
+
+// receivers (of up to 8 receiving meshes) whose donor data one launch gathers
+struct RecvTask {
+    int nmesh;
+    int64_t off[9];                 // prefix sums of receiver counts
+    const int32_t* rdonor[8];
+    const int32_t* rbase[8];
+    const double* rw[8];
+    double* qhat[8];
+    double* fvhat[8];
+    int64_t nrecv[8];
+};
+
+struct MeshTable {
+    DevMesh m[8];
+};
+
+// 2-D donor kernel: for every receiver, 16 lanes (one per donor stencil point) form the donor
+// state on the fly, its Cartesian viscous flux from segmented D1 gradients, and
+// shuffle-reduce the Lagrange-weighted sums into qhat / fvhat.
+void launch_donor2d(const RecvTask& rt, const SrcSet& ss, const MeshTable& mt, const Gas& gas,
+                    cudaStream_t st);
+
 void launch_visc(int dim, const DevMesh& m, const double* Q, double* FV, const Box& box,
                  const Gas& gas, cudaStream_t st);
+// 3-D: direct kernel reading FV and the gathered qhat/fvhat; 2-D: tiled kernel that forms
+// its own viscous fluxes and gathers donor data inline at its receivers from `ds`.
 void launch_rhs(int dim, const DevMesh& m, const double* Q, const double* FV, const Gas& gas,
-                const Epilogue& ep, cudaStream_t st);
+                const Epilogue& ep, const DonorSet& ds, cudaStream_t st);
 void launch_combine(int nc, const DevMesh& m, const Box& box, const double* base, int nsrc,
                     const double* const* src, const double* csrc, double* out, cudaStream_t st);
 void launch_interp(int dim, int viscous, const RecvList& rl, const DonorSet& ds, cudaStream_t st);
 void upload_stencil_rows();
+// L2 scrub for cold-cache timing: write `a` (bytes) then stream-read `b` (bytes) so that the
+// L2 ends up holding clean lines of an unrelated buffer (no dirty write-backs later).
+void launch_l2_scrub(void* a, void* b, size_t bytes, int tag, cudaStream_t st);
 
 }  // namespace mrab

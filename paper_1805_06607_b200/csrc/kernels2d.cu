@@ -1,0 +1,576 @@
+// 2-D fused SBP-SAT right-hand side, shared-memory tiled (sm_100a, fp64).
+//
+// One CTA = one TX x TY tile of output points.  Everything the viscous RHS needs is staged
+// once per tile (kernel k_rhs2d):
+//   phase A  primitives (rho, (u, v), T) of the tile + halo H = 6 (viscous) / 3 (Euler) and
+//            the stencil-class codes, read once from HBM (coalesced rows, periodic wrap),
+//            all loads of a thread issued before the first is consumed;
+//   phase B  at tile + 3: D1 gradients of (u, v, T) (segment closures by class code,
+//            P:1526-1528 D1 o D1), Cartesian gradients via the metric terms, viscous and
+//            inviscid fluxes, contravariant fluxes Fhat_xi, Fhat_eta -> shared memory;
+//   phase C  R = -J (D_xi Fhat_xi + D_eta Fhat_eta), SAT at segment ends
+//            (eq:int P:279-299), and the AB / RK combination epilogue (eq:ab_general) whose
+//            HBM inputs are requested before the divergence is formed.
+// Interior points (class 1 in a direction) take a compile-time 5-point stencil, closure rows
+// the constant-memory table; (u, v) and flux component pairs are packed as double2 so one
+// 16-byte shared load serves two fields.
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+#include "mrab_internal.h"
+#include "stencil_table.cuh"
+
+namespace mrab {
+
+namespace {
+
+constexpr int TX = 32, TY = 16, NT = 256;
+constexpr int G3 = 3;
+constexpr double kP0 = 17.0 / 48.0;
+constexpr double C1 = 2.0 / 3.0, C2 = 1.0 / 12.0;
+
+template <bool VISC>
+struct Geo {
+    static constexpr int H = VISC ? 6 : 3;
+    static constexpr int AX = TX + 2 * H, AY = TY + 2 * H;
+    static constexpr int FX = TX + 2 * G3, FY = TY + 2 * G3;
+    static constexpr int NA = AX * AY, NF = FX * FY;
+    // shared layout: uv[NA] (double2), fh[4][NF] (double2: xi (F0,F1), xi (F2,F3),
+    // eta (F0,F1), eta (F2,F3)), rho[NA], T[NA], cls[NA] (uint16)
+    static constexpr size_t bytes = 16 * (size_t)NA + 64 * (size_t)NF + 16 * (size_t)NA + 2 * (size_t)NA;
+};
+
+__device__ __forceinline__ double d_int(const double* f, int s, int st) {
+    return C1 * (f[s + st] - f[s - st]) - C2 * (f[s + 2 * st] - f[s - 2 * st]);
+}
+__device__ __forceinline__ double2 d_int2(const double2* f, int s, int st) {
+    const double2 a = f[s + st], b = f[s - st], c = f[s + 2 * st], d = f[s - 2 * st];
+    return make_double2(C1 * (a.x - b.x) - C2 * (c.x - d.x), C1 * (a.y - b.y) - C2 * (c.y - d.y));
+}
+__device__ __forceinline__ double d_gen(const double* f, int s, int st, int cl) {
+    double acc = 0.0;
+    const int n = c_nst[cl];
+    for (int t = 0; t < n; ++t) acc += c_cf[cl][t] * f[s + c_off[cl][t] * st];
+    return acc;
+}
+__device__ __forceinline__ double2 d_gen2(const double2* f, int s, int st, int cl) {
+    double2 acc = make_double2(0.0, 0.0);
+    const int n = c_nst[cl];
+    for (int t = 0; t < n; ++t) {
+        const double c = c_cf[cl][t];
+        const double2 v = f[s + c_off[cl][t] * st];
+        acc.x += c * v.x;
+        acc.y += c * v.y;
+    }
+    return acc;
+}
+
+// characteristic SAT penalty (same algebra as kernels.cu kchar<2>)
+__device__ __forceinline__ void kchar2(const double* q, const double* n, double side,
+                                       const double* dq, const Gas& g, double* out) {
+    const double rho = q[0];
+    const double u0 = q[1] / rho, u1 = q[2] / rho;
+    const double ke = u0 * u0 + u1 * u1;
+    const double p = g.gm1 * (q[3] - 0.5 * rho * ke);
+    const double c2 = g.gamma * p / rho, c = sqrt(c2);
+    const double H = (q[3] + p) / rho;
+    const double nn = sqrt(n[0] * n[0] + n[1] * n[1]);
+    const double n0 = n[0] / nn, n1 = n[1] / nn;
+    const double un = u0 * n0 + u1 * n1;
+    const double du0 = (dq[1] - u0 * dq[0]) / rho, du1 = (dq[2] - u1 * dq[0]) / rho;
+    const double dp = g.gm1 * (dq[3] - (u0 * dq[1] + u1 * dq[2]) + 0.5 * ke * dq[0]);
+    const double dun = du0 * n0 + du1 * n1;
+    const double ap = (dp + rho * c * dun) / (2.0 * c2);
+    const double am = (dp - rho * c * dun) / (2.0 * c2);
+    const double a0 = dq[0] - dp / c2;
+    const double l0 = fmax(side * un * nn, 0.0);
+    const double lp = fmax(side * (un + c) * nn, 0.0);
+    const double lm = fmax(side * (un - c) * nn, 0.0);
+    const double dt0 = du0 - dun * n0, dt1 = du1 - dun * n1;
+    const double wp = lp * ap, wm = lm * am, w0 = l0 * a0;
+    out[0] = wp + wm + w0;
+    out[1] = wp * (u0 + c * n0) + wm * (u0 - c * n0) + w0 * u0 + l0 * rho * dt0;
+    out[2] = wp * (u1 + c * n1) + wm * (u1 - c * n1) + w0 * u1 + l0 * rho * dt1;
+    out[3] = wp * (H + c * un) + wm * (H - c * un) + w0 * (0.5 * ke) + l0 * rho * (u0 * dt0 + u1 * dt1);
+}
+
+// Cartesian viscous fluxes at shared point s (prim index) with class code `code`
+template <bool CART, int AX>
+__device__ __forceinline__ void visc_at(const double2* __restrict__ sh_uv, const double* __restrict__ sh_T,
+                                        int s, unsigned code, const DevMesh& m, int64_t p,
+                                        const Gas& g, double* Fx, double* Fy) {
+    const int cx = code & 15, cy = (code >> 4) & 15;
+    double2 uvx, uvy;
+    double Tx, Ty;
+    if (cx == CLS_INT) {
+        uvx = d_int2(sh_uv, s, 1);
+        Tx = d_int(sh_T, s, 1);
+    } else {
+        uvx = d_gen2(sh_uv, s, 1, cx);
+        Tx = d_gen(sh_T, s, 1, cx);
+    }
+    if (cy == CLS_INT) {
+        uvy = d_int2(sh_uv, s, AX);
+        Ty = d_int(sh_T, s, AX);
+    } else {
+        uvy = d_gen2(sh_uv, s, AX, cy);
+        Ty = d_gen(sh_T, s, AX, cy);
+    }
+    double dudx, dudy, dvdx, dvdy, dTdx, dTdy;
+    if (CART) {
+        const double sx = m.cJ * m.cM[0], sy = m.cJ * m.cM[1];
+        dudx = sx * uvx.x; dvdx = sx * uvx.y; dTdx = sx * Tx;
+        dudy = sy * uvy.x; dvdy = sy * uvy.y; dTdy = sy * Ty;
+    } else {
+        const int64_t N = m.npts;
+        const double J = __ldg(m.J + p);
+        const double Mxx = __ldg(m.M + p), Mxy = __ldg(m.M + N + p);
+        const double Myx = __ldg(m.M + 2 * N + p), Myy = __ldg(m.M + 3 * N + p);
+        dudx = J * (Mxx * uvx.x + Myx * uvy.x); dudy = J * (Mxy * uvx.x + Myy * uvy.x);
+        dvdx = J * (Mxx * uvx.y + Myx * uvy.y); dvdy = J * (Mxy * uvx.y + Myy * uvy.y);
+        dTdx = J * (Mxx * Tx + Myx * Ty); dTdy = J * (Mxy * Tx + Myy * Ty);
+    }
+    const double div = dudx + dvdy;
+    const double txx = (2.0 * dudx - (2.0 / 3.0) * div) * g.iRe;
+    const double tyy = (2.0 * dvdy - (2.0 / 3.0) * div) * g.iRe;
+    const double txy = (dudy + dvdx) * g.iRe;
+    const double2 uv = sh_uv[s];
+    Fx[0] = 0.0; Fx[1] = txx; Fx[2] = txy; Fx[3] = uv.x * txx + uv.y * txy + g.kT * dTdx;
+    Fy[0] = 0.0; Fy[1] = txy; Fy[2] = tyy; Fy[3] = uv.x * txy + uv.y * tyy + g.kT * dTdy;
+}
+
+// Lagrange gather of the donor state and Cartesian viscous fluxes at receiver
+// `slot` of mesh m: tensor product of the per-axis weights over the 4 x 4 donor stencil.
+template <bool VISC>
+__device__ __forceinline__ void gather2(const DevMesh& m, const DonorSet& ds, int slot,
+                                        double* qh, double* fvh) {
+    const int dm = m.rdonor[slot];
+    const int b0 = m.rbase[3 * slot], b1 = m.rbase[3 * slot + 1];
+    const double* w = m.rw + 12 * slot;
+    const int n0 = ds.n[dm][0], n1 = ds.n[dm][1];
+    const int64_t N = ds.npts[dm];
+    const double* __restrict__ S = ds.state[dm];
+    const double* __restrict__ F = ds.fv[dm];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) qh[c] = 0.0;
+    if (VISC)
+#pragma unroll
+        for (int c = 0; c < 6; ++c) fvh[c] = 0.0;
+#pragma unroll
+    for (int a1 = 0; a1 < 4; ++a1) {
+        int jj = b1 + a1;
+        if (jj >= n1) jj -= n1;
+        const double w1 = w[4 + a1];
+#pragma unroll
+        for (int a0 = 0; a0 < 4; ++a0) {
+            int ii = b0 + a0;
+            if (ii >= n0) ii -= n0;
+            const double W = w1 * w[a0];
+            const int64_t q = ii + (int64_t)n0 * jj;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) qh[c] += W * __ldg(S + c * N + q);
+            if (VISC)
+#pragma unroll
+                for (int c = 0; c < 6; ++c) fvh[c] += W * __ldg(F + c * N + q);
+        }
+    }
+}
+
+}  // namespace
+
+template <bool VISC, bool CART>
+__global__ void __launch_bounds__(NT, 2) k_rhs2d(DevMesh m, const double* __restrict__ Q, Gas g,
+                                                 Epilogue ep, DonorSet ds) {
+    using GG = Geo<VISC>;
+    constexpr int H = GG::H, AX = GG::AX, FX = GG::FX;
+    constexpr int NA = GG::NA, NF = GG::NF;
+    extern __shared__ __align__(16) double smem[];
+    double2* sh_uv = reinterpret_cast<double2*>(smem);
+    double2* fh = sh_uv + NA;                       // [4][NF]
+    double* sh_r = reinterpret_cast<double*>(fh + 4 * NF);
+    double* sh_T = sh_r + NA;
+    uint16_t* sh_c = reinterpret_cast<uint16_t*>(sh_T + NA);
+
+    const int n0 = m.n[0], n1 = m.n[1];
+    const int64_t N = m.npts;
+    const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
+    const int tid = threadIdx.x;
+
+    // ---- phase A: primitives of tile + halo ------------------------------------------
+    constexpr int KA = (NA + NT - 1) / NT;
+    {
+        double ld[KA][4];
+        unsigned cd[KA];
+#pragma unroll
+        for (int k = 0; k < KA; ++k) {
+            const int t = tid + k * NT;
+            cd[k] = 0;
+            ld[k][0] = 1.0;
+            ld[k][1] = ld[k][2] = ld[k][3] = 0.0;
+            if (t < NA) {
+                const int b = t / AX, a = t - b * AX;
+                int gi = i0 - H + a, gj = j0 - H + b;
+                bool ok = true;
+                if (gi < 0 || gi >= n0) {
+                    if (m.periodic[0]) gi = gi < 0 ? gi + n0 : gi - n0; else ok = false;
+                }
+                if (gj < 0 || gj >= n1) {
+                    if (m.periodic[1]) gj = gj < 0 ? gj + n1 : gj - n1; else ok = false;
+                }
+                if (ok) {
+                    const int64_t q = gi + (int64_t)n0 * gj;
+                    cd[k] = m.cls[q];
+                    ld[k][0] = __ldg(Q + q);
+                    ld[k][1] = __ldg(Q + N + q);
+                    ld[k][2] = __ldg(Q + 2 * N + q);
+                    ld[k][3] = __ldg(Q + 3 * N + q);
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < KA; ++k) {
+            const int t = tid + k * NT;
+            if (t >= NA) break;
+            double r = 1.0, u = 0.0, v = 0.0, T = 0.0;
+            if (cd[k]) {
+                r = ld[k][0];
+                const double ir = 1.0 / r;
+                u = ld[k][1] * ir;
+                v = ld[k][2] * ir;
+                T = g.gamma * g.gm1 * (ld[k][3] - 0.5 * (ld[k][1] * u + ld[k][2] * v)) * ir;
+            }
+            sh_c[t] = (uint16_t)cd[k];
+            sh_r[t] = r;
+            sh_uv[t] = make_double2(u, v);
+            sh_T[t] = T;
+        }
+    }
+    __syncthreads();
+
+    // ---- phase B: contravariant fluxes at tile + 3 -----------------------------------
+    for (int t = tid; t < NF; t += NT) {
+        const int b = t / FX, a = t - b * FX;
+        const int s = (b + H - G3) * AX + (a + H - G3);
+        const unsigned code = sh_c[s];
+        double fx[4] = {0, 0, 0, 0}, fy[4] = {0, 0, 0, 0};
+        if (code) {
+            const double r = sh_r[s];
+            const double2 uv = sh_uv[s];
+            const double u = uv.x, v = uv.y;
+            const double p = r * sh_T[s] * g.igamma;
+            const double E = p * g.igm1 + 0.5 * r * (u * u + v * v);
+            double Ix[4] = {r * u, r * u * u + p, r * u * v, (E + p) * u};
+            double Iy[4] = {r * v, r * u * v, r * v * v + p, (E + p) * v};
+            int64_t q = 0;
+            if (!CART) {
+                int gi = i0 - G3 + a, gj = j0 - G3 + b;
+                if (gi < 0) gi += n0; else if (gi >= n0) gi -= n0;
+                if (gj < 0) gj += n1; else if (gj >= n1) gj -= n1;
+                q = gi + (int64_t)n0 * gj;
+            }
+            if (VISC) {
+                double Vx[4], Vy[4];
+                visc_at<CART, AX>(sh_uv, sh_T, s, code, m, q, g, Vx, Vy);
+#pragma unroll
+                for (int c = 1; c < 4; ++c) {
+                    Ix[c] -= Vx[c];
+                    Iy[c] -= Vy[c];
+                }
+            }
+            if (CART) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    fx[c] = m.cM[0] * Ix[c];
+                    fy[c] = m.cM[1] * Iy[c];
+                }
+            } else {
+                const double Mxx = __ldg(m.M + q), Mxy = __ldg(m.M + N + q);
+                const double Myx = __ldg(m.M + 2 * N + q), Myy = __ldg(m.M + 3 * N + q);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    fx[c] = Mxx * Ix[c] + Mxy * Iy[c];
+                    fy[c] = Myx * Ix[c] + Myy * Iy[c];
+                }
+            }
+        }
+        fh[t] = make_double2(fx[0], fx[1]);
+        fh[NF + t] = make_double2(fx[2], fx[3]);
+        fh[2 * NF + t] = make_double2(fy[0], fy[1]);
+        fh[3 * NF + t] = make_double2(fy[2], fy[3]);
+    }
+    __syncthreads();
+
+    // ---- phase C: divergence, SAT, epilogue ------------------------------------------
+    for (int t = tid; t < TX * TY; t += NT) {
+        const int a = t % TX, b = t / TX;
+        const int gi = i0 + a, gj = j0 + b;
+        if (gi >= n0 || gj >= n1) continue;
+        const int64_t p = gi + (int64_t)n0 * gj;
+        const int s = (b + H) * AX + (a + H);
+        const int f = (b + G3) * FX + (a + G3);
+        const unsigned code = sh_c[s];
+        // epilogue inputs first (streamed from HBM while the divergence is formed)
+        double yb[4] = {0, 0, 0, 0};
+        if (ep.y_out) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) yb[c] = __ldg(ep.base + c * N + p);
+#pragma unroll
+            for (int k = 0; k < 5; ++k)
+                if (k < ep.nsrc) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) yb[c] += ep.csrc[k] * __ldg(ep.src[k] + c * N + p);
+                }
+        }
+        double R[4] = {0, 0, 0, 0};
+        if (code) {
+            const int cx = code & 15, cy = (code >> 4) & 15;
+            double2 x01, x23, y01, y23;
+            if (cx == CLS_INT) {
+                x01 = d_int2(fh, f, 1);
+                x23 = d_int2(fh + NF, f, 1);
+            } else {
+                x01 = d_gen2(fh, f, 1, cx);
+                x23 = d_gen2(fh + NF, f, 1, cx);
+            }
+            if (cy == CLS_INT) {
+                y01 = d_int2(fh + 2 * NF, f, FX);
+                y23 = d_int2(fh + 3 * NF, f, FX);
+            } else {
+                y01 = d_gen2(fh + 2 * NF, f, FX, cy);
+                y23 = d_gen2(fh + 3 * NF, f, FX, cy);
+            }
+            const double Jp = CART ? m.cJ : __ldg(m.J + p);
+            R[0] = -Jp * (x01.x + y01.x);
+            R[1] = -Jp * (x01.y + y01.y);
+            R[2] = -Jp * (x23.x + y23.x);
+            R[3] = -Jp * (x23.y + y23.y);
+            // ---- SAT ----
+            if (cx == CLS_L0 || cx == CLS_R0 || cy == CLS_L0 || cy == CLS_R0) {
+                double q[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) q[c] = __ldg(Q + c * N + p);
+                double Vx[4] = {0, 0, 0, 0}, Vy[4] = {0, 0, 0, 0};
+                if (VISC) visc_at<CART, AX>(sh_uv, sh_T, s, code, m, p, g, Vx, Vy);
+                // donor data gathered by k_donor2d for this receiver
+                const int slot = m.recv_slot[p];
+                double qi[4] = {0, 0, 0, 0}, fvi[6] = {0, 0, 0, 0, 0, 0};
+                if (slot >= 0) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) qi[c] = m.qhat[c * m.nrecv + slot];
+                    if (VISC)
+#pragma unroll
+                        for (int c = 0; c < 6; ++c) fvi[c] = m.fvhat[c * m.nrecv + slot];
+                }
+                const int idx[2] = {gi, gj};
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    const int cl = k == 0 ? cx : cy;
+                    if (cl != CLS_L0 && cl != CLS_R0) continue;
+                    const int sidx = (cl == CLS_L0) ? 0 : 1;
+                    const double side = (cl == CLS_L0) ? 1.0 : -1.0;
+                    const bool at_face = !m.periodic[k] && (sidx == 0 ? idx[k] == 0 : idx[k] == m.n[k] - 1);
+                    const int typ = at_face ? m.face_bc[k][sidx] : MRAB_BC_OVERSET;
+                    double nv[2];
+                    if (CART) {
+                        nv[0] = k == 0 ? m.cJ * m.cM[0] : 0.0;
+                        nv[1] = k == 1 ? m.cJ * m.cM[1] : 0.0;
+                    } else {
+                        nv[0] = Jp * __ldg(m.M + (2 * k) * N + p);
+                        nv[1] = Jp * __ldg(m.M + (2 * k + 1) * N + p);
+                    }
+                    double qh[4];
+                    if (typ == MRAB_BC_OVERSET) {
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) qh[c] = qi[c];
+                    } else if (typ == MRAB_BC_FARFIELD) {
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) qh[c] = g.q_inf[c];
+                    } else {
+                        qh[0] = q[0];
+                        qh[1] = 0.0;
+                        qh[2] = 0.0;
+                        qh[3] = q[0] * g.wall_T * g.igamma * g.igm1;
+                    }
+                    double dq[4], kd[4];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) dq[c] = q[c] - qh[c];
+                    kchar2(q, nv, side, dq, g, kd);
+                    double sig1 = 0.0;
+                    if (VISC) sig1 = 0.5 * (nv[0] * nv[0] + nv[1] * nv[1]) * g.iRe;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) R[c] -= (0.5 * kd[c] + sig1 * dq[c]) / kP0;
+                    if (VISC && typ != MRAB_BC_WALL) {
+#pragma unroll
+                        for (int j = 0; j < 3; ++j) {
+                            const double fk = nv[0] * Vx[1 + j] + nv[1] * Vy[1 + j];
+                            double fhv = 0.0;
+                            if (typ == MRAB_BC_OVERSET) fhv = nv[0] * fvi[j] + nv[1] * fvi[3 + j];
+                            R[1 + j] += 0.5 * side * (fk - fhv) / kP0;
+                        }
+                    }
+                }
+            }
+        }
+        if (ep.r_out) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) ep.r_out[c * N + p] = R[c];
+        }
+        if (ep.y_out) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) ep.y_out[c * N + p] = yb[c] + ep.c_new * R[c];
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// donor kernel (2-D): state on the fly + viscous flux + Lagrange gather per receiver
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ double src_val(const SrcSet& ss, int h, int c, int64_t N, int64_t q) {
+    double v = __ldg(ss.base[h] + c * N + q);
+    const int ns = ss.nsrc[h];
+    for (int k = 0; k < ns; ++k) v += ss.c[h][k] * __ldg(ss.src[h][k] + c * N + q);
+    return v;
+}
+
+__device__ __forceinline__ void src_prim(const SrcSet& ss, int h, int64_t N, int64_t q,
+                                         const Gas& g, double& u, double& v, double& T) {
+    const double r = src_val(ss, h, 0, N, q), mu = src_val(ss, h, 1, N, q);
+    const double mv = src_val(ss, h, 2, N, q), E = src_val(ss, h, 3, N, q);
+    const double ir = 1.0 / r;
+    u = mu * ir;
+    v = mv * ir;
+    T = g.gamma * g.gm1 * (E - 0.5 * (mu * u + mv * v)) * ir;
+}
+
+template <bool VISC>
+__global__ void __launch_bounds__(128) k_donor2d(RecvTask rt, SrcSet ss, MeshTable mt, Gas g) {
+    const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 4;
+    const int a = threadIdx.x & 15;
+    int rm = 0;
+    while (rm < rt.nmesh - 1 && gid >= rt.off[rm + 1]) ++rm;
+    const bool live = gid < rt.off[rt.nmesh];
+    const int64_t r = gid - rt.off[rm];
+    double acc[10];
+#pragma unroll
+    for (int c = 0; c < 10; ++c) acc[c] = 0.0;
+    if (live) {
+        const int h = rt.rdonor[rm][r];
+        const DevMesh& m = mt.m[h];
+        const int n0 = m.n[0], n1 = m.n[1];
+        const int64_t N = m.npts;
+        int ii = rt.rbase[rm][3 * r] + (a & 3), jj = rt.rbase[rm][3 * r + 1] + (a >> 2);
+        if (ii >= n0) ii -= n0;
+        if (jj >= n1) jj -= n1;
+        const double* w = rt.rw[rm] + 12 * r;
+        const double W = w[a & 3] * w[4 + (a >> 2)];
+        const int64_t q = ii + (int64_t)n0 * jj;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[c] = W * src_val(ss, h, c, N, q);
+        if (VISC) {
+            const unsigned code = m.cls[q];
+            const int cl[2] = {(int)(code & 15), (int)((code >> 4) & 15)};
+            const int idx[2] = {ii, jj};
+            const int64_t stride[2] = {1, n0};
+            double d[2][3];   // d[k][u, v, T] along direction k
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                d[k][0] = d[k][1] = d[k][2] = 0.0;
+                const int ns = c_nst[cl[k]];
+                for (int t = 0; t < ns; ++t) {
+                    int o = idx[k] + c_off[cl[k]][t];
+                    const int nk = m.n[k];
+                    if (o < 0) o += nk; else if (o >= nk) o -= nk;
+                    const int64_t qq = q + (int64_t)(o - idx[k]) * stride[k];
+                    double u, v, T;
+                    src_prim(ss, h, N, qq, g, u, v, T);
+                    const double cf = c_cf[cl[k]][t];
+                    d[k][0] += cf * u;
+                    d[k][1] += cf * v;
+                    d[k][2] += cf * T;
+                }
+            }
+            double gx[3], gy[3];   // d/dx, d/dy of (u, v, T)
+            if (m.cart) {
+                const double sx = m.cJ * m.cM[0], sy = m.cJ * m.cM[1];
+#pragma unroll
+                for (int f = 0; f < 3; ++f) {
+                    gx[f] = sx * d[0][f];
+                    gy[f] = sy * d[1][f];
+                }
+            } else {
+                const double J = __ldg(m.J + q);
+                const double Mxx = __ldg(m.M + q), Mxy = __ldg(m.M + N + q);
+                const double Myx = __ldg(m.M + 2 * N + q), Myy = __ldg(m.M + 3 * N + q);
+#pragma unroll
+                for (int f = 0; f < 3; ++f) {
+                    gx[f] = J * (Mxx * d[0][f] + Myx * d[1][f]);
+                    gy[f] = J * (Mxy * d[0][f] + Myy * d[1][f]);
+                }
+            }
+            double u, v, T;
+            src_prim(ss, h, N, q, g, u, v, T);
+            const double div = gx[0] + gy[1];
+            const double txx = (2.0 * gx[0] - (2.0 / 3.0) * div) * g.iRe;
+            const double tyy = (2.0 * gy[1] - (2.0 / 3.0) * div) * g.iRe;
+            const double txy = (gy[0] + gx[1]) * g.iRe;
+            acc[4] = W * txx;
+            acc[5] = W * txy;
+            acc[6] = W * (u * txx + v * txy + g.kT * gx[2]);
+            acc[7] = W * txy;
+            acc[8] = W * tyy;
+            acc[9] = W * (u * txy + v * tyy + g.kT * gy[2]);
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < 10; ++c) {
+        double v = acc[c];
+        v += __shfl_xor_sync(0xffffffffu, v, 8);
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        acc[c] = v;
+    }
+    if (live && a == 0) {
+        const int64_t R = rt.nrecv[rm];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) rt.qhat[rm][c * R + r] = acc[c];
+        if (VISC)
+#pragma unroll
+            for (int c = 0; c < 6; ++c) rt.fvhat[rm][c * R + r] = acc[4 + c];
+    }
+}
+
+void launch_donor2d(const RecvTask& rt, const SrcSet& ss, const MeshTable& mt, const Gas& gas,
+                    cudaStream_t st) {
+    const int64_t tot = rt.off[rt.nmesh];
+    if (tot <= 0) return;
+    const unsigned nb = (unsigned)((tot * 16 + 127) / 128);
+    if (gas.viscous) k_donor2d<true><<<nb, 128, 0, st>>>(rt, ss, mt, gas);
+    else k_donor2d<false><<<nb, 128, 0, st>>>(rt, ss, mt, gas);
+}
+
+template <bool VISC, bool CART>
+static void launch_t(const DevMesh& m, const double* Q, const Gas& g, const Epilogue& ep,
+                     const DonorSet& ds, cudaStream_t st) {
+    static bool init = false;
+    const size_t bytes = Geo<VISC>::bytes;
+    if (!init) {
+        cudaFuncSetAttribute(k_rhs2d<VISC, CART>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        init = true;
+    }
+    dim3 grid((m.n[0] + TX - 1) / TX, (m.n[1] + TY - 1) / TY);
+    k_rhs2d<VISC, CART><<<grid, NT, bytes, st>>>(m, Q, g, ep, ds);
+}
+
+void launch_rhs2d(const DevMesh& m, const double* Q, const Gas& g, const Epilogue& ep,
+                  const DonorSet& ds, cudaStream_t st) {
+    if (g.viscous) {
+        if (m.cart) launch_t<true, true>(m, Q, g, ep, ds, st);
+        else launch_t<true, false>(m, Q, g, ep, ds, st);
+    } else {
+        if (m.cart) launch_t<false, true>(m, Q, g, ep, ds, st);
+        else launch_t<false, false>(m, Q, g, ep, ds, st);
+    }
+}
+
+}  // namespace mrab

@@ -203,12 +203,25 @@ static Box make_box(const int* lo, const int* hi) {
     return b;
 }
 
-// interpolation for the receivers of mesh g; state_of[d] = state array of donor d
-static void issue_interp(mrab_ctx* c, int g, const double* const* state_of) {
+static DonorSet make_ds(mrab_ctx* c, const double* const* state_of) {
+    const Plan& P = *c->P;
+    DonorSet ds{};
+    for (size_t h = 0; h < P.meshes.size(); ++h) {
+        ds.state[h] = state_of[h];
+        ds.fv[h] = c->md[h].FV;
+        for (int k = 0; k < 3; ++k) ds.n[h][k] = P.meshes[h].n[k];
+        ds.npts[h] = P.meshes[h].npts;
+    }
+    return ds;
+}
+
+// gather for the receivers of mesh g (3-D; the 2-D RHS kernel gathers inline);
+// state_of[d] = state array of donor d at the evaluation time
+static void issue_interp(mrab_ctx* c, int g, const double* const* state_of, bool force = false) {
     const Plan& P = *c->P;
     MeshDev& D = c->md[g];
     const MeshPlan& m = P.meshes[g];
-    if (m.rpoint.empty()) return;
+    if (m.rpoint.empty() || (P.dim == 2 && !force)) return;
     RecvList rl{};
     rl.n = (int64_t)m.rpoint.size();
     rl.point = D.rpoint;
@@ -217,15 +230,44 @@ static void issue_interp(mrab_ctx* c, int g, const double* const* state_of) {
     rl.w = D.rw;
     rl.qhat = D.qhat;
     rl.fvhat = D.fvhat;
-    DonorSet ds{};
-    for (size_t h = 0; h < P.meshes.size(); ++h) {
-        ds.state[h] = state_of[h];
-        ds.fv[h] = c->md[h].FV;
-        for (int k = 0; k < 3; ++k) ds.n[h][k] = P.meshes[h].n[k];
-        ds.npts[h] = P.meshes[h].npts;
-    }
-    launch_interp(P.dim, P.viscous, rl, ds, c->st);
+    launch_interp(P.dim, P.viscous, rl, make_ds(c, state_of), c->st);
     c->launch_counter++;
+}
+
+// 2-D: one launch gathers the donor data of every receiver of the meshes in `evaluating`;
+// donor states are formed on the fly from `ss`.
+static void issue_donor2d(mrab_ctx* c, const std::vector<int>& evaluating, const SrcSet& ss) {
+    const Plan& P = *c->P;
+    RecvTask rt{};
+    rt.nmesh = 0;
+    rt.off[0] = 0;
+    for (int g : evaluating) {
+        const MeshPlan& mp = P.meshes[g];
+        if (mp.rpoint.empty()) continue;
+        MeshDev& D = c->md[g];
+        const int k = rt.nmesh++;
+        rt.rdonor[k] = D.rdonor;
+        rt.rbase[k] = D.rbase;
+        rt.rw[k] = D.rw;
+        rt.qhat[k] = D.qhat;
+        rt.fvhat[k] = D.fvhat;
+        rt.nrecv[k] = (int64_t)mp.rpoint.size();
+        rt.off[k + 1] = rt.off[k] + rt.nrecv[k];
+    }
+    if (rt.nmesh == 0) return;
+    MeshTable mt{};
+    for (size_t h = 0; h < P.meshes.size(); ++h) mt.m[h] = c->md[h].dm;
+    launch_donor2d(rt, ss, mt, c->gas, c->st);
+    c->launch_counter++;
+}
+
+static SrcSet plain_states(mrab_ctx* c, const double* const* state_of) {
+    SrcSet ss{};
+    for (size_t h = 0; h < c->P->meshes.size(); ++h) {
+        ss.base[h] = state_of[h];
+        ss.nsrc[h] = 0;
+    }
+    return ss;
 }
 
 static void issue_visc(mrab_ctx* c, int g, const double* Q, const Box& box) {
@@ -235,8 +277,33 @@ static void issue_visc(mrab_ctx* c, int g, const double* Q, const Box& box) {
     c->launch_counter++;
 }
 
-static void issue_rhs(mrab_ctx* c, int g, const double* Q, const Epilogue& ep) {
-    launch_rhs(c->P->dim, c->md[g].dm, Q, c->md[g].FV, c->gas, ep, c->st);
+// viscous fluxes a stepping mesh must provide: the 3-D direct RHS kernel reads them on the
+// whole mesh; the 2-D tiled kernel computes its own, so only the donor box is needed there.
+static void issue_step_visc(mrab_ctx* c, int g, const double* Q) {
+    const Plan& P = *c->P;
+    const MeshPlan& mp = P.meshes[g];
+    if (P.dim == 3)
+        issue_visc(c, g, Q, whole_box(mp));
+    else if (mp.is_donor)
+        issue_visc(c, g, Q, make_box(mp.fv_lo, mp.fv_hi));
+}
+
+// every mesh evaluated at the given states (RK stages, the rhs hook): donor data for all
+static void issue_all_donors(mrab_ctx* c, const double* const* state_of) {
+    const int G = (int)c->P->meshes.size();
+    if (c->P->dim == 2) {
+        std::vector<int> all(G);
+        std::iota(all.begin(), all.end(), 0);
+        issue_donor2d(c, all, plain_states(c, state_of));
+        return;
+    }
+    for (int g = 0; g < G; ++g) issue_step_visc(c, g, state_of[g]);
+    for (int g = 0; g < G; ++g) issue_interp(c, g, state_of);
+}
+
+static void issue_rhs(mrab_ctx* c, int g, const double* Q, const Epilogue& ep,
+                      const double* const* state_of) {
+    launch_rhs(c->P->dim, c->md[g].dm, Q, c->md[g].FV, c->gas, ep, make_ds(c, state_of), c->st);
     c->launch_counter++;
 }
 
@@ -253,7 +320,38 @@ static void issue_macro_step(mrab_ctx* c) {
                 if (stepping[h] && P.donor_of[g][h]) partial[g] = 1;
         }
         std::vector<const double*> state_of(G, nullptr);
-        for (int g = 0; g < G; ++g) {
+        if (P.dim == 2) {
+            // donor states on the fly: stepping meshes at their current state, the others at
+            // base + h_g sum_k beta_k R_k (partial integral of the extrapolant)
+            SrcSet ss{};
+            std::vector<int> ev;
+            for (int g = 0; g < G; ++g) {
+                MeshDev& D = c->md[g];
+                if (stepping[g]) {
+                    if (c->book.pending[g]) {
+                        c->book.cur[g] ^= 1;
+                        c->book.pending[g] = 0;
+                    }
+                    ev.push_back(g);
+                }
+                ss.base[g] = D.Q[c->book.cur[g]];
+                state_of[g] = ss.base[g];
+                ss.nsrc[g] = 0;
+                if (!stepping[g] && partial[g]) {
+                    const MeshPlan& mp = P.meshes[g];
+                    const int jj = j % mp.s;
+                    const double hg = P.h * mp.s;
+                    ss.nsrc[g] = m;
+                    for (int k = 0; k < m; ++k) {
+                        int slot = ((c->book.head[g] - (m - 1) + k) % m + m) % m;   // oldest first
+                        ss.src[g][k] = D.ring[slot];
+                        ss.c[g][k] = hg * P.coef[g][jj][k];
+                    }
+                }
+            }
+            issue_donor2d(c, ev, ss);
+        }
+        for (int g = 0; g < G && P.dim == 3; ++g) {
             MeshDev& D = c->md[g];
             if (stepping[g]) {
                 if (c->book.pending[g]) {
@@ -262,7 +360,7 @@ static void issue_macro_step(mrab_ctx* c) {
                 }
                 const double* Q = D.Q[c->book.cur[g]];
                 state_of[g] = Q;
-                issue_visc(c, g, Q, whole_box(P.meshes[g]));
+                issue_step_visc(c, g, Q);
             } else if (partial[g]) {
                 const MeshPlan& mp = P.meshes[g];
                 const int jj = j % mp.s;
@@ -301,7 +399,7 @@ static void issue_macro_step(mrab_ctx* c) {
                 ep.src[k] = D.ring[slot];
                 ep.csrc[k] = hg * al[k];
             }
-            issue_rhs(c, g, D.Q[c->book.cur[g]], ep);
+            issue_rhs(c, g, D.Q[c->book.cur[g]], ep, state_of.data());
             c->book.head[g] = newslot;
             c->book.pending[g] = 1;
             c->evals[g]++;
@@ -354,9 +452,8 @@ static void issue_rk_step(mrab_ctx* c) {
         for (int g = 0; g < G; ++g) {
             MeshDev& D = c->md[g];
             state_of[g] = (s == 0) ? D.Q[c->book.cur[g]] : D.ystage;
-            issue_visc(c, g, state_of[g], whole_box(P.meshes[g]));
         }
-        for (int g = 0; g < G; ++g) issue_interp(c, g, state_of.data());
+        issue_all_donors(c, state_of.data());
         // every mesh reads its own stage state; the next stage state goes to a second
         // buffer (dstate) so that no mesh overwrites what another still gathers from.
         for (int g = 0; g < G; ++g) {
@@ -383,7 +480,7 @@ static void issue_rk_step(mrab_ctx* c) {
                         ep.csrc[ep.nsrc++] = P.h * b[jx];
                     }
             }
-            issue_rhs(c, g, state_of[g], ep);
+            issue_rhs(c, g, state_of[g], ep, state_of.data());
             c->evals[g]++;
         }
         if (s < ns - 1)
@@ -487,6 +584,11 @@ mrab_status mrab_create(const mrab_plan* plan, const double* const* q0, void* d_
     c->gas.wall_T = P.wall_T;
     c->gas.viscous = P.viscous;
     for (int k = 0; k < 5; ++k) c->gas.q_inf[k] = P.q_inf[k];
+    c->gas.iRe = 1.0 / c->gas.Re;
+    c->gas.kT = 1.0 / (c->gas.Re * P.Pr * (P.gamma - 1.0));
+    c->gas.gm1 = P.gamma - 1.0;
+    c->gas.igm1 = 1.0 / (P.gamma - 1.0);
+    c->gas.igamma = 1.0 / P.gamma;
     const int nc = P.nc, d = P.dim;
     for (int g = 0; g < G; ++g) {
         const MeshPlan& m = P.meshes[g];
@@ -530,6 +632,9 @@ mrab_status mrab_create(const mrab_plan* plan, const double* const* q0, void* d_
         dm.recv_slot = D.recv_slot;
         dm.qhat = D.qhat;
         dm.fvhat = D.fvhat;
+        dm.rdonor = D.rdonor;
+        dm.rbase = D.rbase;
+        dm.rw = D.rw;
         dm.nrecv = (int64_t)R;
         c->book.head[g] = P.history_m - 1;   // empty ring: the first push goes to slot 0
         c->book.cur[g] = 0;
@@ -644,12 +749,11 @@ mrab_status mrab_rhs(mrab_ctx* c, const double* const* q, double* const* rhs_out
         CK(cudaMemcpyAsync(c->md[g].ystage, q[g], bytes, cudaMemcpyDefault, c->st));
         state_of[g] = c->md[g].ystage;
     }
-    for (int g = 0; g < G; ++g) issue_visc(c, g, state_of[g], whole_box(P.meshes[g]));
-    for (int g = 0; g < G; ++g) issue_interp(c, g, state_of.data());
+    issue_all_donors(c, state_of.data());
     for (int g = 0; g < G; ++g) {
         Epilogue ep{};
         ep.r_out = c->md[g].kbuf[3];
-        issue_rhs(c, g, state_of[g], ep);
+        issue_rhs(c, g, state_of[g], ep, state_of.data());
     }
     CK(cudaGetLastError());
     for (int g = 0; g < G; ++g) {
@@ -691,7 +795,7 @@ mrab_status mrab_time_kernel(mrab_ctx* c, int kernel, int mesh, int reps, int fl
     CK(cudaStreamSynchronize(c->st));
     void* flush = nullptr;
     const size_t fbytes = (size_t)256 << 20;
-    if (flush_l2) CK(cudaMalloc(&flush, fbytes));
+    if (flush_l2) CK(cudaMalloc(&flush, 2 * fbytes));
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
@@ -701,7 +805,7 @@ mrab_status mrab_time_kernel(mrab_ctx* c, int kernel, int mesh, int reps, int fl
     double total = 0.0;
     double bytes = 0.0;
     for (int r = 0; r < reps; ++r) {
-        if (flush) CK(cudaMemsetAsync(flush, r & 0xff, fbytes, c->st));
+        if (flush) launch_l2_scrub(flush, (char*)flush + fbytes, fbytes, r, c->st);
         CK(cudaEventRecord(e0, c->st));
         if (kernel == 0) {
             Epilogue ep{};
@@ -714,15 +818,21 @@ mrab_status mrab_time_kernel(mrab_ctx* c, int kernel, int mesh, int reps, int fl
                 ep.src[k] = D.ring[k];
                 ep.csrc[k] = P.h * mp.s * P.coef[mesh][mp.s][k];
             }
-            launch_rhs(d, D.dm, Q, D.FV, c->gas, ep, c->st);
+            launch_rhs(d, D.dm, Q, D.FV, c->gas, ep, make_ds(c, state_of.data()), c->st);
             // Q read, R written, (m-1) ring reads, state written, metrics if curvilinear
             bytes = 8.0 * N * (nc * (m + 2) + (mp.cartesian ? 0 : 1 + d * d));
         } else if (kernel == 1) {
-            launch_visc(d, D.dm, Q, D.dstate == nullptr ? D.FV : D.FV, whole_box(mp), c->gas, c->st);
+            // the box the MRAB step uses: whole mesh (3-D), donor box (2-D)
+            Box b = (d == 3 || !mp.is_donor) ? whole_box(mp) : make_box(mp.fv_lo, mp.fv_hi);
+            launch_visc(d, D.dm, Q, D.FV, b, c->gas, c->st);
+            const double Nb = (double)(b.hi[0] - b.lo[0] + 1) * (b.hi[1] - b.lo[1] + 1) * (b.hi[2] - b.lo[2] + 1);
             // Q read, Cartesian viscous fluxes written, metrics if curvilinear
-            bytes = 8.0 * N * (nc + d * (d + 1) + (mp.cartesian ? 0 : 1 + d * d));
+            bytes = 8.0 * Nb * (nc + d * (d + 1) + (mp.cartesian ? 0 : 1 + d * d));
         } else {
-            issue_interp(c, mesh, state_of.data());
+            if (d == 2)
+                issue_donor2d(c, std::vector<int>{mesh}, plain_states(c, state_of.data()));
+            else
+                issue_interp(c, mesh, state_of.data(), true);
             const double R = (double)mp.rpoint.size();
             const int np = d == 2 ? 16 : 64;
             // per receiver: indices + weights in, nc (+ d(d+1)) gathered values out; the
