@@ -44,7 +44,13 @@ struct Epilogue {
     int nsrc;
     const double* src[8];
     double csrc[8];
+    // 2-D only: restrict the launch to a list of tiles (tile = ty * ntx + tx); NULL = all
+    const int32_t* tiles;
+    int ntiles;
 };
+
+// tile grid of the 2-D RHS kernel (for building tile lists on the host)
+void rhs2d_tile_shape(int* tx, int* ty);
 
 struct Box {
     int lo[3];
@@ -89,6 +95,11 @@ struct RecvTask {
     double* qhat[8];
     double* fvhat[8];
     int64_t nrecv[8];
+    int set[8];                     // which SrcSet (evaluation time) each entry reads
+};
+
+struct SrcSets {
+    SrcSet s[8];
 };
 
 struct MeshTable {
@@ -98,7 +109,7 @@ struct MeshTable {
 // 2-D donor kernel: for every receiver, 16 lanes (one per donor stencil point) form the donor
 // state on the fly, its Cartesian viscous flux from segmented D1 gradients, and
 // shuffle-reduce the Lagrange-weighted sums into qhat / fvhat.
-void launch_donor2d(const RecvTask& rt, const SrcSet& ss, const MeshTable& mt, const Gas& gas,
+void launch_donor2d(const RecvTask& rt, const SrcSets& ss, const MeshTable& mt, const Gas& gas,
                     cudaStream_t st);
 
 void launch_visc(int dim, const DevMesh& m, const double* Q, double* FV, const Box& box,

@@ -16,6 +16,8 @@
 // 16-byte shared load serves two fields.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "kernels.cuh"
 #include "mrab_internal.h"
 #include "stencil_table.cuh"
@@ -24,12 +26,12 @@ namespace mrab {
 
 namespace {
 
-constexpr int TX = 32, TY = 16, NT = 256;
+constexpr int TX = 32, NT = 256;
 constexpr int G3 = 3;
 constexpr double kP0 = 17.0 / 48.0;
 constexpr double C1 = 2.0 / 3.0, C2 = 1.0 / 12.0;
 
-template <bool VISC>
+template <bool VISC, int TY>
 struct Geo {
     static constexpr int H = VISC ? 6 : 3;
     static constexpr int AX = TX + 2 * H, AY = TY + 2 * H;
@@ -178,10 +180,10 @@ __device__ __forceinline__ void gather2(const DevMesh& m, const DonorSet& ds, in
 
 }  // namespace
 
-template <bool VISC, bool CART>
-__global__ void __launch_bounds__(NT, 2) k_rhs2d(DevMesh m, const double* __restrict__ Q, Gas g,
-                                                 Epilogue ep, DonorSet ds) {
-    using GG = Geo<VISC>;
+template <bool VISC, bool CART, int TY, int MINB, int NTH>
+__global__ void __launch_bounds__(NTH, MINB) k_rhs2d(DevMesh m, const double* __restrict__ Q, Gas g,
+                                                    Epilogue ep, DonorSet ds) {
+    using GG = Geo<VISC, TY>;
     constexpr int H = GG::H, AX = GG::AX, FX = GG::FX;
     constexpr int NA = GG::NA, NF = GG::NF;
     extern __shared__ __align__(16) double smem[];
@@ -193,17 +195,24 @@ __global__ void __launch_bounds__(NT, 2) k_rhs2d(DevMesh m, const double* __rest
 
     const int n0 = m.n[0], n1 = m.n[1];
     const int64_t N = m.npts;
-    const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
+    int bx = blockIdx.x, by = blockIdx.y;
+    if (ep.tiles) {
+        const int ntx = (m.n[0] + TX - 1) / TX;
+        const int tl = ep.tiles[blockIdx.x];
+        by = tl / ntx;
+        bx = tl - by * ntx;
+    }
+    const int i0 = bx * TX, j0 = by * TY;
     const int tid = threadIdx.x;
 
     // ---- phase A: primitives of tile + halo ------------------------------------------
-    constexpr int KA = (NA + NT - 1) / NT;
+    constexpr int KA = (NA + NTH - 1) / NTH;
     {
         double ld[KA][4];
         unsigned cd[KA];
 #pragma unroll
         for (int k = 0; k < KA; ++k) {
-            const int t = tid + k * NT;
+            const int t = tid + k * NTH;
             cd[k] = 0;
             ld[k][0] = 1.0;
             ld[k][1] = ld[k][2] = ld[k][3] = 0.0;
@@ -229,7 +238,7 @@ __global__ void __launch_bounds__(NT, 2) k_rhs2d(DevMesh m, const double* __rest
         }
 #pragma unroll
         for (int k = 0; k < KA; ++k) {
-            const int t = tid + k * NT;
+            const int t = tid + k * NTH;
             if (t >= NA) break;
             double r = 1.0, u = 0.0, v = 0.0, T = 0.0;
             if (cd[k]) {
@@ -248,7 +257,7 @@ __global__ void __launch_bounds__(NT, 2) k_rhs2d(DevMesh m, const double* __rest
     __syncthreads();
 
     // ---- phase B: contravariant fluxes at tile + 3 -----------------------------------
-    for (int t = tid; t < NF; t += NT) {
+    for (int t = tid; t < NF; t += NTH) {
         const int b = t / FX, a = t - b * FX;
         const int s = (b + H - G3) * AX + (a + H - G3);
         const unsigned code = sh_c[s];
@@ -301,7 +310,7 @@ __global__ void __launch_bounds__(NT, 2) k_rhs2d(DevMesh m, const double* __rest
     __syncthreads();
 
     // ---- phase C: divergence, SAT, epilogue ------------------------------------------
-    for (int t = tid; t < TX * TY; t += NT) {
+    for (int t = tid; t < TX * TY; t += NTH) {
         const int a = t % TX, b = t / TX;
         const int gi = i0 + a, gj = j0 + b;
         if (gi >= n0 || gj >= n1) continue;
@@ -312,14 +321,28 @@ __global__ void __launch_bounds__(NT, 2) k_rhs2d(DevMesh m, const double* __rest
         // epilogue inputs first (streamed from HBM while the divergence is formed)
         double yb[4] = {0, 0, 0, 0};
         if (ep.y_out) {
+            // all loads issued back to back (unused source slots re-read `base` with a zero
+            // weight, an L1 hit) so the history ring costs one memory round trip
+            const double* sp[4];
+            double cw[4];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) yb[c] = __ldg(ep.base + c * N + p);
+            for (int k = 0; k < 4; ++k) {
+                sp[k] = k < ep.nsrc ? ep.src[k] : ep.base;
+                cw[k] = k < ep.nsrc ? ep.csrc[k] : 0.0;
+            }
+            double v[5][4];
 #pragma unroll
-            for (int k = 0; k < 5; ++k)
-                if (k < ep.nsrc) {
+            for (int c = 0; c < 4; ++c) {
+                v[0][c] = __ldg(ep.base + c * N + p);
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) yb[c] += ep.csrc[k] * __ldg(ep.src[k] + c * N + p);
-                }
+                for (int k = 0; k < 4; ++k) v[1 + k][c] = __ldg(sp[k] + c * N + p);
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                yb[c] = v[0][c] + cw[0] * v[1][c] + cw[1] * v[2][c] + cw[2] * v[3][c] + cw[3] * v[4][c];
+            for (int k = 4; k < ep.nsrc; ++k)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) yb[c] += ep.csrc[k] * __ldg(ep.src[k] + c * N + p);
         }
         double R[4] = {0, 0, 0, 0};
         if (code) {
@@ -443,13 +466,14 @@ __device__ __forceinline__ void src_prim(const SrcSet& ss, int h, int64_t N, int
 }
 
 template <bool VISC>
-__global__ void __launch_bounds__(128) k_donor2d(RecvTask rt, SrcSet ss, MeshTable mt, Gas g) {
+__global__ void __launch_bounds__(128) k_donor2d(RecvTask rt, SrcSets sets, MeshTable mt, Gas g) {
     const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 4;
     const int a = threadIdx.x & 15;
     int rm = 0;
     while (rm < rt.nmesh - 1 && gid >= rt.off[rm + 1]) ++rm;
     const bool live = gid < rt.off[rt.nmesh];
     const int64_t r = gid - rt.off[rm];
+    const SrcSet& ss = sets.s[rt.set[rm]];
     double acc[10];
 #pragma unroll
     for (int c = 0; c < 10; ++c) acc[c] = 0.0;
@@ -540,7 +564,7 @@ __global__ void __launch_bounds__(128) k_donor2d(RecvTask rt, SrcSet ss, MeshTab
     }
 }
 
-void launch_donor2d(const RecvTask& rt, const SrcSet& ss, const MeshTable& mt, const Gas& gas,
+void launch_donor2d(const RecvTask& rt, const SrcSets& ss, const MeshTable& mt, const Gas& gas,
                     cudaStream_t st) {
     const int64_t tot = rt.off[rt.nmesh];
     if (tot <= 0) return;
@@ -549,27 +573,61 @@ void launch_donor2d(const RecvTask& rt, const SrcSet& ss, const MeshTable& mt, c
     else k_donor2d<false><<<nb, 128, 0, st>>>(rt, ss, mt, gas);
 }
 
-template <bool VISC, bool CART>
+template <bool VISC, bool CART, int TY, int MINB, int NTH>
 static void launch_t(const DevMesh& m, const double* Q, const Gas& g, const Epilogue& ep,
                      const DonorSet& ds, cudaStream_t st) {
     static bool init = false;
-    const size_t bytes = Geo<VISC>::bytes;
+    const size_t bytes = Geo<VISC, TY>::bytes;
     if (!init) {
-        cudaFuncSetAttribute(k_rhs2d<VISC, CART>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        cudaFuncSetAttribute(k_rhs2d<VISC, CART, TY, MINB, NTH>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
         init = true;
     }
     dim3 grid((m.n[0] + TX - 1) / TX, (m.n[1] + TY - 1) / TY);
-    k_rhs2d<VISC, CART><<<grid, NT, bytes, st>>>(m, Q, g, ep, ds);
+    if (ep.tiles) grid = dim3(ep.ntiles, 1);
+    if (grid.x * grid.y == 0) return;
+    k_rhs2d<VISC, CART, TY, MINB, NTH><<<grid, NTH, bytes, st>>>(m, Q, g, ep, ds);
+}
+
+// tile-shape variant (set once per process from MRAB_K2D, for tuning): 0 = 32x16 tile, 256
+// threads, 2 CTAs/SM (default); 1 = 32x8 / 256 / 2; 2 = 32x8 / 256 / 3; 3 = 32x16 / 512 / 1;
+// 4 = 32x32 / 512 / 1
+static int k2d_variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("MRAB_K2D");
+        v = e ? atoi(e) : 0;
+        if (v < 0 || v > 4) v = 0;
+    }
+    return v;
+}
+
+void rhs2d_tile_shape(int* tx, int* ty) {
+    *tx = TX;
+    const int v = k2d_variant();
+    *ty = (v == 0 || v == 3) ? 16 : (v == 4 ? 32 : 8);
+}
+
+template <bool VISC, bool CART>
+static void launch_v(const DevMesh& m, const double* Q, const Gas& g, const Epilogue& ep,
+                     const DonorSet& ds, cudaStream_t st) {
+    switch (k2d_variant()) {
+        case 1: launch_t<VISC, CART, 8, 2, 256>(m, Q, g, ep, ds, st); break;
+        case 2: launch_t<VISC, CART, 8, 3, 256>(m, Q, g, ep, ds, st); break;
+        case 3: launch_t<VISC, CART, 16, 1, 512>(m, Q, g, ep, ds, st); break;
+        case 4: launch_t<VISC, CART, 32, 1, 512>(m, Q, g, ep, ds, st); break;
+        default: launch_t<VISC, CART, 16, 2, 256>(m, Q, g, ep, ds, st); break;
+    }
 }
 
 void launch_rhs2d(const DevMesh& m, const double* Q, const Gas& g, const Epilogue& ep,
                   const DonorSet& ds, cudaStream_t st) {
     if (g.viscous) {
-        if (m.cart) launch_t<true, true>(m, Q, g, ep, ds, st);
-        else launch_t<true, false>(m, Q, g, ep, ds, st);
+        if (m.cart) launch_v<true, true>(m, Q, g, ep, ds, st);
+        else launch_v<true, false>(m, Q, g, ep, ds, st);
     } else {
-        if (m.cart) launch_t<false, true>(m, Q, g, ep, ds, st);
-        else launch_t<false, false>(m, Q, g, ep, ds, st);
+        if (m.cart) launch_v<false, true>(m, Q, g, ep, ds, st);
+        else launch_v<false, false>(m, Q, g, ep, ds, st);
     }
 }
 

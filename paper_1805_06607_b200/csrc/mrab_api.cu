@@ -58,8 +58,10 @@ struct MeshDev {
     int32_t* rdonor = nullptr;
     int32_t* rbase = nullptr;
     double* rw = nullptr;
-    double* qhat = nullptr;
-    double* fvhat = nullptr;
+    double* qhat = nullptr;       // [S][nc][R]: one set per micro index j (batched gathers)
+    double* fvhat = nullptr;      // [S][d(d+1)][R]
+    int32_t* tiles = nullptr;     // 2-D: critical tiles (cover the donor box) then the bulk
+    int ncrit = 0, nbulk = 0;
     DevMesh dm{};
 };
 
@@ -101,6 +103,11 @@ struct mrab_ctx {
     std::vector<std::vector<int64_t>> evals_per_phase;
     int64_t launches_last = 0;
     int64_t launch_counter = 0;
+    // 2-D multi-stream schedule: one stream per mesh (priority by rate) + a gather stream
+    cudaStream_t side[kMaxMeshes + 1] = {};
+    std::vector<cudaEvent_t> evpool;
+    size_t evnext = 0;
+    bool overlap = true;
 };
 
 // ----------------------------------------------------------------------------------------
@@ -167,8 +174,8 @@ static size_t plan_bytes(const Plan& P, bool dry, mrab_ctx* ctx, Bump* bump, boo
             void* b = take(Rm * sizeof(int32_t));
             void* c = take(Rm * 3 * sizeof(int32_t));
             void* e = take(Rm * 12 * sizeof(double));
-            void* f = take(Rm * nc * sizeof(double));
-            void* h = take(Rm * d * (d + 1) * sizeof(double));
+            void* f = take((size_t)P.S * Rm * nc * sizeof(double));
+            void* h = take((size_t)P.S * Rm * d * (d + 1) * sizeof(double));
             if (D) {
                 D->rpoint = (int64_t*)a;
                 D->rdonor = (int32_t*)b;
@@ -177,6 +184,13 @@ static size_t plan_bytes(const Plan& P, bool dry, mrab_ctx* ctx, Bump* bump, boo
                 D->qhat = (double*)f;
                 D->fvhat = (double*)h;
             }
+        }
+        if (d == 2) {
+            int tx, ty;
+            rhs2d_tile_shape(&tx, &ty);
+            const size_t nt = (size_t)((m.n[0] + tx - 1) / tx) * ((m.n[1] + ty - 1) / ty);
+            void* a = take(nt * sizeof(int32_t));
+            if (D) D->tiles = (int32_t*)a;
         }
     }
     return total + 1024;
@@ -236,29 +250,55 @@ static void issue_interp(mrab_ctx* c, int g, const double* const* state_of, bool
 
 // 2-D: one launch gathers the donor data of every receiver of the meshes in `evaluating`;
 // donor states are formed on the fly from `ss`.
-static void issue_donor2d(mrab_ctx* c, const std::vector<int>& evaluating, const SrcSet& ss) {
+static double* qhat_set(mrab_ctx* c, int g, int j) {
+    const MeshPlan& mp = c->P->meshes[g];
+    const size_t R = std::max<size_t>(mp.rpoint.size(), 1);
+    return c->md[g].qhat + (size_t)j * R * c->P->nc;
+}
+static double* fvhat_set(mrab_ctx* c, int g, int j) {
+    const MeshPlan& mp = c->P->meshes[g];
+    const size_t R = std::max<size_t>(mp.rpoint.size(), 1);
+    const int d = c->P->dim;
+    return c->md[g].fvhat + (size_t)j * R * d * (d + 1);
+}
+
+// one k_donor2d launch for the gather tasks (receiving mesh g, micro index j, state set)
+struct GatherTask {
+    int g, j, set;
+};
+static void issue_donor2d_tasks(mrab_ctx* c, const std::vector<GatherTask>& tasks,
+                                const SrcSets& sets, cudaStream_t st) {
     const Plan& P = *c->P;
     RecvTask rt{};
     rt.nmesh = 0;
     rt.off[0] = 0;
-    for (int g : evaluating) {
-        const MeshPlan& mp = P.meshes[g];
+    for (const GatherTask& t : tasks) {
+        const MeshPlan& mp = P.meshes[t.g];
         if (mp.rpoint.empty()) continue;
-        MeshDev& D = c->md[g];
+        MeshDev& D = c->md[t.g];
         const int k = rt.nmesh++;
         rt.rdonor[k] = D.rdonor;
         rt.rbase[k] = D.rbase;
         rt.rw[k] = D.rw;
-        rt.qhat[k] = D.qhat;
-        rt.fvhat[k] = D.fvhat;
+        rt.qhat[k] = qhat_set(c, t.g, t.j);
+        rt.fvhat[k] = fvhat_set(c, t.g, t.j);
         rt.nrecv[k] = (int64_t)mp.rpoint.size();
+        rt.set[k] = t.set;
         rt.off[k + 1] = rt.off[k] + rt.nrecv[k];
     }
     if (rt.nmesh == 0) return;
     MeshTable mt{};
     for (size_t h = 0; h < P.meshes.size(); ++h) mt.m[h] = c->md[h].dm;
-    launch_donor2d(rt, ss, mt, c->gas, c->st);
+    launch_donor2d(rt, sets, mt, c->gas, st);
     c->launch_counter++;
+}
+
+static void issue_donor2d(mrab_ctx* c, const std::vector<int>& evaluating, const SrcSet& ss) {
+    std::vector<GatherTask> tasks;
+    for (int g : evaluating) tasks.push_back({g, 0, 0});
+    SrcSets sets{};
+    sets.s[0] = ss;
+    issue_donor2d_tasks(c, tasks, sets, c->st);
 }
 
 static SrcSet plain_states(mrab_ctx* c, const double* const* state_of) {
@@ -308,8 +348,14 @@ static void issue_rhs(mrab_ctx* c, int g, const double* Q, const Epilogue& ep,
 }
 
 // one MRAB macro step (host bookkeeping + launches)
+static void issue_macro_step_dag2d(mrab_ctx* c);
+
 static void issue_macro_step(mrab_ctx* c) {
     const Plan& P = *c->P;
+    if (P.dim == 2) {
+        issue_macro_step_dag2d(c);
+        return;
+    }
     const int G = (int)P.meshes.size(), m = P.history_m;
     for (int j = 0; j < P.S; ++j) {
         std::vector<int> stepping(G, 0), partial(G, 0);
@@ -404,6 +450,215 @@ static void issue_macro_step(mrab_ctx* c) {
             c->book.pending[g] = 1;
             c->evals[g]++;
         }
+    }
+}
+
+// ----------------------------------------------------------------------------------------
+// 2-D macro step as a multi-stream DAG (captured into the phase graph).
+//
+// Nodes: gather launches (k_donor2d, possibly batching several micro indices) and RHS
+// launches (k_rhs2d, one per stepping mesh and micro index; a mesh whose intermediate states
+// are read later in the step is split into the tiles covering its donor box -- "critical" --
+// and the bulk, so the fast substeps only wait for the critical tiles while the bulk overlaps
+// them: the single-GPU analogue of the paper's interleaved communication).
+// Times are micro indices relative to the macro step start.
+// ----------------------------------------------------------------------------------------
+static cudaEvent_t dag_event(mrab_ctx* c) {
+    if (c->evnext == c->evpool.size()) {
+        cudaEvent_t e;
+        cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        c->evpool.push_back(e);
+    }
+    return c->evpool[c->evnext++];
+}
+
+struct DagNode {
+    int stream = -1;
+    cudaEvent_t ev = nullptr;
+};
+
+static void dag_wait(mrab_ctx* c, int s, const DagNode& d) {
+    if (d.ev && d.stream != s) cudaStreamWaitEvent(c->side[s], d.ev, 0);
+}
+static DagNode dag_done(mrab_ctx* c, int s) {
+    DagNode n;
+    n.stream = s;
+    n.ev = dag_event(c);
+    cudaEventRecord(n.ev, c->side[s]);
+    return n;
+}
+
+static void issue_macro_step_dag2d(mrab_ctx* c) {
+    const Plan& P = *c->P;
+    const int G = (int)P.meshes.size(), m = P.history_m, S = P.S;
+    const int GS = G;                       // index of the gather stream
+    c->evnext = 0;
+    // fork
+    {
+        cudaEvent_t e = dag_event(c);
+        cudaEventRecord(e, c->st);
+        for (int s = 0; s <= G; ++s) cudaStreamWaitEvent(c->side[s], e, 0);
+    }
+    // per mesh: which buffer holds which time, ring newest time
+    int tq[kMaxMeshes][2], tring[kMaxMeshes];
+    for (int g = 0; g < G; ++g) {
+        const int sg = P.meshes[g].s;
+        const int cur = c->book.cur[g];
+        // at a macro boundary every mesh has a pending state (its last RHS was at -s_g)
+        tq[g][cur] = -sg;
+        tq[g][cur ^ 1] = 0;
+        tring[g] = -sg;
+    }
+    auto buf_at = [&](int g, int t) -> int {
+        if (tq[g][0] == t) return 0;
+        if (tq[g][1] == t) return 1;
+        return -1;
+    };
+    auto steps_at = [&](int g, int j) { return j % P.meshes[g].s == 0; };
+    // does mesh h's intermediate state get read after micro index j in this step?
+    auto partial_read_after = [&](int h, int j) {
+        for (int jj = j + 1; jj < S; ++jj) {
+            if (steps_at(h, jj)) break;
+            for (int g = 0; g < G; ++g)
+                if (steps_at(g, jj) && P.donor_of[h][g]) return true;
+        }
+        return false;
+    };
+    std::vector<DagNode> last_full(G), last_crit(G);
+    std::vector<std::vector<DagNode>> readers(G);     // gather nodes that read mesh h
+    std::vector<std::vector<int>> emitted(G, std::vector<int>(S, 0));
+    std::vector<std::vector<DagNode>> gnode(G, std::vector<DagNode>(S));
+    for (int j = 0; j < S; ++j) {
+        // ---- gathers: all tasks (g, jj >= j) whose producers are already emitted ----
+        std::vector<GatherTask> tasks;
+        SrcSets sets{};
+        int nsets = 0;
+        std::vector<DagNode> deps;
+        std::vector<int> readmesh(G, 0);
+        for (int jj = j; jj < S; ++jj) {
+            bool any = false;
+            for (int g = 0; g < G; ++g) any = any || (steps_at(g, jj) && !emitted[g][jj]);
+            if (!any) continue;
+            // readiness of every donor of the meshes stepping at jj
+            bool ready = true;
+            for (int h = 0; h < G && ready; ++h) {
+                bool needed = false;
+                for (int g = 0; g < G; ++g) needed = needed || (steps_at(g, jj) && P.donor_of[h][g] && g != h);
+                if (!needed) continue;
+                if (steps_at(h, jj)) {
+                    ready = buf_at(h, jj) >= 0 && (jj - P.meshes[h].s < j);
+                } else {
+                    const int th = jj - jj % P.meshes[h].s;
+                    ready = th < j && tring[h] == th;
+                }
+            }
+            if (!ready) {
+                if (jj == j) ready = true;   // cannot happen (producers of j precede j)
+                else continue;
+            }
+            if (nsets == 8) break;
+            SrcSet& ss = sets.s[nsets];
+            for (int h = 0; h < G; ++h) {
+                ss.nsrc[h] = 0;
+                if (steps_at(h, jj)) {
+                    int b = buf_at(h, jj);
+                    ss.base[h] = c->md[h].Q[b < 0 ? 0 : b];
+                } else {
+                    const MeshPlan& mh = P.meshes[h];
+                    const int th = jj - jj % mh.s;
+                    int b = buf_at(h, th);
+                    ss.base[h] = c->md[h].Q[b < 0 ? 0 : b];
+                    const double hg = P.h * mh.s;
+                    ss.nsrc[h] = m;
+                    for (int k = 0; k < m; ++k) {
+                        int slot = ((c->book.head[h] - (m - 1) + k) % m + m) % m;
+                        ss.src[h][k] = c->md[h].ring[slot];
+                        ss.c[h][k] = hg * P.coef[h][jj % mh.s][k];
+                    }
+                }
+            }
+            for (int g = 0; g < G; ++g) {
+                if (!steps_at(g, jj) || emitted[g][jj]) continue;
+                tasks.push_back({g, jj, nsets});
+                emitted[g][jj] = 1;
+                for (int h = 0; h < G; ++h) {
+                    if (!P.donor_of[h][g] || h == g) continue;
+                    readmesh[h] = 1;
+                    deps.push_back(steps_at(h, jj) ? last_full[h] : last_crit[h]);
+                }
+            }
+            nsets++;
+        }
+        DagNode gn;
+        if (!tasks.empty()) {
+            for (auto& d : deps) dag_wait(c, GS, d);
+            issue_donor2d_tasks(c, tasks, sets, c->side[GS]);
+            gn = dag_done(c, GS);
+            for (auto& t : tasks) gnode[t.g][t.j] = gn;
+            for (int h = 0; h < G; ++h)
+                if (readmesh[h]) readers[h].push_back(gn);
+        }
+        // ---- RHS + AB update of the meshes stepping at j ----
+        for (int g = 0; g < G; ++g) {
+            if (!steps_at(g, j)) continue;
+            MeshDev& D = c->md[g];
+            const MeshPlan& mp = P.meshes[g];
+            if (c->book.pending[g]) {
+                c->book.cur[g] ^= 1;
+                c->book.pending[g] = 0;
+            }
+            dag_wait(c, g, gnode[g][j]);
+            for (auto& r : readers[g]) dag_wait(c, g, r);     // WAR on ring slot / state buffer
+            const double hg = P.h * mp.s;
+            const int newslot = (c->book.head[g] + 1) % m;
+            Epilogue ep{};
+            ep.r_out = D.ring[newslot];
+            ep.y_out = D.Q[c->book.cur[g] ^ 1];
+            ep.base = D.Q[c->book.cur[g]];
+            const std::vector<double>& al = P.coef[g][mp.s];
+            ep.c_new = hg * al[m - 1];
+            ep.nsrc = m - 1;
+            for (int k = 0; k < m - 1; ++k) {
+                int slot = ((c->book.head[g] - (m - 2) + k) % m + m) % m;
+                ep.src[k] = D.ring[slot];
+                ep.csrc[k] = hg * al[k];
+            }
+            DevMesh dm = D.dm;
+            dm.qhat = qhat_set(c, g, j);
+            dm.fvhat = fvhat_set(c, g, j);
+            const DonorSet ds{};
+            const bool split = c->overlap && D.ncrit > 0 && D.nbulk > 0 && partial_read_after(g, j);
+            if (split) {
+                Epilogue e1 = ep;
+                e1.tiles = D.tiles;
+                e1.ntiles = D.ncrit;
+                launch_rhs(2, dm, ep.base, D.FV, c->gas, e1, ds, c->side[g]);
+                last_crit[g] = dag_done(c, g);
+                Epilogue e2 = ep;
+                e2.tiles = D.tiles + D.ncrit;
+                e2.ntiles = D.nbulk;
+                launch_rhs(2, dm, ep.base, D.FV, c->gas, e2, ds, c->side[g]);
+                c->launch_counter += 2;
+                last_full[g] = dag_done(c, g);
+            } else {
+                launch_rhs(2, dm, ep.base, D.FV, c->gas, ep, ds, c->side[g]);
+                c->launch_counter++;
+                last_full[g] = dag_done(c, g);
+                last_crit[g] = last_full[g];
+            }
+            readers[g].clear();
+            c->book.head[g] = newslot;
+            c->book.pending[g] = 1;
+            c->evals[g]++;
+            tring[g] = j;
+            tq[g][c->book.cur[g] ^ 1] = j + mp.s;
+        }
+    }
+    // join
+    for (int s = 0; s <= G; ++s) {
+        cudaEvent_t e = dag_event(c);
+        cudaEventRecord(e, c->side[s]);
+        cudaStreamWaitEvent(c->st, e, 0);
     }
 }
 
@@ -576,6 +831,22 @@ mrab_status mrab_create(const mrab_plan* plan, const double* const* q0, void* d_
     plan_bytes(P, false, c.get(), &bump, &ok);
     if (!ok) return fail(MRAB_E_WORKSPACE, "workspace too small (layout)");
     CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    {
+        // side streams: the gather stream and the fastest meshes get the highest priority
+        int least = 0, greatest = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        int smin = P.S;
+        for (auto& mp : P.meshes) smin = std::min(smin, mp.s);
+        for (int g = 0; g < (int)P.meshes.size(); ++g) {
+            const int prio = P.meshes[g].s == smin ? greatest : least;
+            CK(cudaStreamCreateWithPriority(&c->side[g], cudaStreamNonBlocking, prio));
+        }
+        CK(cudaStreamCreateWithPriority(&c->side[P.meshes.size()], cudaStreamNonBlocking, greatest));
+        const char* ov = getenv("MRAB_OVERLAP");
+        // the critical/bulk split is off by default: measured slower on config 3 (the bulk
+        // tiles occupy every SM and delay the fast substeps); MRAB_OVERLAP=1 enables it
+        c->overlap = ov && ov[0] == '1';
+    }
     CK(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
     c->gas.gamma = P.gamma;
@@ -635,6 +906,25 @@ mrab_status mrab_create(const mrab_plan* plan, const double* const* q0, void* d_
         dm.rdonor = D.rdonor;
         dm.rbase = D.rbase;
         dm.rw = D.rw;
+        if (d == 2) {
+            // tile lists: tiles meeting the donor state box first (critical), then the rest
+            int tx, ty;
+            rhs2d_tile_shape(&tx, &ty);
+            const int ntx = (m.n[0] + tx - 1) / tx, nty = (m.n[1] + ty - 1) / ty;
+            std::vector<int32_t> crit, bulk;
+            for (int by = 0; by < nty; ++by)
+                for (int bx = 0; bx < ntx; ++bx) {
+                    const int t = by * ntx + bx;
+                    const bool meets = m.is_donor && bx * tx <= m.st_hi[0] &&
+                                       bx * tx + tx - 1 >= m.st_lo[0] && by * ty <= m.st_hi[1] &&
+                                       by * ty + ty - 1 >= m.st_lo[1];
+                    (meets ? crit : bulk).push_back(t);
+                }
+            D.ncrit = (int)crit.size();
+            D.nbulk = (int)bulk.size();
+            crit.insert(crit.end(), bulk.begin(), bulk.end());
+            CK(cudaMemcpy(D.tiles, crit.data(), crit.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        }
         dm.nrecv = (int64_t)R;
         c->book.head[g] = P.history_m - 1;   // empty ring: the first push goes to slot 0
         c->book.cur[g] = 0;
@@ -663,6 +953,9 @@ void mrab_destroy(mrab_ctx* c) {
     cudaStreamSynchronize(c->st);
     for (auto& g : c->graphs)
         if (g) cudaGraphExecDestroy(g);
+    for (auto& s : c->side)
+        if (s) cudaStreamDestroy(s);
+    for (auto& e : c->evpool) cudaEventDestroy(e);
     if (c->ev_in) cudaEventDestroy(c->ev_in);
     if (c->ev_out) cudaEventDestroy(c->ev_out);
     if (c->st) cudaStreamDestroy(c->st);

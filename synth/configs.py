@@ -282,18 +282,18 @@ def _config5_velocity(meshes, coarse, rng, nmodes=32, rms=1e-3):
     phases = rng.uniform(0.0, 2 * math.pi, size=(nmodes, 3))
 
     def raw(mesh):
-        out = []
-        for c in range(3):
-            acc = np.zeros(mesh.xyz.shape[1:])
-            for mi in range(nmodes):
-                arg = math.pi * sum(ks[mi, a] * (mesh.xyz[a] + 1.0) for a in range(3))
-                acc += np.cos(arg + phases[mi, c])
-            out.append(acc)
-        return out
+        # sum_m cos(pi k_m.(x+1) + phi_mc) = Re sum_m exp(i pi k_m.(x+1)) exp(i phi_mc)
+        acc = [np.zeros(mesh.xyz.shape[1:]) for _ in range(3)]
+        for mi in range(nmodes):
+            arg = math.pi * sum(ks[mi, a] * (mesh.xyz[a] + 1.0) for a in range(3))
+            E = np.exp(1j * arg)
+            for c in range(3):
+                acc[c] += (E * complex(math.cos(phases[mi, c]), math.sin(phases[mi, c]))).real
+        return acc
 
     rc = raw(coarse)
     amps = [rms / math.sqrt(float(np.mean(rc[c] ** 2))) for c in range(3)]
-    return [[amps[c] * r for c, r in enumerate(raw(m))] for m in meshes]
+    return [[amps[c] * r for c, r in enumerate(rc if m is coarse else raw(m))] for m in meshes]
 
 
 def config5(scale="full", order_n=4, history_m=None, sr=None, n_macro=None):
