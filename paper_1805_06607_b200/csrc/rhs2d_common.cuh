@@ -1,0 +1,114 @@
+// Shared device helpers of the 2-D RHS kernels (k_rhs2d, k_rhs2d_tma): SBP 2-4 stencils on
+// shared-memory rows, the characteristic SAT penalty and the Cartesian viscous fluxes.
+#pragma once
+#include "kernels.cuh"
+#include "mrab_internal.h"
+#include "stencil_table.cuh"
+
+namespace mrab {
+namespace k2d {
+
+constexpr double C1 = 2.0 / 3.0, C2 = 1.0 / 12.0;
+
+static __device__ __forceinline__ double d_int(const double* f, int s, int st) {
+    return C1 * (f[s + st] - f[s - st]) - C2 * (f[s + 2 * st] - f[s - 2 * st]);
+}
+static __device__ __forceinline__ double2 d_int2(const double2* f, int s, int st) {
+    const double2 a = f[s + st], b = f[s - st], c = f[s + 2 * st], d = f[s - 2 * st];
+    return make_double2(C1 * (a.x - b.x) - C2 * (c.x - d.x), C1 * (a.y - b.y) - C2 * (c.y - d.y));
+}
+static __device__ __forceinline__ double d_gen(const double* f, int s, int st, int cl) {
+    double acc = 0.0;
+    const int n = c_nst[cl];
+    for (int t = 0; t < n; ++t) acc += c_cf[cl][t] * f[s + c_off[cl][t] * st];
+    return acc;
+}
+static __device__ __forceinline__ double2 d_gen2(const double2* f, int s, int st, int cl) {
+    double2 acc = make_double2(0.0, 0.0);
+    const int n = c_nst[cl];
+    for (int t = 0; t < n; ++t) {
+        const double c = c_cf[cl][t];
+        const double2 v = f[s + c_off[cl][t] * st];
+        acc.x += c * v.x;
+        acc.y += c * v.y;
+    }
+    return acc;
+}
+
+// characteristic SAT penalty (same algebra as kernels.cu kchar<2>)
+static __device__ __forceinline__ void kchar2(const double* q, const double* n, double side,
+                                       const double* dq, const Gas& g, double* out) {
+    const double rho = q[0];
+    const double u0 = q[1] / rho, u1 = q[2] / rho;
+    const double ke = u0 * u0 + u1 * u1;
+    const double p = g.gm1 * (q[3] - 0.5 * rho * ke);
+    const double c2 = g.gamma * p / rho, c = sqrt(c2);
+    const double H = (q[3] + p) / rho;
+    const double nn = sqrt(n[0] * n[0] + n[1] * n[1]);
+    const double n0 = n[0] / nn, n1 = n[1] / nn;
+    const double un = u0 * n0 + u1 * n1;
+    const double du0 = (dq[1] - u0 * dq[0]) / rho, du1 = (dq[2] - u1 * dq[0]) / rho;
+    const double dp = g.gm1 * (dq[3] - (u0 * dq[1] + u1 * dq[2]) + 0.5 * ke * dq[0]);
+    const double dun = du0 * n0 + du1 * n1;
+    const double ap = (dp + rho * c * dun) / (2.0 * c2);
+    const double am = (dp - rho * c * dun) / (2.0 * c2);
+    const double a0 = dq[0] - dp / c2;
+    const double l0 = fmax(side * un * nn, 0.0);
+    const double lp = fmax(side * (un + c) * nn, 0.0);
+    const double lm = fmax(side * (un - c) * nn, 0.0);
+    const double dt0 = du0 - dun * n0, dt1 = du1 - dun * n1;
+    const double wp = lp * ap, wm = lm * am, w0 = l0 * a0;
+    out[0] = wp + wm + w0;
+    out[1] = wp * (u0 + c * n0) + wm * (u0 - c * n0) + w0 * u0 + l0 * rho * dt0;
+    out[2] = wp * (u1 + c * n1) + wm * (u1 - c * n1) + w0 * u1 + l0 * rho * dt1;
+    out[3] = wp * (H + c * un) + wm * (H - c * un) + w0 * (0.5 * ke) + l0 * rho * (u0 * dt0 + u1 * dt1);
+}
+
+// Cartesian viscous fluxes at shared point s (prim index) with class code `code`
+template <bool CART, int AX>
+static __device__ __forceinline__ void visc_at(const double2* __restrict__ sh_uv, const double* __restrict__ sh_T,
+                                        int s, unsigned code, const DevMesh& m, int64_t p,
+                                        const Gas& g, double* Fx, double* Fy) {
+    const int cx = code & 15, cy = (code >> 4) & 15;
+    double2 uvx, uvy;
+    double Tx, Ty;
+    if (cx == CLS_INT) {
+        uvx = d_int2(sh_uv, s, 1);
+        Tx = d_int(sh_T, s, 1);
+    } else {
+        uvx = d_gen2(sh_uv, s, 1, cx);
+        Tx = d_gen(sh_T, s, 1, cx);
+    }
+    if (cy == CLS_INT) {
+        uvy = d_int2(sh_uv, s, AX);
+        Ty = d_int(sh_T, s, AX);
+    } else {
+        uvy = d_gen2(sh_uv, s, AX, cy);
+        Ty = d_gen(sh_T, s, AX, cy);
+    }
+    double dudx, dudy, dvdx, dvdy, dTdx, dTdy;
+    if (CART) {
+        const double sx = m.cJ * m.cM[0], sy = m.cJ * m.cM[1];
+        dudx = sx * uvx.x; dvdx = sx * uvx.y; dTdx = sx * Tx;
+        dudy = sy * uvy.x; dvdy = sy * uvy.y; dTdy = sy * Ty;
+    } else {
+        const int64_t N = m.npts;
+        const double J = __ldg(m.J + p);
+        const double Mxx = __ldg(m.M + p), Mxy = __ldg(m.M + N + p);
+        const double Myx = __ldg(m.M + 2 * N + p), Myy = __ldg(m.M + 3 * N + p);
+        dudx = J * (Mxx * uvx.x + Myx * uvy.x); dudy = J * (Mxy * uvx.x + Myy * uvy.x);
+        dvdx = J * (Mxx * uvx.y + Myx * uvy.y); dvdy = J * (Mxy * uvx.y + Myy * uvy.y);
+        dTdx = J * (Mxx * Tx + Myx * Ty); dTdy = J * (Mxy * Tx + Myy * Ty);
+    }
+    const double div = dudx + dvdy;
+    const double txx = (2.0 * dudx - (2.0 / 3.0) * div) * g.iRe;
+    const double tyy = (2.0 * dvdy - (2.0 / 3.0) * div) * g.iRe;
+    const double txy = (dudy + dvdx) * g.iRe;
+    const double2 uv = sh_uv[s];
+    Fx[0] = 0.0; Fx[1] = txx; Fx[2] = txy; Fx[3] = uv.x * txx + uv.y * txy + g.kT * dTdx;
+    Fy[0] = 0.0; Fy[1] = txy; Fy[2] = tyy; Fy[3] = uv.x * txy + uv.y * tyy + g.kT * dTdy;
+}
+
+
+}  // namespace k2d
+}  // namespace mrab
