@@ -246,6 +246,12 @@ static void d1_host(const MeshPlan& m, int k, const double* f, double jump, cons
     }
 }
 
+// A mesh whose computed metric terms are constant and diagonal to this relative tolerance is
+// treated as Cartesian (constants instead of per-point arrays).  The Thomas-Lombard products
+// of 3-D coordinates carry ~5e-12 relative rounding at 256^3; the constants then differ from
+// the computed arrays by less than that, far inside the 1e-10 parity bar.
+static const double kCartTol = 1e-10;
+
 static bool compute_metrics(MeshPlan& m, Error& err) {
     const int d = m.dim;
     const int64_t N = m.npts;
@@ -303,12 +309,12 @@ static bool compute_metrics(MeshPlan& m, Error& err) {
         for (int k = 0; k < d; ++k) md[k] = Mp(k, k)[first];
         for (int64_t p = 0; p < N && m.cartesian; ++p) {
             if (!m.active[p]) continue;
-            if (std::fabs(m.jinv[p] - j0) > 1e-12 * std::fabs(j0)) m.cartesian = false;
+            if (std::fabs(m.jinv[p] - j0) > kCartTol * std::fabs(j0)) m.cartesian = false;
             for (int k = 0; k < d && m.cartesian; ++k)
                 for (int i = 0; i < d; ++i) {
                     double v = Mp(k, i)[p];
                     double e = (k == i) ? md[k] : 0.0;
-                    if (std::fabs(v - e) > 1e-12 * std::fabs(md[k])) {
+                    if (std::fabs(v - e) > kCartTol * std::fabs(md[k])) {
                         m.cartesian = false;
                         break;
                     }

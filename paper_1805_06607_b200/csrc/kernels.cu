@@ -178,6 +178,71 @@ __device__ __forceinline__ void kchar(const double* q, const double* n, double s
     out[D + 1] = wp * (H + c * un) + wm * (H - c * un) + w0 * (0.5 * ke) + l0 * rho * udt;
 }
 
+// SAT penalties at one point (eq:int P:279-299; edges/corners sum over flagged directions,
+// P:292-294), added to R.  Shared by the direct and the tiled 3-D RHS kernels.
+template <int D, bool VISC, bool CART>
+__device__ __forceinline__ void sat_point(const DevMesh& m, const double* __restrict__ Q,
+                                          const double* __restrict__ FV, const Gas& g, int64_t p,
+                                          const int* idx, unsigned code, double Jp, double* R) {
+    constexpr int NC = D + 2;
+    const int64_t N = m.npts;
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            const int cl = (code >> (4 * k)) & 15;
+            if (cl != CLS_L0 && cl != CLS_R0) continue;
+            const int sidx = (cl == CLS_L0) ? 0 : 1;
+            const double side = (cl == CLS_L0) ? 1.0 : -1.0;
+            const bool at_face = !m.periodic[k] && (sidx == 0 ? idx[k] == 0 : idx[k] == m.n[k] - 1);
+            const int typ = at_face ? m.face_bc[k][sidx] : MRAB_BC_OVERSET;
+            double q[NC], qh[NC], dq[NC], nv[D];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) q[c] = __ldg(Q + c * N + p);
+#pragma unroll
+            for (int i = 0; i < D; ++i)
+                nv[i] = CART ? (i == k ? m.cJ * m.cM[k] : 0.0) : Jp * __ldg(m.M + (k * D + i) * N + p);
+            int slot = -1;
+            if (typ == MRAB_BC_OVERSET) {
+                slot = m.recv_slot[p];
+#pragma unroll
+                for (int c = 0; c < NC; ++c) qh[c] = m.qhat[c * m.nrecv + slot];
+            } else if (typ == MRAB_BC_FARFIELD) {
+#pragma unroll
+                for (int c = 0; c < NC; ++c) qh[c] = g.q_inf[c];
+            } else {   // isothermal no-slip wall
+                qh[0] = q[0];
+#pragma unroll
+                for (int i = 0; i < D; ++i) qh[1 + i] = 0.0;
+                qh[D + 1] = q[0] * g.wall_T / (g.gamma * (g.gamma - 1.0));
+            }
+#pragma unroll
+            for (int c = 0; c < NC; ++c) dq[c] = q[c] - qh[c];
+            double kd[NC];
+            kchar<D>(q, nv, side, dq, g.gamma, kd);
+            double sig1 = 0.0;
+            if (VISC) {
+#pragma unroll
+                for (int i = 0; i < D; ++i) sig1 += nv[i] * nv[i];
+                sig1 *= 0.5 / g.Re;
+            }
+#pragma unroll
+            for (int c = 0; c < NC; ++c) R[c] -= (0.5 * kd[c] + sig1 * dq[c]) / kP0;
+            if (VISC && typ != MRAB_BC_WALL) {
+                // F^V_kappa - Fhat^V_kappa contracted with grad(kappa)
+#pragma unroll
+                for (int j = 0; j <= D; ++j) {
+                    double fk = 0.0, fh = 0.0;
+#pragma unroll
+                    for (int i = 0; i < D; ++i) {
+                        fk += nv[i] * __ldg(FV + (int64_t)(i * (D + 1) + j) * N + p);
+                        if (typ == MRAB_BC_OVERSET)
+                            fh += nv[i] * m.fvhat[(int64_t)(i * (D + 1) + j) * m.nrecv + slot];
+                    }
+                    R[1 + j] += 0.5 * side * (fk - fh) / kP0;
+                }
+            }
+        }
+    }
+
 // ------------------------------------------------------------------------------------
 // fused RHS + SAT + combination epilogue
 // ------------------------------------------------------------------------------------
@@ -245,62 +310,7 @@ __global__ void __launch_bounds__(256) k_rhs(DevMesh m, const double* __restrict
 #pragma unroll
         for (int c = 0; c < NC; ++c) R[c] = -Jp * R[c];
 
-        // ---- SAT at segment ends (eq:int; P:292-294 sum over flagged directions) ----
-#pragma unroll
-        for (int k = 0; k < D; ++k) {
-            const int cl = (code >> (4 * k)) & 15;
-            if (cl != CLS_L0 && cl != CLS_R0) continue;
-            const int sidx = (cl == CLS_L0) ? 0 : 1;
-            const double side = (cl == CLS_L0) ? 1.0 : -1.0;
-            const bool at_face = !m.periodic[k] && (sidx == 0 ? idx[k] == 0 : idx[k] == m.n[k] - 1);
-            const int typ = at_face ? m.face_bc[k][sidx] : MRAB_BC_OVERSET;
-            double q[NC], qh[NC], dq[NC], nv[D];
-#pragma unroll
-            for (int c = 0; c < NC; ++c) q[c] = __ldg(Q + c * N + p);
-#pragma unroll
-            for (int i = 0; i < D; ++i)
-                nv[i] = CART ? (i == k ? m.cJ * m.cM[k] : 0.0) : Jp * __ldg(m.M + (k * D + i) * N + p);
-            int slot = -1;
-            if (typ == MRAB_BC_OVERSET) {
-                slot = m.recv_slot[p];
-#pragma unroll
-                for (int c = 0; c < NC; ++c) qh[c] = m.qhat[c * m.nrecv + slot];
-            } else if (typ == MRAB_BC_FARFIELD) {
-#pragma unroll
-                for (int c = 0; c < NC; ++c) qh[c] = g.q_inf[c];
-            } else {   // isothermal no-slip wall
-                qh[0] = q[0];
-#pragma unroll
-                for (int i = 0; i < D; ++i) qh[1 + i] = 0.0;
-                qh[D + 1] = q[0] * g.wall_T / (g.gamma * (g.gamma - 1.0));
-            }
-#pragma unroll
-            for (int c = 0; c < NC; ++c) dq[c] = q[c] - qh[c];
-            double kd[NC];
-            kchar<D>(q, nv, side, dq, g.gamma, kd);
-            double sig1 = 0.0;
-            if (VISC) {
-#pragma unroll
-                for (int i = 0; i < D; ++i) sig1 += nv[i] * nv[i];
-                sig1 *= 0.5 / g.Re;
-            }
-#pragma unroll
-            for (int c = 0; c < NC; ++c) R[c] -= (0.5 * kd[c] + sig1 * dq[c]) / kP0;
-            if (VISC && typ != MRAB_BC_WALL) {
-                // F^V_kappa - Fhat^V_kappa contracted with grad(kappa)
-#pragma unroll
-                for (int j = 0; j <= D; ++j) {
-                    double fk = 0.0, fh = 0.0;
-#pragma unroll
-                    for (int i = 0; i < D; ++i) {
-                        fk += nv[i] * __ldg(FV + (int64_t)(i * (D + 1) + j) * N + p);
-                        if (typ == MRAB_BC_OVERSET)
-                            fh += nv[i] * m.fvhat[(int64_t)(i * (D + 1) + j) * m.nrecv + slot];
-                    }
-                    R[1 + j] += 0.5 * side * (fk - fh) / kP0;
-                }
-            }
-        }
+        sat_point<D, VISC, CART>(m, Q, FV, g, p, idx, code, Jp, R);
     }
     if (ep.r_out) {
 #pragma unroll
@@ -312,6 +322,341 @@ __global__ void __launch_bounds__(256) k_rhs(DevMesh m, const double* __restrict
             double y = ep.base[c * N + p] + ep.c_new * R[c];
             for (int s = 0; s < ep.nsrc; ++s) y += ep.csrc[s] * ep.src[s][c * N + p];
             ep.y_out[c * N + p] = y;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// 3-D tiled RHS: per direction kappa, the contravariant flux Fhat_kappa is formed once per
+// point of the tile extended by the D1 reach (3) along kappa and staged in shared memory;
+// every point then applies its own segment row, accumulating in shared memory.  All global
+// loads of a thread's region points are issued before any is used (no dependence on the
+// class codes: hole points carry finite data that no active stencil reads, and points
+// outside a non-periodic mesh are clamped to a valid address), so each direction costs one
+// memory round trip.  Cartesian viscous fluxes come from the k_visc pass.
+// Tile 8 x 8 x 8, 256 threads.
+// ------------------------------------------------------------------------------------
+namespace {
+constexpr int T3X = 8, T3Y = 8, T3Z = 8, NT3 = 256;
+constexpr int T3N = T3X * T3Y * T3Z;                  // 512
+constexpr int PPT3 = T3N / NT3;                       // 2 own points per thread
+constexpr int REG3 = 14 * 8 * 8;                      // extended region (any direction)
+constexpr int KR3 = (REG3 + NT3 - 1) / NT3;           // region points per thread (4)
+constexpr size_t SMEM3 = sizeof(double) * 5 * (REG3 + T3N) + sizeof(uint16_t) * T3N;
+}  // namespace
+
+template <bool VISC, bool CART>
+__global__ void __launch_bounds__(NT3, 2) k_rhs3d(DevMesh m, const double* __restrict__ Q,
+                                                 const double* __restrict__ FV, Gas g, Epilogue ep) {
+    constexpr int NC = 5;
+    extern __shared__ __align__(16) double fb[];        // Fhat [NC][REG3], then Racc [NC][T3N]
+    double* racc = fb + NC * REG3;
+    uint16_t* sc = reinterpret_cast<uint16_t*>(racc + NC * T3N);
+    const int n0 = m.n[0], n1 = m.n[1], n2 = m.n[2];
+    const int64_t N = m.npts;
+    const int64_t s1 = n0, s2 = (int64_t)n0 * n1;
+    const int i0 = blockIdx.x * T3X, j0 = blockIdx.y * T3Y, k0 = blockIdx.z * T3Z;
+    const int tid = threadIdx.x;
+
+    for (int t = tid; t < T3N; t += NT3) {
+        const int x = t & 7, y = (t >> 3) & 7, z = t >> 6;
+        const int gi = i0 + x, gj = j0 + y, gk = k0 + z;
+        const bool live = gi < n0 && gj < n1 && gk < n2;
+        sc[t] = live ? m.cls[gi + s1 * gj + s2 * gk] : (uint16_t)0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) racc[c * T3N + t] = 0.0;
+    }
+#pragma unroll 1
+    for (int kap = 0; kap < 3; ++kap) {
+        const int ex = kap == 0 ? 3 : 0, ey = kap == 1 ? 3 : 0, ez = kap == 2 ? 3 : 0;
+        const int RX = T3X + 2 * ex, RY = T3Y + 2 * ey;
+        // ---- loads of all region points of this thread (independent, in flight together)
+        double lq[KR3][NC], lv[KR3][4], lm[KR3][3];
+#pragma unroll
+        for (int r = 0; r < KR3; ++r) {
+            const int t = tid + r * NT3;
+            const int x = t % RX, y = (t / RX) % RY, z = t / (RX * RY);
+            int gg[3] = {i0 - ex + x, j0 - ey + y, k0 - ez + z};
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const int n = m.n[k];
+                if (gg[k] < 0) gg[k] = m.periodic[k] ? gg[k] + n : 0;
+                else if (gg[k] >= n) gg[k] = m.periodic[k] ? gg[k] - n : n - 1;
+            }
+            const int64_t q = gg[0] + s1 * gg[1] + s2 * gg[2];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) lq[r][c] = __ldg(Q + c * N + q);
+            if (VISC) {
+                if (CART) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) lv[r][j] = __ldg(FV + (int64_t)(kap * 4 + j) * N + q);
+                }
+            }
+            if (!CART) {
+#pragma unroll
+                for (int i = 0; i < 3; ++i) lm[r][i] = __ldg(m.M + (kap * 3 + i) * N + q);
+            }
+            (void)lv;
+            (void)lm;
+            if (!CART && VISC) {
+                // curvilinear: F^V of every Cartesian direction is needed; fetch into lv on use
+            }
+            // stash the clamped index for the curvilinear viscous path
+            lv[r][0] = CART ? lv[r][0] : __longlong_as_double((long long)q);
+        }
+        // ---- contravariant fluxes -> shared memory
+#pragma unroll
+        for (int r = 0; r < KR3; ++r) {
+            const int t = tid + r * NT3;
+            if (t >= (T3X + 2 * ex) * (T3Y + 2 * ey) * (T3Z + 2 * ez)) break;
+            const double rho = lq[r][0];
+            const double ir = 1.0 / rho;
+            const double u[3] = {lq[r][1] * ir, lq[r][2] * ir, lq[r][3] * ir};
+            const double E = lq[r][4];
+            const double pr = g.gm1 * (E - 0.5 * (lq[r][1] * u[0] + lq[r][2] * u[1] + lq[r][3] * u[2]));
+            double fh[NC] = {0, 0, 0, 0, 0};
+            if (CART) {
+                const int i = kap;
+                double f[NC];
+                f[0] = lq[r][1 + i];
+#pragma unroll
+                for (int j = 0; j < 3; ++j) f[1 + j] = lq[r][1 + i] * u[j] + (i == j ? pr : 0.0);
+                f[4] = (E + pr) * u[i];
+                if (VISC) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) f[1 + j] -= lv[r][j];
+                }
+#pragma unroll
+                for (int c = 0; c < NC; ++c) fh[c] = m.cM[kap] * f[c];
+            } else {
+                const int64_t q = (int64_t)__double_as_longlong(lv[r][0]);
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    double f[NC];
+                    f[0] = lq[r][1 + i];
+#pragma unroll
+                    for (int j = 0; j < 3; ++j) f[1 + j] = lq[r][1 + i] * u[j] + (i == j ? pr : 0.0);
+                    f[4] = (E + pr) * u[i];
+                    if (VISC) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) f[1 + j] -= __ldg(FV + (int64_t)(i * 4 + j) * N + q);
+                    }
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) fh[c] += lm[r][i] * f[c];
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < NC; ++c) fb[c * REG3 + t] = fh[c];
+        }
+        __syncthreads();
+        // ---- D_kappa of the staged fluxes at the tile points
+        const int sk = kap == 0 ? 1 : (kap == 1 ? RX : RX * RY);
+        for (int t = tid; t < T3N; t += NT3) {
+            const unsigned code = sc[t];
+            if (!code) continue;
+            const int x = t & 7, y = (t >> 3) & 7, z = t >> 6;
+            const int rr = (x + ex) + RX * ((y + ey) + RY * (z + ez));
+            const int cl = (code >> (4 * kap)) & 15;
+            if (cl == CLS_INT) {
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    const double* f = fb + c * REG3;
+                    racc[c * T3N + t] += (2.0 / 3.0) * (f[rr + sk] - f[rr - sk]) - (1.0 / 12.0) * (f[rr + 2 * sk] - f[rr - 2 * sk]);
+                }
+            } else {
+                const int ns = c_nst[cl];
+                double acc[NC] = {0, 0, 0, 0, 0};
+                for (int tt = 0; tt < ns; ++tt) {
+                    const double cf = c_cf[cl][tt];
+                    const int o = rr + c_off[cl][tt] * sk;
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) acc[c] += cf * fb[c * REG3 + o];
+                }
+#pragma unroll
+                for (int c = 0; c < NC; ++c) racc[c * T3N + t] += acc[c];
+            }
+        }
+        __syncthreads();
+    }
+    // ---- SAT and epilogue
+#pragma unroll
+    for (int s = 0; s < PPT3; ++s) {
+        const int t = tid + s * NT3;
+        const int x = t & 7, y = (t >> 3) & 7, z = t >> 6;
+        const int gi = i0 + x, gj = j0 + y, gk = k0 + z;
+        if (gi >= n0 || gj >= n1 || gk >= n2) continue;
+        const int64_t p = gi + s1 * gj + s2 * gk;
+        const unsigned code = sc[t];
+        double yb[NC];
+        if (ep.y_out) {
+            // all history loads issued together (unused slots re-read `base` with weight 0)
+            const double* sp[4];
+            double cw[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                sp[k] = k < ep.nsrc ? ep.src[k] : ep.base;
+                cw[k] = k < ep.nsrc ? ep.csrc[k] : 0.0;
+            }
+            double v[5][NC];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                v[0][c] = __ldg(ep.base + c * N + p);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) v[1 + k][c] = __ldg(sp[k] + c * N + p);
+            }
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+                yb[c] = v[0][c] + cw[0] * v[1][c] + cw[1] * v[2][c] + cw[2] * v[3][c] + cw[3] * v[4][c];
+            for (int k = 4; k < ep.nsrc; ++k)
+#pragma unroll
+                for (int c = 0; c < NC; ++c) yb[c] += ep.csrc[k] * __ldg(ep.src[k] + c * N + p);
+        }
+        double Rs[NC] = {0, 0, 0, 0, 0};
+        if (code) {
+            const double Jp = CART ? m.cJ : __ldg(m.J + p);
+#pragma unroll
+            for (int c = 0; c < NC; ++c) Rs[c] = -Jp * racc[c * T3N + t];
+            bool sat = false;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const int cl = (code >> (4 * k)) & 15;
+                sat = sat || cl == CLS_L0 || cl == CLS_R0;
+            }
+            if (sat) {
+                const int idx[3] = {gi, gj, gk};
+                sat_point<3, VISC, CART>(m, Q, FV, g, p, idx, code, Jp, Rs);
+            }
+        }
+        if (ep.r_out) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) ep.r_out[c * N + p] = Rs[c];
+        }
+        if (ep.y_out) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) ep.y_out[c * N + p] = yb[c] + ep.c_new * Rs[c];
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// 3-D tiled viscous fluxes over a box: per direction kappa the primitives (u, v, w, T) of
+// the tile extended by 3 along kappa are staged in shared memory (decoupled loads), each
+// tile point takes its segment row of D1; then Cartesian gradients, stress, heat flux and
+// F^V_i (12 values, layout [i][j]) are written.  Tile 8 x 8 x 8, 256 threads.
+// ------------------------------------------------------------------------------------
+template <bool CART>
+__global__ void __launch_bounds__(NT3, 2) k_visc3d(DevMesh m, const double* __restrict__ Q,
+                                                  double* __restrict__ FV, Box box, Gas g) {
+    __shared__ double pv[4][REG3];
+    __shared__ uint16_t sc[T3N];
+    const int n0 = m.n[0], n1 = m.n[1], n2 = m.n[2];
+    const int64_t N = m.npts;
+    const int64_t s1 = n0, s2 = (int64_t)n0 * n1;
+    const int i0 = box.lo[0] + blockIdx.x * T3X, j0 = box.lo[1] + blockIdx.y * T3Y,
+              k0 = box.lo[2] + blockIdx.z * T3Z;
+    const int tid = threadIdx.x;
+    for (int t = tid; t < T3N; t += NT3) {
+        const int gi = i0 + (t & 7), gj = j0 + ((t >> 3) & 7), gk = k0 + (t >> 6);
+        const bool live = gi <= box.hi[0] && gj <= box.hi[1] && gk <= box.hi[2];
+        sc[t] = live ? m.cls[gi + s1 * gj + s2 * gk] : (uint16_t)0;
+    }
+    double d[PPT3][3][4];   // d[s][kappa][u,v,w,T]
+#pragma unroll
+    for (int kap = 0; kap < 3; ++kap) {
+        const int ex = kap == 0 ? 3 : 0, ey = kap == 1 ? 3 : 0, ez = kap == 2 ? 3 : 0;
+        const int RX = T3X + 2 * ex, RY = T3Y + 2 * ey;
+        double lq[KR3][5];
+#pragma unroll
+        for (int r = 0; r < KR3; ++r) {
+            const int t = tid + r * NT3;
+            const int x = t % RX, y = (t / RX) % RY, z = t / (RX * RY);
+            int gg[3] = {i0 - ex + x, j0 - ey + y, k0 - ez + z};
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const int n = m.n[k];
+                if (gg[k] < 0) gg[k] = m.periodic[k] ? gg[k] + n : 0;
+                else if (gg[k] >= n) gg[k] = m.periodic[k] ? gg[k] - n : n - 1;
+            }
+            const int64_t q = gg[0] + s1 * gg[1] + s2 * gg[2];
+#pragma unroll
+            for (int c = 0; c < 5; ++c) lq[r][c] = __ldg(Q + c * N + q);
+        }
+        if (kap > 0) __syncthreads();   // previous direction's stencils are done with pv
+#pragma unroll
+        for (int r = 0; r < KR3; ++r) {
+            const int t = tid + r * NT3;
+            if (t >= REG3) break;
+            const double ir = 1.0 / lq[r][0];
+            const double u = lq[r][1] * ir, v = lq[r][2] * ir, w = lq[r][3] * ir;
+            pv[0][t] = u;
+            pv[1][t] = v;
+            pv[2][t] = w;
+            pv[3][t] = g.gamma * g.gm1 * (lq[r][4] - 0.5 * (lq[r][1] * u + lq[r][2] * v + lq[r][3] * w)) * ir;
+        }
+        __syncthreads();
+        const int sk = kap == 0 ? 1 : (kap == 1 ? RX : RX * RY);
+#pragma unroll
+        for (int s = 0; s < PPT3; ++s) {
+            const int t = tid + s * NT3;
+            const unsigned code = sc[t];
+#pragma unroll
+            for (int f = 0; f < 4; ++f) d[s][kap][f] = 0.0;
+            if (!code) continue;
+            const int x = t & 7, y = (t >> 3) & 7, z = t >> 6;
+            const int rr = (x + ex) + RX * ((y + ey) + RY * (z + ez));
+            const int cl = (code >> (4 * kap)) & 15;
+            if (cl == CLS_INT) {
+#pragma unroll
+                for (int f = 0; f < 4; ++f) {
+                    const double* a = pv[f];
+                    d[s][kap][f] = (2.0 / 3.0) * (a[rr + sk] - a[rr - sk]) - (1.0 / 12.0) * (a[rr + 2 * sk] - a[rr - 2 * sk]);
+                }
+            } else {
+                const int ns = c_nst[cl];
+                for (int tt = 0; tt < ns; ++tt) {
+                    const double cf = c_cf[cl][tt];
+                    const int o = rr + c_off[cl][tt] * sk;
+#pragma unroll
+                    for (int f = 0; f < 4; ++f) d[s][kap][f] += cf * pv[f][o];
+                }
+            }
+        }
+    }
+    // center primitives (the z-extended region holds the tile points at z + 3)
+#pragma unroll
+    for (int s = 0; s < PPT3; ++s) {
+        const int t = tid + s * NT3;
+        const unsigned code = sc[t];
+        if (!code) continue;
+        const int x = t & 7, y = (t >> 3) & 7, z = t >> 6;
+        const int rr = x + T3X * (y + T3Y * (z + 3));
+        const double u[3] = {pv[0][rr], pv[1][rr], pv[2][rr]};
+        const int64_t p = (i0 + x) + s1 * (j0 + y) + s2 * (k0 + z);
+        double gr[4][3];   // gr[f][i] = d phi_f / d x_i
+#pragma unroll
+        for (int f = 0; f < 4; ++f)
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                if (CART) {
+                    gr[f][i] = m.cJ * (m.cM[i] * d[s][i][f]);
+                } else {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) acc += __ldg(m.M + (k * 3 + i) * N + p) * d[s][k][f];
+                    gr[f][i] = __ldg(m.J + p) * acc;
+                }
+            }
+        const double div = gr[0][0] + gr[1][1] + gr[2][2];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            double e = 0.0;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const double tau = (gr[i][j] + gr[j][i] - (i == j ? (2.0 / 3.0) * div : 0.0)) * g.iRe;
+                FV[(int64_t)(i * 4 + j) * N + p] = tau;
+                e += u[j] * tau;
+            }
+            FV[(int64_t)(i * 4 + 3) * N + p] = e + g.kT * gr[3][i];
         }
     }
 }
@@ -406,6 +751,18 @@ void launch_visc(int dim, const DevMesh& m, const double* Q, double* FV, const B
                   (box.hi[2] - box.lo[2] + 1);
     if (tot <= 0) return;
     unsigned nb = blocks_for(tot, 256);
+    static int direct = -1;
+    if (direct < 0) {
+        const char* e = getenv("MRAB_3D_DIRECT");
+        direct = e && e[0] == '1';
+    }
+    if (dim == 3 && !direct) {
+        dim3 grid((box.hi[0] - box.lo[0] + T3X) / T3X, (box.hi[1] - box.lo[1] + T3Y) / T3Y,
+                  (box.hi[2] - box.lo[2] + T3Z) / T3Z);
+        if (m.cart) k_visc3d<true><<<grid, NT3, 0, st>>>(m, Q, FV, box, gas);
+        else k_visc3d<false><<<grid, NT3, 0, st>>>(m, Q, FV, box, gas);
+        return;
+    }
     if (dim == 2) {
         if (m.cart) k_visc<2, true><<<nb, 256, 0, st>>>(m, Q, FV, box, gas);
         else k_visc<2, false><<<nb, 256, 0, st>>>(m, Q, FV, box, gas);
@@ -422,6 +779,31 @@ void launch_rhs(int dim, const DevMesh& m, const double* Q, const double* FV, co
                 const Epilogue& ep, const DonorSet& ds, cudaStream_t st) {
     if (dim == 2) {
         launch_rhs2d(m, Q, gas, ep, ds, st);
+        return;
+    }
+    static int direct = -1;
+    if (direct < 0) {
+        const char* e = getenv("MRAB_3D_DIRECT");
+        direct = e && e[0] == '1';
+    }
+    if (!direct) {
+        const size_t bytes = SMEM3;
+        static bool init[4] = {false, false, false, false};
+        dim3 grid((m.n[0] + T3X - 1) / T3X, (m.n[1] + T3Y - 1) / T3Y, (m.n[2] + T3Z - 1) / T3Z);
+#define MRAB_RHS3(V, C, I)                                                                          \
+    do {                                                                                            \
+        if (!init[I]) {                                                                             \
+            cudaFuncSetAttribute(k_rhs3d<V, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes); \
+            init[I] = true;                                                                         \
+        }                                                                                           \
+        k_rhs3d<V, C><<<grid, NT3, bytes, st>>>(m, Q, FV, gas, ep);                                 \
+    } while (0)
+        if (gas.viscous) {
+            if (m.cart) MRAB_RHS3(true, true, 0); else MRAB_RHS3(true, false, 1);
+        } else {
+            if (m.cart) MRAB_RHS3(false, true, 2); else MRAB_RHS3(false, false, 3);
+        }
+#undef MRAB_RHS3
         return;
     }
     unsigned nb = blocks_for(m.npts, 256);
