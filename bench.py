@@ -89,6 +89,19 @@ class Clocks:
                 "samples": len(sm)}
 
 
+def combine_ranks(total_ms, point_rhs, dist=None, device="cpu"):
+    """Whole-job numbers over replicas: the MAX of the ranks' timed totals and
+    the SUM of their point-RHS counts (value = sum / max)."""
+    if dist is None:
+        return total_ms, point_rhs
+    import torch
+    t = torch.tensor([total_ms], device=device, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    c = torch.tensor([float(point_rhs)], device=device, dtype=torch.float64)
+    dist.all_reduce(c, op=dist.ReduceOp.SUM)
+    return float(t.item()), int(c.item())
+
+
 def _problem(cid, scale, sr=None):
     import synth
     kw = {} if sr is None else {"sr": sr}
@@ -216,13 +229,7 @@ def run_gpu(args):
     ev1, _, _ = ctx.counters()
     active = [plan.info(g)[1] for g in range(G)]
     pr = int(sum((ev1[g] - ev0[g]) * active[g] for g in range(G)))
-    t_max, pr_sum = total_ms, pr
-    if dist is not None:
-        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        c = torch.tensor([pr], device="cuda", dtype=torch.float64)
-        dist.all_reduce(c, op=dist.ReduceOp.SUM)
-        t_max, pr_sum = float(t.item()), int(c.item())
+    t_max, pr_sum = combine_ranks(total_ms, pr, dist, "cuda")
     value = pr_sum / (t_max * 1e-3)
     launches = ctx.launches_per_macro_step()
 
