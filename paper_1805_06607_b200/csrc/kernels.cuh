@@ -47,6 +47,9 @@ struct Epilogue {
     // 2-D only: restrict the launch to a list of tiles (tile = ty * ntx + tx); NULL = all
     const int32_t* tiles;
     int ntiles;
+    // launch priority recorded on the launch itself (survives graph capture); 0 = default
+    int prio;
+    int has_prio;
 };
 
 // tile grid of the 2-D RHS kernel (for building tile lists on the host)

@@ -471,8 +471,23 @@ void launch_donor2d(const RecvTask& rt, const SrcSets& ss, const MeshTable& mt, 
     const int64_t tot = rt.off[rt.nmesh];
     if (tot <= 0) return;
     const unsigned nb = (unsigned)((tot * 16 + 127) / 128);
-    if (gas.viscous) k_donor2d<true><<<nb, 128, 0, st>>>(rt, ss, mt, gas);
-    else k_donor2d<false><<<nb, 128, 0, st>>>(rt, ss, mt, gas);
+    // the gather sits on the critical path of the fast substeps: highest launch priority
+    static int greatest = 1;
+    if (greatest > 0) {
+        int least = 0;
+        cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nb);
+    cfg.blockDim = dim3(128);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributePriority;
+    at[0].val.priority = greatest;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (gas.viscous) cudaLaunchKernelEx(&cfg, k_donor2d<true>, rt, ss, mt, gas);
+    else cudaLaunchKernelEx(&cfg, k_donor2d<false>, rt, ss, mt, gas);
 }
 
 template <bool VISC, bool CART, int TY, int MINB, int NTH>
@@ -488,6 +503,20 @@ static void launch_t(const DevMesh& m, const double* Q, const Gas& g, const Epil
     dim3 grid((m.n[0] + TX - 1) / TX, (m.n[1] + TY - 1) / TY);
     if (ep.tiles) grid = dim3(ep.ntiles, 1);
     if (grid.x * grid.y == 0) return;
+    if (ep.has_prio) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(NTH);
+        cfg.dynamicSmemBytes = bytes;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributePriority;
+        at[0].val.priority = ep.prio;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, k_rhs2d<VISC, CART, TY, MINB, NTH>, m, Q, g, ep, ds);
+        return;
+    }
     k_rhs2d<VISC, CART, TY, MINB, NTH><<<grid, NTH, bytes, st>>>(m, Q, g, ep, ds);
 }
 

@@ -628,6 +628,15 @@ static void issue_macro_step_dag2d(mrab_ctx* c) {
             dm.fvhat = fvhat_set(c, g, j);
             const DonorSet ds{};
             const bool split = c->overlap && D.ncrit > 0 && D.nbulk > 0 && partial_read_after(g, j);
+            {
+                // priorities travel with the launches into the graph: fastest meshes first
+                int least = 0, greatest = 0;
+                cudaDeviceGetStreamPriorityRange(&least, &greatest);
+                int smin = S;
+                for (auto& q : P.meshes) smin = std::min(smin, q.s);
+                ep.has_prio = 1;
+                ep.prio = mp.s == smin ? greatest : least;
+            }
             if (split) {
                 Epilogue e1 = ep;
                 e1.tiles = D.tiles;
