@@ -5,9 +5,11 @@ Contract:
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mrab|reference] [--config C]
 One "step" = one MRAB macro step H = S_max h of the whole hot path (every mesh's fused
 SBP-SAT RHS + AB update at its own rate, donor intermediate states, Lagrange gathers) on the
-workload of BASELINE.json configs[1] (config 2, full size) unless --config says otherwise.
+cylinder workload, BASELINE.json configs[2] (config 3, full size: every timed number of the
+paper is on its cylinder case) unless --config says otherwise.
 metric = grid-point RHS evaluations per second (sum over meshes of active points x RHS
-evaluations, fp64).  L2 is flushed (256 MiB write) between timed steps.  Multi-GPU: one
+evaluations, fp64).  L2 is scrubbed (256 MiB write + 256 MiB read of another buffer)
+between timed steps.  Multi-GPU: one
 process per GPU, each an independent replica (no data-path collective).
 --impl reference times the oracle (oracle/, plain numpy fp64) on host cores instead.
 """
@@ -251,8 +253,17 @@ def run_gpu(args):
             mk, _ = ctx.time_kernel(kid, g, reps=10, flush_l2=True)
             tot += mk * evals_per_step[g]
         kernel_times[name] = tot
+    traffic = None
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        ent = tj.get(f"config{args.config}/mesh{gdom}/k_rhs2d" if p.dim == 2
+                     else f"config{args.config}/mesh{gdom}/k_rhs3d")
+        if ent:
+            traffic = ent["total"]
+    except Exception:
+        traffic = None
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": None,
+            "frac": achieved / peak, "traffic": traffic,
             "kernel": f"k_rhs (fused RHS+SAT+AB) on mesh {gdom} ({p.meshes[gdom].name})",
             "algorithmic_bytes_per_launch": by, "ms_per_launch": ms, "peak_source": peak_src,
             "kernel_ms_per_step_cold": kernel_times}
