@@ -109,6 +109,7 @@ __global__ void __launch_bounds__(NTH, MINB) k_rhs2d(DevMesh m, const double* __
 
     // ---- phase A: primitives of tile + halo ------------------------------------------
     constexpr int KA = (NA + NTH - 1) / NTH;
+    int allint = 1;
     {
         double ld[KA][4];
         unsigned cd[KA];
@@ -154,11 +155,65 @@ __global__ void __launch_bounds__(NTH, MINB) k_rhs2d(DevMesh m, const double* __
             sh_r[t] = r;
             sh_uv[t] = make_double2(u, v);
             sh_T[t] = T;
+            // tile-uniform fast path: every flux point (tile + 3) interior in both directions
+            const int b = t / AX, a = t - b * AX;
+            if (b >= H - G3 && b < H + TY + G3 && a >= H - G3 && a < H + TX + G3 &&
+                cd[k] != (unsigned)(CLS_INT | (CLS_INT << 4)))
+                allint = 0;
         }
     }
-    __syncthreads();
+    const int fast = __syncthreads_and(allint);
 
     // ---- phase B: contravariant fluxes at tile + 3 -----------------------------------
+    if (fast) {
+        for (int t = tid; t < NF; t += NTH) {
+            const int b = t / FX, a = t - b * FX;
+            const int s = (b + H - G3) * AX + (a + H - G3);
+            const double r = sh_r[s];
+            const double2 uv = sh_uv[s];
+            const double u = uv.x, v = uv.y;
+            const double p = r * sh_T[s] * g.igamma;
+            const double E = p * g.igm1 + 0.5 * r * (u * u + v * v);
+            double Ix[4] = {r * u, r * u * u + p, r * u * v, (E + p) * u};
+            double Iy[4] = {r * v, r * u * v, r * v * v + p, (E + p) * v};
+            int64_t q = 0;
+            if (!CART) {
+                int gi = i0 - G3 + a, gj = j0 - G3 + b;
+                if (gi < 0) gi += n0; else if (gi >= n0) gi -= n0;
+                if (gj < 0) gj += n1; else if (gj >= n1) gj -= n1;
+                q = gi + (int64_t)n0 * gj;
+            }
+            if (VISC) {
+                double Vx[4], Vy[4];
+                visc_at_int<CART, AX>(sh_uv, sh_T, s, m, q, g, Vx, Vy);
+#pragma unroll
+                for (int c = 1; c < 4; ++c) {
+                    Ix[c] -= Vx[c];
+                    Iy[c] -= Vy[c];
+                }
+            }
+            double fx[4], fy[4];
+            if (CART) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    fx[c] = m.cM[0] * Ix[c];
+                    fy[c] = m.cM[1] * Iy[c];
+                }
+            } else {
+                const double Mxx = __ldg(m.M + q), Mxy = __ldg(m.M + N + q);
+                const double Myx = __ldg(m.M + 2 * N + q), Myy = __ldg(m.M + 3 * N + q);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    fx[c] = Mxx * Ix[c] + Mxy * Iy[c];
+                    fy[c] = Myx * Ix[c] + Myy * Iy[c];
+                }
+            }
+            fh[t] = make_double2(fx[0], fx[1]);
+            fh[NF + t] = make_double2(fx[2], fx[3]);
+            fh[2 * NF + t] = make_double2(fy[0], fy[1]);
+            fh[3 * NF + t] = make_double2(fy[2], fy[3]);
+        }
+    } else
     for (int t = tid; t < NF; t += NTH) {
         const int b = t / FX, a = t - b * FX;
         const int s = (b + H - G3) * AX + (a + H - G3);
@@ -212,6 +267,55 @@ __global__ void __launch_bounds__(NTH, MINB) k_rhs2d(DevMesh m, const double* __
     __syncthreads();
 
     // ---- phase C: divergence, SAT, epilogue ------------------------------------------
+    if (fast) {
+        // interior tile: no closures, no SAT, no holes
+        for (int t = tid; t < TX * TY; t += NTH) {
+            const int a = t % TX, b = t / TX;
+            const int gi = i0 + a, gj = j0 + b;
+            const int64_t p = gi + (int64_t)n0 * gj;
+            const int f = (b + G3) * FX + (a + G3);
+            double yb[4] = {0, 0, 0, 0};
+            if (ep.y_out) {
+                const double* sp[4];
+                double cw[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    sp[k] = k < ep.nsrc ? ep.src[k] : ep.base;
+                    cw[k] = k < ep.nsrc ? ep.csrc[k] : 0.0;
+                }
+                double v[5][4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    v[0][c] = __ldg(ep.base + c * N + p);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) v[1 + k][c] = __ldg(sp[k] + c * N + p);
+                }
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    yb[c] = v[0][c] + cw[0] * v[1][c] + cw[1] * v[2][c] + cw[2] * v[3][c] + cw[3] * v[4][c];
+                for (int k = 4; k < ep.nsrc; ++k)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) yb[c] += ep.csrc[k] * __ldg(ep.src[k] + c * N + p);
+            }
+            const double2 x01 = d_int2(fh, f, 1), x23 = d_int2(fh + NF, f, 1);
+            const double2 y01 = d_int2(fh + 2 * NF, f, FX), y23 = d_int2(fh + 3 * NF, f, FX);
+            const double Jp = CART ? m.cJ : __ldg(m.J + p);
+            double R[4];
+            R[0] = -Jp * (x01.x + y01.x);
+            R[1] = -Jp * (x01.y + y01.y);
+            R[2] = -Jp * (x23.x + y23.x);
+            R[3] = -Jp * (x23.y + y23.y);
+            if (ep.r_out) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) ep.r_out[c * N + p] = R[c];
+            }
+            if (ep.y_out) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) ep.y_out[c * N + p] = yb[c] + ep.c_new * R[c];
+            }
+        }
+        return;
+    }
     for (int t = tid; t < TX * TY; t += NTH) {
         const int a = t % TX, b = t / TX;
         const int gi = i0 + a, gj = j0 + b;

@@ -110,5 +110,36 @@ static __device__ __forceinline__ void visc_at(const double2* __restrict__ sh_uv
 }
 
 
+// visc_at for a point whose rows are interior in both directions (compile-time stencils)
+template <bool CART, int AX>
+static __device__ __forceinline__ void visc_at_int(const double2* __restrict__ sh_uv,
+                                                   const double* __restrict__ sh_T, int s,
+                                                   const DevMesh& m, int64_t p, const Gas& g,
+                                                   double* Fx, double* Fy) {
+    const double2 uvx = d_int2(sh_uv, s, 1), uvy = d_int2(sh_uv, s, AX);
+    const double Tx = d_int(sh_T, s, 1), Ty = d_int(sh_T, s, AX);
+    double dudx, dudy, dvdx, dvdy, dTdx, dTdy;
+    if (CART) {
+        const double sx = m.cJ * m.cM[0], sy = m.cJ * m.cM[1];
+        dudx = sx * uvx.x; dvdx = sx * uvx.y; dTdx = sx * Tx;
+        dudy = sy * uvy.x; dvdy = sy * uvy.y; dTdy = sy * Ty;
+    } else {
+        const int64_t N = m.npts;
+        const double J = __ldg(m.J + p);
+        const double Mxx = __ldg(m.M + p), Mxy = __ldg(m.M + N + p);
+        const double Myx = __ldg(m.M + 2 * N + p), Myy = __ldg(m.M + 3 * N + p);
+        dudx = J * (Mxx * uvx.x + Myx * uvy.x); dudy = J * (Mxy * uvx.x + Myy * uvy.x);
+        dvdx = J * (Mxx * uvx.y + Myx * uvy.y); dvdy = J * (Mxy * uvx.y + Myy * uvy.y);
+        dTdx = J * (Mxx * Tx + Myx * Ty); dTdy = J * (Mxy * Tx + Myy * Ty);
+    }
+    const double div = dudx + dvdy;
+    const double txx = (2.0 * dudx - (2.0 / 3.0) * div) * g.iRe;
+    const double tyy = (2.0 * dvdy - (2.0 / 3.0) * div) * g.iRe;
+    const double txy = (dudy + dvdx) * g.iRe;
+    const double2 uv = sh_uv[s];
+    Fx[0] = 0.0; Fx[1] = txx; Fx[2] = txy; Fx[3] = uv.x * txx + uv.y * txy + g.kT * dTdx;
+    Fy[0] = 0.0; Fy[1] = txy; Fy[2] = tyy; Fy[3] = uv.x * txy + uv.y * tyy + g.kT * dTdy;
+}
+
 }  // namespace k2d
 }  // namespace mrab
