@@ -839,6 +839,18 @@ void launch_combine(int nc, const DevMesh& m, const Box& box, const double* base
     k_combine<<<blocks_for(tot, 256), 256, 0, st>>>(nc, m.npts, m.n[0], m.n[1], box, a, out);
 }
 
+// "rhs blowup" check: any non-finite value in n doubles sets *flag
+__global__ void k_finite(const double* __restrict__ a, size_t n, int* flag) {
+    int bad = 0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        bad |= !isfinite(a[i]);
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+void launch_finite(const double* a, size_t n, int* flag, cudaStream_t st) {
+    k_finite<<<148 * 4, 256, 0, st>>>(a, n, flag);
+}
+
 __global__ void k_scrub_read(const double4* __restrict__ b, size_t n, double* sink) {
     double acc = 0.0;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {

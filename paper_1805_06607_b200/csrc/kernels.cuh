@@ -128,5 +128,7 @@ void upload_stencil_rows();
 // L2 scrub for cold-cache timing: write `a` (bytes) then stream-read `b` (bytes) so that the
 // L2 ends up holding clean lines of an unrelated buffer (no dirty write-backs later).
 void launch_l2_scrub(void* a, void* b, size_t bytes, int tag, cudaStream_t st);
+// sets *flag (device int) if any of the n doubles is not finite
+void launch_finite(const double* a, size_t n, int* flag, cudaStream_t st);
 
 }  // namespace mrab

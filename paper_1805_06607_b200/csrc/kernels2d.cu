@@ -143,14 +143,13 @@ __global__ void __launch_bounds__(NTH, MINB) k_rhs2d(DevMesh m, const double* __
         for (int k = 0; k < KA; ++k) {
             const int t = tid + k * NTH;
             if (t >= NA) break;
-            double r = 1.0, u = 0.0, v = 0.0, T = 0.0;
-            if (cd[k]) {
-                r = ld[k][0];
-                const double ir = 1.0 / r;
-                u = ld[k][1] * ir;
-                v = ld[k][2] * ir;
-                T = g.gamma * g.gm1 * (ld[k][3] - 0.5 * (ld[k][1] * u + ld[k][2] * v)) * ir;
-            }
+            // branch-free: holes carry valid (initial) states and points outside the mesh
+            // rho = 1, so the primitives are finite; no active stencil reads them
+            const double r = ld[k][0];
+            const double ir = 1.0 / r;
+            const double u = ld[k][1] * ir;
+            const double v = ld[k][2] * ir;
+            const double T = g.gamma * g.gm1 * (ld[k][3] - 0.5 * (ld[k][1] * u + ld[k][2] * v)) * ir;
             sh_c[t] = (uint16_t)cd[k];
             sh_r[t] = r;
             sh_uv[t] = make_double2(u, v);

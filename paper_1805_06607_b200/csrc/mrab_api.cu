@@ -108,6 +108,7 @@ struct mrab_ctx {
     std::vector<cudaEvent_t> evpool;
     size_t evnext = 0;
     bool overlap = true;
+    int* dflag = nullptr;          // device flag of the finite check (in the workspace)
 };
 
 // ----------------------------------------------------------------------------------------
@@ -192,6 +193,10 @@ static size_t plan_bytes(const Plan& P, bool dry, mrab_ctx* ctx, Bump* bump, boo
             void* a = take(nt * sizeof(int32_t));
             if (D) D->tiles = (int32_t*)a;
         }
+    }
+    {
+        void* f = take(256);
+        if (!dry) ctx->dflag = (int*)f;
     }
     return total + 1024;
 }
@@ -1023,10 +1028,18 @@ mrab_status mrab_get_state(mrab_ctx* c, int mesh, double* dst, double* t) {
     if (!c || mesh < 0 || mesh >= (int)c->md.size() || !dst) return fail(MRAB_E_INVALID, "bad arguments");
     const Plan& P = *c->P;
     CK(cudaStreamSynchronize(c->st));
-    const size_t bytes = (size_t)P.nc * P.meshes[mesh].npts * sizeof(double);
-    CK(cudaMemcpyAsync(dst, current_state(c, mesh), bytes, cudaMemcpyDefault, c->st));
+    const size_t n = (size_t)P.nc * P.meshes[mesh].npts;
+    const double* src = current_state(c, mesh);
+    CK(cudaMemsetAsync(c->dflag, 0, sizeof(int), c->st));
+    launch_finite(src, n, c->dflag, c->st);
+    CK(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDefault, c->st));
+    int bad = 0;
+    CK(cudaMemcpyAsync(&bad, c->dflag, sizeof(int), cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
     if (t) *t = (double)c->macro * P.S * P.h;
+    if (bad)
+        return fail(MRAB_E_NONFINITE, "mesh " + std::to_string(mesh) +
+                                          ": non-finite state (rhs blowup); the state was copied");
     return MRAB_OK;
 }
 

@@ -119,3 +119,18 @@ def test_eval_counts():
     ev1, pr, _ = ctx.counters()
     d = ev1 - ev0
     assert d[0] == 5 * 1 and d[1] == 5 * 4      # slow bg: 1 per macro step, fast inner: SR
+
+
+def test_nonfinite_reported():
+    """A blown-up state is reported as NONFINITE by mrab_get_state ("rhs blowup")."""
+    p = synth.make_config(1, "test")
+    plan = mrab.Plan(p)
+    ctx = mrab.Context(plan, p.q0)
+    bad = p.q0[1].copy()
+    bad[0, 5, 5] = np.nan
+    ctx.set_state(1, bad)
+    with pytest.raises(mrab.MrabError, match="NONFINITE"):
+        ctx.get_state(1)
+    q, _ = ctx.get_state(0)
+    assert np.all(np.isfinite(q))
+    ctx.close()
