@@ -80,6 +80,21 @@ __device__ __forceinline__ void gather2(const DevMesh& m, const DonorSet& ds, in
     }
 }
 
+// base + sum_k c_k src_k of component c at element offset up (NS history slots, all loads
+// independent so they are in flight together)
+template <int NS>
+__device__ __forceinline__ double epi_sum(const Epilogue& ep, unsigned uN, unsigned up, int c) {
+    const unsigned o = c * uN + up;
+    double v[NS + 1];
+    v[0] = __ldg(ep.base + o);
+#pragma unroll
+    for (int k = 0; k < NS; ++k) v[1 + k] = __ldg(ep.src[k] + o);
+    double y = v[0];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) y += ep.csrc[k] * v[1 + k];
+    return y;
+}
+
 }  // namespace
 
 template <bool VISC, bool CART, int TY, int MINB, int NTH>
@@ -130,12 +145,14 @@ __global__ void __launch_bounds__(NTH, MINB) k_rhs2d(DevMesh m, const double* __
                     if (m.periodic[1]) gj = gj < 0 ? gj + n1 : gj - n1; else ok = false;
                 }
                 if (ok) {
-                    const int64_t q = gi + (int64_t)n0 * gj;
+                    // 32-bit element offsets: one IMAD.WIDE per address (nc * npts < 2^32)
+                    const unsigned q = (unsigned)gi + (unsigned)n0 * (unsigned)gj;
+                    const unsigned uN = (unsigned)N;
                     cd[k] = m.cls[q];
                     ld[k][0] = __ldg(Q + q);
-                    ld[k][1] = __ldg(Q + N + q);
-                    ld[k][2] = __ldg(Q + 2 * N + q);
-                    ld[k][3] = __ldg(Q + 3 * N + q);
+                    ld[k][1] = __ldg(Q + (uN + q));
+                    ld[k][2] = __ldg(Q + (2 * uN + q));
+                    ld[k][3] = __ldg(Q + (3 * uN + q));
                 }
             }
         }
@@ -267,38 +284,32 @@ __global__ void __launch_bounds__(NTH, MINB) k_rhs2d(DevMesh m, const double* __
 
     // ---- phase C: divergence, SAT, epilogue ------------------------------------------
     if (fast) {
-        // interior tile: no closures, no SAT, no holes
+        // interior tile: no closures, no SAT, no holes; 32-bit element offsets (one
+        // IMAD.WIDE per address) and the history-ring length resolved per launch
+        const unsigned uN = (unsigned)N;
+        const int ns = ep.y_out ? ep.nsrc : -1;
         for (int t = tid; t < TX * TY; t += NTH) {
             const int a = t % TX, b = t / TX;
-            const int gi = i0 + a, gj = j0 + b;
-            const int64_t p = gi + (int64_t)n0 * gj;
+            const unsigned up = (unsigned)(i0 + a) + (unsigned)n0 * (unsigned)(j0 + b);
             const int f = (b + G3) * FX + (a + G3);
-            double yb[4] = {0, 0, 0, 0};
-            if (ep.y_out) {
-                const double* sp[4];
-                double cw[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    sp[k] = k < ep.nsrc ? ep.src[k] : ep.base;
-                    cw[k] = k < ep.nsrc ? ep.csrc[k] : 0.0;
-                }
-                double v[5][4];
+            double yb[4];
+            if (ns == 2) {
+                yb[0] = epi_sum<2>(ep, uN, up, 0); yb[1] = epi_sum<2>(ep, uN, up, 1);
+                yb[2] = epi_sum<2>(ep, uN, up, 2); yb[3] = epi_sum<2>(ep, uN, up, 3);
+            } else if (ns == 3) {
+                yb[0] = epi_sum<3>(ep, uN, up, 0); yb[1] = epi_sum<3>(ep, uN, up, 1);
+                yb[2] = epi_sum<3>(ep, uN, up, 2); yb[3] = epi_sum<3>(ep, uN, up, 3);
+            } else if (ns >= 0) {
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
-                    v[0][c] = __ldg(ep.base + c * N + p);
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) v[1 + k][c] = __ldg(sp[k] + c * N + p);
+                    double y = __ldg(ep.base + (c * uN + up));
+                    for (int k = 0; k < ns; ++k) y += ep.csrc[k] * __ldg(ep.src[k] + (c * uN + up));
+                    yb[c] = y;
                 }
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-                    yb[c] = v[0][c] + cw[0] * v[1][c] + cw[1] * v[2][c] + cw[2] * v[3][c] + cw[3] * v[4][c];
-                for (int k = 4; k < ep.nsrc; ++k)
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) yb[c] += ep.csrc[k] * __ldg(ep.src[k] + c * N + p);
             }
             const double2 x01 = d_int2(fh, f, 1), x23 = d_int2(fh + NF, f, 1);
             const double2 y01 = d_int2(fh + 2 * NF, f, FX), y23 = d_int2(fh + 3 * NF, f, FX);
-            const double Jp = CART ? m.cJ : __ldg(m.J + p);
+            const double Jp = CART ? m.cJ : __ldg(m.J + up);
             double R[4];
             R[0] = -Jp * (x01.x + y01.x);
             R[1] = -Jp * (x01.y + y01.y);
@@ -306,11 +317,11 @@ __global__ void __launch_bounds__(NTH, MINB) k_rhs2d(DevMesh m, const double* __
             R[3] = -Jp * (x23.y + y23.y);
             if (ep.r_out) {
 #pragma unroll
-                for (int c = 0; c < 4; ++c) ep.r_out[c * N + p] = R[c];
+                for (int c = 0; c < 4; ++c) ep.r_out[c * uN + up] = R[c];
             }
-            if (ep.y_out) {
+            if (ns >= 0) {
 #pragma unroll
-                for (int c = 0; c < 4; ++c) ep.y_out[c * N + p] = yb[c] + ep.c_new * R[c];
+                for (int c = 0; c < 4; ++c) ep.y_out[c * uN + up] = yb[c] + ep.c_new * R[c];
             }
         }
         return;
