@@ -50,6 +50,10 @@ struct Epilogue {
     // launch priority recorded on the launch itself (survives graph capture); 0 = default
     int prio;
     int has_prio;
+    // 2-D kernel L2 prefetch (set by the launcher): bit 0 = this tile's epilogue rows at
+    // kernel entry, bit 1 = the state rows of the tile `pf_ahead` tiles further on
+    int pf;
+    int pf_ahead;
 };
 
 // tile grid of the 2-D RHS kernel (for building tile lists on the host)

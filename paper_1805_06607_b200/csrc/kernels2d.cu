@@ -82,6 +82,10 @@ __device__ __forceinline__ void gather2(const DevMesh& m, const DonorSet& ds, in
 
 // base + sum_k c_k src_k of component c at element offset up (NS history slots, all loads
 // independent so they are in flight together)
+__device__ __forceinline__ void prefetch_l2(const double* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 template <int NS>
 __device__ __forceinline__ double epi_sum(const Epilogue& ep, unsigned uN, unsigned up, int c) {
     const unsigned o = c * uN + up;
@@ -121,6 +125,40 @@ __global__ void __launch_bounds__(NTH, MINB) k_rhs2d(DevMesh m, const double* __
     }
     const int i0 = bx * TX, j0 = by * TY;
     const int tid = threadIdx.x;
+
+    // ---- L2 prefetch: the epilogue's history rows (read last, in phase C) and the state
+    // rows of a tile of the next wave; turns their HBM latency into L2 latency
+    if (ep.pf) {
+        const unsigned uN = (unsigned)N;
+        if ((ep.pf & 1) && ep.y_out) {
+            // per history array: TY rows x 2 lines x 4 components
+            constexpr int NL = TY * 2 * 4;
+            for (int t = tid; t < NL; t += NTH) {
+                const int line = t & 1, row = (t >> 1) % TY, c = (t >> 1) / TY;
+                const int gj = j0 + row, gi = i0 + 16 * line;
+                if (gj >= n1 || gi >= n0) continue;
+                const unsigned o = c * uN + (unsigned)gi + (unsigned)n0 * (unsigned)gj;
+                prefetch_l2(ep.base + o);
+#pragma unroll
+                for (int k = 0; k < 3; ++k)
+                    if (k < ep.nsrc) prefetch_l2(ep.src[k] + o);
+            }
+        }
+        if ((ep.pf & 2) && !ep.tiles) {
+            const int ntx = gridDim.x;
+            const int nxt = by * ntx + bx + ep.pf_ahead;
+            const int ny = nxt / ntx, nx = nxt - ny * ntx;
+            if (ny < (int)gridDim.y) {
+                const int nl = TY * 2 * 4;
+                for (int t = tid; t < nl; t += NTH) {
+                    const int line = t & 1, row = (t >> 1) % TY, c = (t >> 1) / TY;
+                    const int gj = ny * TY + row, gi = nx * TX + 16 * line;
+                    if (gj >= n1 || gi >= n0) continue;
+                    prefetch_l2(Q + (c * uN + (unsigned)gi + (unsigned)n0 * (unsigned)gj));
+                }
+            }
+        }
+    }
 
     // ---- phase A: primitives of tile + halo ------------------------------------------
     constexpr int KA = (NA + NTH - 1) / NTH;
@@ -605,9 +643,20 @@ void launch_donor2d(const RecvTask& rt, const SrcSets& ss, const MeshTable& mt, 
 }
 
 template <bool VISC, bool CART, int TY, int MINB, int NTH>
-static void launch_t(const DevMesh& m, const double* Q, const Gas& g, const Epilogue& ep,
+static void launch_t(const DevMesh& m, const double* Q, const Gas& g, const Epilogue& ep0,
                      const DonorSet& ds, cudaStream_t st) {
     static bool init = false;
+    static int pf = -1, nsm = 0;
+    if (pf < 0) {
+        const char* e = getenv("MRAB_PF");
+        pf = e ? atoi(e) : 1;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    Epilogue ep = ep0;
+    ep.pf = pf;
+    ep.pf_ahead = MINB * nsm;
     const size_t bytes = Geo<VISC, TY>::bytes;
     if (!init) {
         cudaFuncSetAttribute(k_rhs2d<VISC, CART, TY, MINB, NTH>,
@@ -665,14 +714,18 @@ static void launch_v(const DevMesh& m, const double* Q, const Gas& g, const Epil
     }
 }
 
+bool launch_rhs2d_stream(const DevMesh& m, const double* Q, const Gas& g, const Epilogue& ep,
+                         cudaStream_t st);
 bool rhs2d_tma_possible(const DevMesh& m, const Epilogue& ep, const double* Q);
 bool launch_rhs2d_tma(const DevMesh& m, const double* Q, const Gas& g, const Epilogue& ep,
                       cudaStream_t st);
 
 void launch_rhs2d(const DevMesh& m, const double* Q, const Gas& g, const Epilogue& ep,
                   const DonorSet& ds, cudaStream_t st) {
-    // persistent TMA-pipelined kernel whenever its layout constraints hold
+    // persistent TMA-pipelined kernel whenever its layout constraints hold (opt-in)
     if (rhs2d_tma_possible(m, ep, Q) && launch_rhs2d_tma(m, Q, g, ep, st)) return;
+    // y-streaming tiles for meshes with more than one wave of tiles
+    if (launch_rhs2d_stream(m, Q, g, ep, st)) return;
     if (g.viscous) {
         if (m.cart) launch_v<true, true>(m, Q, g, ep, ds, st);
         else launch_v<true, false>(m, Q, g, ep, ds, st);

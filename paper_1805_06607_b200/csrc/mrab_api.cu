@@ -639,7 +639,7 @@ static void issue_macro_step_dag2d(mrab_ctx* c) {
                 cudaDeviceGetStreamPriorityRange(&least, &greatest);
                 int smin = S;
                 for (auto& q : P.meshes) smin = std::min(smin, q.s);
-                ep.has_prio = 1;
+                ep.has_prio = split ? 1 : 0;
                 ep.prio = mp.s == smin ? greatest : least;
             }
             if (split) {

@@ -110,6 +110,80 @@ static __device__ __forceinline__ void visc_at(const double2* __restrict__ sh_uv
 }
 
 
+// SAT penalties (eq:int P:279-299; corners sum both directions) at a segment-end
+// point of a 2-D tile, added to R.  qhat / fvhat come from k_donor2d.
+template <bool VISC, bool CART, int AX>
+static __device__ __forceinline__ void sat2d(const DevMesh& m, const double* __restrict__ Q,
+                                             const Gas& g, const double2* __restrict__ sh_uv,
+                                             const double* __restrict__ sh_T, int s, unsigned code,
+                                             int64_t p, int gi, int gj, double Jp, double* R) {
+    constexpr double kP0 = 17.0 / 48.0;
+    const int64_t N = m.npts;
+    const int cx = code & 15, cy = (code >> 4) & 15;
+    double q[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) q[c] = __ldg(Q + c * N + p);
+    double Vx[4] = {0, 0, 0, 0}, Vy[4] = {0, 0, 0, 0};
+    if (VISC) visc_at<CART, AX>(sh_uv, sh_T, s, code, m, p, g, Vx, Vy);
+    const int slot = m.recv_slot[p];
+    double qi[4] = {0, 0, 0, 0}, fvi[6] = {0, 0, 0, 0, 0, 0};
+    if (slot >= 0) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) qi[c] = m.qhat[c * m.nrecv + slot];
+        if (VISC)
+#pragma unroll
+            for (int c = 0; c < 6; ++c) fvi[c] = m.fvhat[c * m.nrecv + slot];
+    }
+    const int idx[2] = {gi, gj};
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int cl = k == 0 ? cx : cy;
+        if (cl != CLS_L0 && cl != CLS_R0) continue;
+        const int sidx = (cl == CLS_L0) ? 0 : 1;
+        const double side = (cl == CLS_L0) ? 1.0 : -1.0;
+        const bool at_face = !m.periodic[k] && (sidx == 0 ? idx[k] == 0 : idx[k] == m.n[k] - 1);
+        const int typ = at_face ? m.face_bc[k][sidx] : MRAB_BC_OVERSET;
+        double nv[2];
+        if (CART) {
+            nv[0] = k == 0 ? m.cJ * m.cM[0] : 0.0;
+            nv[1] = k == 1 ? m.cJ * m.cM[1] : 0.0;
+        } else {
+            nv[0] = Jp * __ldg(m.M + (2 * k) * N + p);
+            nv[1] = Jp * __ldg(m.M + (2 * k + 1) * N + p);
+        }
+        double qh[4];
+        if (typ == MRAB_BC_OVERSET) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) qh[c] = qi[c];
+        } else if (typ == MRAB_BC_FARFIELD) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) qh[c] = g.q_inf[c];
+        } else {
+            qh[0] = q[0];
+            qh[1] = 0.0;
+            qh[2] = 0.0;
+            qh[3] = q[0] * g.wall_T * g.igamma * g.igm1;
+        }
+        double dq[4], kd[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) dq[c] = q[c] - qh[c];
+        kchar2(q, nv, side, dq, g, kd);
+        double sig1 = 0.0;
+        if (VISC) sig1 = 0.5 * (nv[0] * nv[0] + nv[1] * nv[1]) * g.iRe;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) R[c] -= (0.5 * kd[c] + sig1 * dq[c]) / kP0;
+        if (VISC && typ != MRAB_BC_WALL) {
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const double fk = nv[0] * Vx[1 + j] + nv[1] * Vy[1 + j];
+                double fhv = 0.0;
+                if (typ == MRAB_BC_OVERSET) fhv = nv[0] * fvi[j] + nv[1] * fvi[3 + j];
+                R[1 + j] += 0.5 * side * (fk - fhv) / kP0;
+            }
+        }
+    }
+}
+
 // visc_at for a point whose rows are interior in both directions (compile-time stencils)
 template <bool CART, int AX>
 static __device__ __forceinline__ void visc_at_int(const double2* __restrict__ sh_uv,
