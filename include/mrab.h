@@ -154,6 +154,15 @@ mrab_status mrab_launches_per_macro_step(mrab_ctx* ctx, int64_t* launches);
 mrab_status mrab_time_kernel(mrab_ctx* ctx, int kernel, int mesh, int reps, int flush_l2,
                              double* ms_per_launch, double* algorithmic_bytes);
 
+/* Diagnostics: record a launch timeline of the 2-D MRAB step into `dev_buf` (device memory,
+ * u64: [0] record count (zero it before stepping), [1] capacity in records, then records of
+ * 5 u64 = (smid << 56 | CTA index << 16 | tag, CTA start ns, CTA end ns, 2-D RHS: end of
+ * phase A ns, end of phase B ns (last tile of the CTA), else 0) from %globaltimer; tag = kind << 12 |
+ * mesh << 8 | micro index, kind 1 RHS, 2 donor gather, 3 bulk part of a split RHS).  NULL
+ * turns it off.  Drops the captured step graphs (re-captured on the next step).  Not part of
+ * the hot path; synchronises. */
+mrab_status mrab_set_trace(mrab_ctx* ctx, void* dev_buf);
+
 /* Thread-local message of the last failing call on this thread. */
 const char* mrab_last_error(void);
 

@@ -25,6 +25,10 @@ struct DevMesh {
     const int32_t* rdonor;     // [R] donor mesh of each receiver
     const int32_t* rbase;      // [R][3] donor stencil base
     const double* rw;          // [R][3][4] per-axis Lagrange weights
+    // 2-D: tile list of the RHS kernel, every tile once, non-interior tiles first;
+    // bit 31 set = interior tile (see rhs2d_interior_tile); NULL = decide in the kernel
+    const int32_t* tlist;
+    int ntl;
 };
 
 struct Gas {
@@ -50,14 +54,21 @@ struct Epilogue {
     // launch priority recorded on the launch itself (survives graph capture); 0 = default
     int prio;
     int has_prio;
-    // 2-D kernel L2 prefetch (set by the launcher): bit 0 = this tile's epilogue rows at
-    // kernel entry, bit 1 = the state rows of the tile `pf_ahead` tiles further on
+    // 2-D kernel L2 prefetch (set by the launcher): bit 0 = this tile's epilogue rows
     int pf;
-    int pf_ahead;
+    // 2-D with a tile list: at most `persist` CTAs walk the list (0 = one CTA per tile)
+    int persist;
+    // launch timeline (mrab_set_trace; NULL = off): one record per CTA, see trace_rec
+    unsigned long long* trace;
+    int trace_tag;
 };
 
 // tile grid of the 2-D RHS kernel (for building tile lists on the host)
 void rhs2d_tile_shape(int* tx, int* ty);
+// host: true if tile (bx, by) of a 2-D mesh may take the kernel's interior fast path: the
+// tile is full, its primitive halo (H = 6 viscous / 3 Euler) lies inside the mesh without
+// periodic wrap, and every flux point (tile + 3) is interior in both directions
+bool rhs2d_interior_tile(const int* n, const uint16_t* cls, int viscous, int bx, int by);
 
 struct Box {
     int lo[3];
@@ -103,6 +114,8 @@ struct RecvTask {
     double* fvhat[8];
     int64_t nrecv[8];
     int set[8];                     // which SrcSet (evaluation time) each entry reads
+    unsigned long long* trace;      // launch timeline (NULL = off)
+    int trace_tag;
 };
 
 struct SrcSets {
@@ -134,5 +147,30 @@ void upload_stencil_rows();
 void launch_l2_scrub(void* a, void* b, size_t bytes, int tag, cudaStream_t st);
 // sets *flag (device int) if any of the n doubles is not finite
 void launch_finite(const double* a, size_t n, int* flag, cudaStream_t st);
+
+#ifdef __CUDACC__
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// trace buffer: [0] record count, [1] capacity (records), then records of 5 u64:
+// (smid << 56 | blockIdx.x << 16 | tag, CTA start ns, CTA end ns, two phase marks or 0)
+__device__ __forceinline__ void trace_rec(unsigned long long* buf, int tag, unsigned long long t0,
+                                          unsigned long long ta = 0, unsigned long long tb = 0) {
+    const unsigned long long i = atomicAdd(buf, 1ull);
+    if (i < buf[1]) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        unsigned long long* rec = buf + 2 + 5 * i;
+        rec[0] = ((unsigned long long)smid << 56) | ((unsigned long long)blockIdx.x << 16) |
+                 (unsigned)(tag & 0xffff);
+        rec[1] = t0;
+        rec[2] = gtimer();
+        rec[3] = ta;
+        rec[4] = tb;
+    }
+}
+#endif
 
 }  // namespace mrab

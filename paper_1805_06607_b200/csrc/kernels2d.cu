@@ -16,6 +16,8 @@
 // 16-byte shared load serves two fields.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include <cstdlib>
 
 #include "kernels.cuh"
@@ -101,13 +103,14 @@ __device__ __forceinline__ double epi_sum(const Epilogue& ep, unsigned uN, unsig
 
 }  // namespace
 
-template <bool VISC, bool CART, int TY, int MINB, int NTH>
-__global__ void __launch_bounds__(NTH, MINB) k_rhs2d(DevMesh m, const double* __restrict__ Q, Gas g,
-                                                    Epilogue ep, DonorSet ds) {
+// one tile (bx, by); tfast = 1 interior tile, 0 general, -1 decide from the class codes
+template <bool VISC, bool CART, int TY, int NTH>
+__device__ __forceinline__ void rhs2d_tile(const DevMesh& m, const double* __restrict__ Q,
+                                           const Gas& g, const Epilogue& ep, int bx, int by,
+                                           int tfast, double* smem, unsigned long long* tph) {
     using GG = Geo<VISC, TY>;
     constexpr int H = GG::H, AX = GG::AX, FX = GG::FX;
     constexpr int NA = GG::NA, NF = GG::NF;
-    extern __shared__ __align__(16) double smem[];
     double2* sh_uv = reinterpret_cast<double2*>(smem);
     double2* fh = sh_uv + NA;                       // [4][NF]
     double* sh_r = reinterpret_cast<double*>(fh + 4 * NF);
@@ -116,18 +119,10 @@ __global__ void __launch_bounds__(NTH, MINB) k_rhs2d(DevMesh m, const double* __
 
     const int n0 = m.n[0], n1 = m.n[1];
     const int64_t N = m.npts;
-    int bx = blockIdx.x, by = blockIdx.y;
-    if (ep.tiles) {
-        const int ntx = (m.n[0] + TX - 1) / TX;
-        const int tl = ep.tiles[blockIdx.x];
-        by = tl / ntx;
-        bx = tl - by * ntx;
-    }
     const int i0 = bx * TX, j0 = by * TY;
     const int tid = threadIdx.x;
 
-    // ---- L2 prefetch: the epilogue's history rows (read last, in phase C) and the state
-    // rows of a tile of the next wave; turns their HBM latency into L2 latency
+    // ---- L2 prefetch of the epilogue's history rows (read last, in phase C)
     if (ep.pf) {
         const unsigned uN = (unsigned)N;
         if ((ep.pf & 1) && ep.y_out) {
@@ -144,26 +139,44 @@ __global__ void __launch_bounds__(NTH, MINB) k_rhs2d(DevMesh m, const double* __
                     if (k < ep.nsrc) prefetch_l2(ep.src[k] + o);
             }
         }
-        if ((ep.pf & 2) && !ep.tiles) {
-            const int ntx = gridDim.x;
-            const int nxt = by * ntx + bx + ep.pf_ahead;
-            const int ny = nxt / ntx, nx = nxt - ny * ntx;
-            if (ny < (int)gridDim.y) {
-                const int nl = TY * 2 * 4;
-                for (int t = tid; t < nl; t += NTH) {
-                    const int line = t & 1, row = (t >> 1) % TY, c = (t >> 1) / TY;
-                    const int gj = ny * TY + row, gi = nx * TX + 16 * line;
-                    if (gj >= n1 || gi >= n0) continue;
-                    prefetch_l2(Q + (c * uN + (unsigned)gi + (unsigned)n0 * (unsigned)gj));
-                }
-            }
-        }
     }
 
     // ---- phase A: primitives of tile + halo ------------------------------------------
     constexpr int KA = (NA + NTH - 1) / NTH;
     int allint = 1;
-    {
+    if (tfast == 1) {
+        // interior tile: halo inside the mesh, no class codes needed by phases B / C
+        const unsigned uN = (unsigned)N;
+        const unsigned q0 = (unsigned)(i0 - H) + (unsigned)n0 * (unsigned)(j0 - H);
+        double ld[KA][4];
+#pragma unroll
+        for (int k = 0; k < KA; ++k) {
+            const int t = tid + k * NTH;
+            ld[k][0] = 1.0;
+            ld[k][1] = ld[k][2] = ld[k][3] = 0.0;
+            if (t < NA) {
+                const int bb = t / AX, a = t - bb * AX;
+                const unsigned q = q0 + (unsigned)a + (unsigned)n0 * (unsigned)bb;
+                ld[k][0] = __ldg(Q + q);
+                ld[k][1] = __ldg(Q + (uN + q));
+                ld[k][2] = __ldg(Q + (2 * uN + q));
+                ld[k][3] = __ldg(Q + (3 * uN + q));
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < KA; ++k) {
+            const int t = tid + k * NTH;
+            if (t >= NA) break;
+            const double r = ld[k][0];
+            const double ir = 1.0 / r;
+            const double u = ld[k][1] * ir;
+            const double v = ld[k][2] * ir;
+            const double T = g.gamma * g.gm1 * (ld[k][3] - 0.5 * (ld[k][1] * u + ld[k][2] * v)) * ir;
+            sh_r[t] = r;
+            sh_uv[t] = make_double2(u, v);
+            sh_T[t] = T;
+        }
+    } else {
         double ld[KA][4];
         unsigned cd[KA];
 #pragma unroll
@@ -216,7 +229,9 @@ __global__ void __launch_bounds__(NTH, MINB) k_rhs2d(DevMesh m, const double* __
                 allint = 0;
         }
     }
+    if (tfast == 0) allint = 0;
     const int fast = __syncthreads_and(allint);
+    if (ep.trace && threadIdx.x == 0) tph[0] = gtimer();
 
     // ---- phase B: contravariant fluxes at tile + 3 -----------------------------------
     if (fast) {
@@ -319,6 +334,7 @@ __global__ void __launch_bounds__(NTH, MINB) k_rhs2d(DevMesh m, const double* __
         fh[3 * NF + t] = make_double2(fy[2], fy[3]);
     }
     __syncthreads();
+    if (ep.trace && threadIdx.x == 0) tph[1] = gtimer();
 
     // ---- phase C: divergence, SAT, epilogue ------------------------------------------
     if (fast) {
@@ -499,6 +515,40 @@ __global__ void __launch_bounds__(NTH, MINB) k_rhs2d(DevMesh m, const double* __
     }
 }
 
+
+// tile lists (host-built, mrab_api.cu): bit 31 marks an interior tile -- full, halo inside
+// the mesh without periodic wrap, every flux point interior in both directions.  With
+// ep.persist the grid is smaller than the list and each CTA walks tiles blockIdx.x,
+// blockIdx.x + gridDim.x, ... (a bulk launch that leaves SM slots to concurrent substeps).
+template <bool VISC, bool CART, int TY, int MINB, int NTH>
+__global__ void __launch_bounds__(NTH, MINB) k_rhs2d(DevMesh m, const double* __restrict__ Q, Gas g,
+                                                    Epilogue ep, DonorSet ds) {
+    extern __shared__ __align__(16) double smem[];
+    unsigned long long t0 = 0, tph[2] = {0, 0};
+    if (ep.trace && threadIdx.x == 0) t0 = gtimer();
+    const int32_t* tlist = ep.tiles ? ep.tiles : m.tlist;
+    const int ntl = ep.tiles ? ep.ntiles : m.ntl;
+    const int ntx = (m.n[0] + TX - 1) / TX;
+    for (int it = blockIdx.x;;) {
+        int bx = it, by = blockIdx.y, tf = -1;
+        if (tlist) {
+            const unsigned raw = (unsigned)tlist[it];
+            const int tl = (int)(raw & 0x7fffffffu);
+            by = tl / ntx;
+            bx = tl - by * ntx;
+            tf = (int)(raw >> 31);
+        }
+        rhs2d_tile<VISC, CART, TY, NTH>(m, Q, g, ep, bx, by, tf, smem, tph);
+        it += gridDim.x;
+        if (!tlist || it >= ntl) break;
+        __syncthreads();   // the previous tile's shared data is dead
+    }
+    if (ep.trace) {
+        __syncthreads();
+        if (threadIdx.x == 0) trace_rec(ep.trace, ep.trace_tag, t0, tph[0], tph[1]);
+    }
+}
+
 // ------------------------------------------------------------------------------------
 // donor kernel (2-D): state on the fly + viscous flux + Lagrange gather per receiver
 // ------------------------------------------------------------------------------------
@@ -521,6 +571,8 @@ __device__ __forceinline__ void src_prim(const SrcSet& ss, int h, int64_t N, int
 
 template <bool VISC>
 __global__ void __launch_bounds__(128) k_donor2d(RecvTask rt, SrcSets sets, MeshTable mt, Gas g) {
+    unsigned long long t0 = 0;
+    if (rt.trace && threadIdx.x == 0) t0 = gtimer();
     const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 4;
     const int a = threadIdx.x & 15;
     int rm = 0;
@@ -616,6 +668,188 @@ __global__ void __launch_bounds__(128) k_donor2d(RecvTask rt, SrcSets sets, Mesh
 #pragma unroll
             for (int c = 0; c < 6; ++c) rt.fvhat[rm][c * R + r] = acc[4 + c];
     }
+    if (rt.trace) {
+        __syncthreads();
+        if (threadIdx.x == 0) trace_rec(rt.trace, rt.trace_tag, t0);
+    }
+}
+
+// Region-staged variant: the 16 lanes of a receiver first form the donor state at the
+// plus-shaped region every SBP row of the 4 x 4 stencil can reach (rows of the stencil
+// +-3 along xi, columns +-3 along eta: 64 points, 4 per lane, all loads independent), keep
+// the primitives (u, v, T) in shared memory, then take the segmented D1 from there.  Same
+// arithmetic as k_donor2d, ~3x fewer global loads and no dependent load chains.
+constexpr int RG = 10;                 // region box edge (-3 .. 6)
+template <bool VISC>
+__global__ void __launch_bounds__(128) k_donor2d_r(RecvTask rt, SrcSets sets, MeshTable mt, Gas g) {
+    __shared__ double sh_p[8][3][RG * RG];     // (u, v, T) of the region, per receiver
+    __shared__ double sh_q[8][4][16];          // state at the 16 stencil points
+    unsigned long long t0 = 0;
+    if (rt.trace && threadIdx.x == 0) t0 = gtimer();
+    const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 4;
+    const int a = threadIdx.x & 15;
+    const int slot = threadIdx.x >> 4;
+    int rm = 0;
+    while (rm < rt.nmesh - 1 && gid >= rt.off[rm + 1]) ++rm;
+    const bool live = gid < rt.off[rt.nmesh];
+    const int64_t r = gid - rt.off[rm];
+    const SrcSet& ss = sets.s[rt.set[rm]];
+    int h = 0, ib = 0, jb = 0;
+    if (live) {
+        h = rt.rdonor[rm][r];
+        ib = rt.rbase[rm][3 * r];
+        jb = rt.rbase[rm][3 * r + 1];
+    }
+    const DevMesh& m = mt.m[h];
+    const int n0 = m.n[0], n1 = m.n[1];
+    const unsigned uN = (unsigned)m.npts;
+    const int ns = ss.nsrc[h];
+    // ---- stage the region ----
+    if (live) {
+        double ld[4][4];
+        bool ok[4];
+        int di[4], dj[4];
+#pragma unroll
+        for (int s4 = 0; s4 < 4; ++s4) {
+            const int k = a + 16 * s4;
+            if (k < 40) {
+                dj[s4] = k / 10;
+                di[s4] = k % 10 - 3;
+            } else {
+                const int kk = k - 40, r6 = kk >> 2;
+                di[s4] = kk & 3;
+                dj[s4] = r6 < 3 ? r6 - 3 : r6 + 1;
+            }
+            if (!VISC && !(dj[s4] >= 0 && dj[s4] < 4 && di[s4] >= 0 && di[s4] < 4)) {
+                ok[s4] = false;
+                continue;
+            }
+            int ii = ib + di[s4], jj = jb + dj[s4];
+            ok[s4] = true;
+            if (ii < 0 || ii >= n0) {
+                if (m.periodic[0]) ii = ii < 0 ? ii + n0 : ii - n0; else ok[s4] = false;
+            }
+            if (jj < 0 || jj >= n1) {
+                if (m.periodic[1]) jj = jj < 0 ? jj + n1 : jj - n1; else ok[s4] = false;
+            }
+            const unsigned q = (unsigned)ii + (unsigned)n0 * (unsigned)jj;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                double v = 0.0;
+                if (ok[s4]) {
+                    v = __ldg(ss.base[h] + (c * uN + q));
+#pragma unroll
+                    for (int t = 0; t < 4; ++t)
+                        if (t < ns) v += ss.c[h][t] * __ldg(ss.src[h][t] + (c * uN + q));
+                }
+                ld[s4][c] = v;
+            }
+        }
+#pragma unroll
+        for (int s4 = 0; s4 < 4; ++s4) {
+            const int e = (dj[s4] + 3) * RG + (di[s4] + 3);
+            if (dj[s4] >= 0 && dj[s4] < 4 && di[s4] >= 0 && di[s4] < 4) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) sh_q[slot][c][dj[s4] * 4 + di[s4]] = ld[s4][c];
+            }
+            if (VISC) {
+                double u = 0.0, v = 0.0, T = 0.0;
+                if (ok[s4]) {
+                    const double ir = 1.0 / ld[s4][0];
+                    u = ld[s4][1] * ir;
+                    v = ld[s4][2] * ir;
+                    T = g.gamma * g.gm1 * (ld[s4][3] - 0.5 * (ld[s4][1] * u + ld[s4][2] * v)) * ir;
+                }
+                sh_p[slot][0][e] = u;
+                sh_p[slot][1][e] = v;
+                sh_p[slot][2][e] = T;
+            }
+        }
+    }
+    __syncwarp();
+    double acc[10];
+#pragma unroll
+    for (int c = 0; c < 10; ++c) acc[c] = 0.0;
+    if (live) {
+        const int ai = a & 3, aj = a >> 2;
+        int ii = ib + ai, jj = jb + aj;
+        if (ii >= n0) ii -= n0;
+        if (jj >= n1) jj -= n1;
+        const double* w = rt.rw[rm] + 12 * r;
+        const double W = w[ai] * w[4 + aj];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[c] = W * sh_q[slot][c][a];
+        if (VISC) {
+            const unsigned q = (unsigned)ii + (unsigned)n0 * (unsigned)jj;
+            const unsigned code = m.cls[q];
+            const int cl[2] = {(int)(code & 15), (int)((code >> 4) & 15)};
+            const int e0 = (aj + 3) * RG + (ai + 3);
+            const int stride[2] = {1, RG};
+            double d[2][3];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                d[k][0] = d[k][1] = d[k][2] = 0.0;
+                const int nt = c_nst[cl[k]];
+                for (int t = 0; t < nt; ++t) {
+                    const int e = e0 + c_off[cl[k]][t] * stride[k];
+                    const double cf = c_cf[cl[k]][t];
+                    d[k][0] += cf * sh_p[slot][0][e];
+                    d[k][1] += cf * sh_p[slot][1][e];
+                    d[k][2] += cf * sh_p[slot][2][e];
+                }
+            }
+            double gx[3], gy[3];
+            if (m.cart) {
+                const double sx = m.cJ * m.cM[0], sy = m.cJ * m.cM[1];
+#pragma unroll
+                for (int f = 0; f < 3; ++f) {
+                    gx[f] = sx * d[0][f];
+                    gy[f] = sy * d[1][f];
+                }
+            } else {
+                const double J = __ldg(m.J + q);
+                const double Mxx = __ldg(m.M + q), Mxy = __ldg(m.M + uN + q);
+                const double Myx = __ldg(m.M + 2 * uN + q), Myy = __ldg(m.M + 3 * uN + q);
+#pragma unroll
+                for (int f = 0; f < 3; ++f) {
+                    gx[f] = J * (Mxx * d[0][f] + Myx * d[1][f]);
+                    gy[f] = J * (Mxy * d[0][f] + Myy * d[1][f]);
+                }
+            }
+            const double u = sh_p[slot][0][e0], v = sh_p[slot][1][e0];
+            const double div = gx[0] + gy[1];
+            const double txx = (2.0 * gx[0] - (2.0 / 3.0) * div) * g.iRe;
+            const double tyy = (2.0 * gy[1] - (2.0 / 3.0) * div) * g.iRe;
+            const double txy = (gy[0] + gx[1]) * g.iRe;
+            acc[4] = W * txx;
+            acc[5] = W * txy;
+            acc[6] = W * (u * txx + v * txy + g.kT * gx[2]);
+            acc[7] = W * txy;
+            acc[8] = W * tyy;
+            acc[9] = W * (u * txy + v * tyy + g.kT * gy[2]);
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < 10; ++c) {
+        double v = acc[c];
+        v += __shfl_xor_sync(0xffffffffu, v, 8);
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        acc[c] = v;
+    }
+    if (live && a == 0) {
+        const int64_t R = rt.nrecv[rm];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) rt.qhat[rm][c * R + r] = acc[c];
+        if (VISC)
+#pragma unroll
+            for (int c = 0; c < 6; ++c) rt.fvhat[rm][c * R + r] = acc[4 + c];
+    }
+    if (rt.trace) {
+        __syncthreads();
+        if (threadIdx.x == 0) trace_rec(rt.trace, rt.trace_tag, t0);
+    }
 }
 
 void launch_donor2d(const RecvTask& rt, const SrcSets& ss, const MeshTable& mt, const Gas& gas,
@@ -638,25 +872,31 @@ void launch_donor2d(const RecvTask& rt, const SrcSets& ss, const MeshTable& mt, 
     at[0].val.priority = greatest;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    if (gas.viscous) cudaLaunchKernelEx(&cfg, k_donor2d<true>, rt, ss, mt, gas);
-    else cudaLaunchKernelEx(&cfg, k_donor2d<false>, rt, ss, mt, gas);
+    static int staged = -1;
+    if (staged < 0) {
+        const char* e = getenv("MRAB_DONOR_STAGED");
+        staged = e ? atoi(e) : 1;
+    }
+    if (staged) {
+        if (gas.viscous) cudaLaunchKernelEx(&cfg, k_donor2d_r<true>, rt, ss, mt, gas);
+        else cudaLaunchKernelEx(&cfg, k_donor2d_r<false>, rt, ss, mt, gas);
+    } else {
+        if (gas.viscous) cudaLaunchKernelEx(&cfg, k_donor2d<true>, rt, ss, mt, gas);
+        else cudaLaunchKernelEx(&cfg, k_donor2d<false>, rt, ss, mt, gas);
+    }
 }
 
 template <bool VISC, bool CART, int TY, int MINB, int NTH>
 static void launch_t(const DevMesh& m, const double* Q, const Gas& g, const Epilogue& ep0,
                      const DonorSet& ds, cudaStream_t st) {
     static bool init = false;
-    static int pf = -1, nsm = 0;
+    static int pf = -1;
     if (pf < 0) {
         const char* e = getenv("MRAB_PF");
         pf = e ? atoi(e) : 1;
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     }
     Epilogue ep = ep0;
     ep.pf = pf;
-    ep.pf_ahead = MINB * nsm;
     const size_t bytes = Geo<VISC, TY>::bytes;
     if (!init) {
         cudaFuncSetAttribute(k_rhs2d<VISC, CART, TY, MINB, NTH>,
@@ -664,7 +904,8 @@ static void launch_t(const DevMesh& m, const double* Q, const Gas& g, const Epil
         init = true;
     }
     dim3 grid((m.n[0] + TX - 1) / TX, (m.n[1] + TY - 1) / TY);
-    if (ep.tiles) grid = dim3(ep.ntiles, 1);
+    if (ep.tiles) grid = dim3(ep.persist > 0 ? std::min(ep.persist, ep.ntiles) : ep.ntiles, 1);
+    else if (m.tlist) grid = dim3(m.ntl, 1);
     if (grid.x * grid.y == 0) return;
     if (ep.has_prio) {
         cudaLaunchConfig_t cfg = {};
@@ -694,6 +935,20 @@ static int k2d_variant() {
         if (v < 0 || v > 4) v = 0;
     }
     return v;
+}
+
+bool rhs2d_interior_tile(const int* n, const uint16_t* cls, int viscous, int bx, int by) {
+    int tx, ty;
+    rhs2d_tile_shape(&tx, &ty);
+    const int H = viscous ? Geo<true, 16>::H : Geo<false, 16>::H;
+    const int i0 = bx * tx, j0 = by * ty;
+    if (i0 + tx > n[0] || j0 + ty > n[1]) return false;
+    if (i0 - H < 0 || j0 - H < 0 || i0 + tx + H > n[0] || j0 + ty + H > n[1]) return false;
+    const unsigned want = CLS_INT | (CLS_INT << 4);
+    for (int j = j0 - G3; j < j0 + ty + G3; ++j)
+        for (int i = i0 - G3; i < i0 + tx + G3; ++i)
+            if (cls[i + (size_t)n[0] * j] != want) return false;
+    return true;
 }
 
 void rhs2d_tile_shape(int* tx, int* ty) {

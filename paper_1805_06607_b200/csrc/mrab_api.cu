@@ -61,6 +61,7 @@ struct MeshDev {
     double* qhat = nullptr;       // [S][nc][R]: one set per micro index j (batched gathers)
     double* fvhat = nullptr;      // [S][d(d+1)][R]
     int32_t* tiles = nullptr;     // 2-D: critical tiles (cover the donor box) then the bulk
+    int32_t* tlist = nullptr;     // 2-D: all tiles, non-interior first (bit 31 = interior)
     int ncrit = 0, nbulk = 0;
     DevMesh dm{};
 };
@@ -109,6 +110,8 @@ struct mrab_ctx {
     size_t evnext = 0;
     bool overlap = true;
     int* dflag = nullptr;          // device flag of the finite check (in the workspace)
+    int bulk_ctas = 0;             // persistent CTAs of a bulk launch (0 = one per tile)
+    unsigned long long* trace = nullptr;   // launch timeline buffer (mrab_set_trace)
 };
 
 // ----------------------------------------------------------------------------------------
@@ -191,7 +194,11 @@ static size_t plan_bytes(const Plan& P, bool dry, mrab_ctx* ctx, Bump* bump, boo
             rhs2d_tile_shape(&tx, &ty);
             const size_t nt = (size_t)((m.n[0] + tx - 1) / tx) * ((m.n[1] + ty - 1) / ty);
             void* a = take(nt * sizeof(int32_t));
-            if (D) D->tiles = (int32_t*)a;
+            void* b = take(nt * sizeof(int32_t));
+            if (D) {
+                D->tiles = (int32_t*)a;
+                D->tlist = (int32_t*)b;
+            }
         }
     }
     {
@@ -292,6 +299,8 @@ static void issue_donor2d_tasks(mrab_ctx* c, const std::vector<GatherTask>& task
         rt.off[k + 1] = rt.off[k] + rt.nrecv[k];
     }
     if (rt.nmesh == 0) return;
+    rt.trace = c->trace;
+    rt.trace_tag = (2 << 12) | (tasks[0].g << 8) | (tasks[0].j & 0xff);
     MeshTable mt{};
     for (size_t h = 0; h < P.meshes.size(); ++h) mt.m[h] = c->md[h].dm;
     launch_donor2d(rt, sets, mt, c->gas, st);
@@ -642,6 +651,8 @@ static void issue_macro_step_dag2d(mrab_ctx* c) {
                 ep.has_prio = split ? 1 : 0;
                 ep.prio = mp.s == smin ? greatest : least;
             }
+            ep.trace = c->trace;
+            ep.trace_tag = (1 << 12) | (g << 8) | (j & 0xff);
             if (split) {
                 Epilogue e1 = ep;
                 e1.tiles = D.tiles;
@@ -651,6 +662,8 @@ static void issue_macro_step_dag2d(mrab_ctx* c) {
                 Epilogue e2 = ep;
                 e2.tiles = D.tiles + D.ncrit;
                 e2.ntiles = D.nbulk;
+                e2.persist = c->bulk_ctas;
+                e2.trace_tag = (3 << 12) | (g << 8) | (j & 0xff);
                 launch_rhs(2, dm, ep.base, D.FV, c->gas, e2, ds, c->side[g]);
                 c->launch_counter += 2;
                 last_full[g] = dag_done(c, g);
@@ -860,6 +873,13 @@ mrab_status mrab_create(const mrab_plan* plan, const double* const* q0, void* d_
         // the critical/bulk split is off by default: measured slower on config 3 (the bulk
         // tiles occupy every SM and delay the fast substeps); MRAB_OVERLAP=1 enables it
         c->overlap = ov && ov[0] == '1';
+        // the bulk launch walks its tiles with one CTA per SM by default, so each SM keeps
+        // room for a CTA of the fast meshes' substeps
+        int dev = 0, nsm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        const char* bc = getenv("MRAB_BULK_CTAS");
+        c->bulk_ctas = bc ? atoi(bc) : nsm;
     }
     CK(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
@@ -925,19 +945,30 @@ mrab_status mrab_create(const mrab_plan* plan, const double* const* q0, void* d_
             int tx, ty;
             rhs2d_tile_shape(&tx, &ty);
             const int ntx = (m.n[0] + tx - 1) / tx, nty = (m.n[1] + ty - 1) / ty;
-            std::vector<int32_t> crit, bulk;
+            std::vector<int32_t> crit, bulk, slow, fastl;
+            static const bool tag = [] {
+                const char* e = getenv("MRAB_TILE_FLAGS");
+                return !(e && e[0] == '0');
+            }();
             for (int by = 0; by < nty; ++by)
                 for (int bx = 0; bx < ntx; ++bx) {
-                    const int t = by * ntx + bx;
+                    const bool interior = tag && rhs2d_interior_tile(m.n, m.cls.data(), P.viscous, bx, by);
+                    const int32_t t = (by * ntx + bx) | (interior ? (int32_t)0x80000000u : 0);
                     const bool meets = m.is_donor && bx * tx <= m.st_hi[0] &&
                                        bx * tx + tx - 1 >= m.st_lo[0] && by * ty <= m.st_hi[1] &&
                                        by * ty + ty - 1 >= m.st_lo[1];
                     (meets ? crit : bulk).push_back(t);
+                    (interior ? fastl : slow).push_back(t);
                 }
             D.ncrit = (int)crit.size();
             D.nbulk = (int)bulk.size();
             crit.insert(crit.end(), bulk.begin(), bulk.end());
             CK(cudaMemcpy(D.tiles, crit.data(), crit.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+            // the longer non-interior tiles go first so they do not form the tail
+            slow.insert(slow.end(), fastl.begin(), fastl.end());
+            CK(cudaMemcpy(D.tlist, slow.data(), slow.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+            dm.tlist = D.tlist;
+            dm.ntl = (int)slow.size();
         }
         dm.nrecv = (int64_t)R;
         c->book.head[g] = P.history_m - 1;   // empty ring: the first push goes to slot 0
@@ -1089,6 +1120,18 @@ mrab_status mrab_get_counters(mrab_ctx* c, int64_t* rhs_evals, int64_t* point_rh
     }
     if (point_rhs) *point_rhs = pr;
     if (macro_steps) *macro_steps = c->macro;
+    return MRAB_OK;
+}
+
+mrab_status mrab_set_trace(mrab_ctx* c, void* dev_buf) {
+    if (!c) return fail(MRAB_E_INVALID, "bad ctx");
+    CK(cudaStreamSynchronize(c->st));
+    for (auto& g : c->graphs)
+        if (g) {
+            cudaGraphExecDestroy(g);
+            g = nullptr;
+        }
+    c->trace = (unsigned long long*)dev_buf;
     return MRAB_OK;
 }
 

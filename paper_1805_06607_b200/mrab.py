@@ -70,6 +70,7 @@ def lib():
         L.mrab_get_counters.argtypes = [vp, i64p, i64p, i64p]
         L.mrab_launches_per_macro_step.argtypes = [vp, i64p]
         L.mrab_time_kernel.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, dp, dp]
+        L.mrab_set_trace.argtypes = [vp, vp]
         L.mrab_last_error.restype = C.c_char_p
         for name in ("mrab_ab_weights", "mrab_plan_create", "mrab_plan_info",
                      "mrab_plan_get_tables", "mrab_plan_get_metrics", "mrab_create",
@@ -84,7 +85,7 @@ EXPORTED = ["mrab_ab_weights", "mrab_plan_create", "mrab_plan_destroy", "mrab_pl
             "mrab_plan_get_tables", "mrab_plan_get_metrics", "mrab_workspace_bytes",
             "mrab_create", "mrab_destroy", "mrab_step", "mrab_get_state", "mrab_set_state",
             "mrab_rhs", "mrab_get_counters", "mrab_launches_per_macro_step", "mrab_time_kernel",
-            "mrab_last_error"]
+            "mrab_set_trace", "mrab_last_error"]
 
 
 def _check(st):
@@ -249,6 +250,11 @@ class Context:
         v = C.c_int64()
         _check(lib().mrab_launches_per_macro_step(self.h, C.byref(v)))
         return v.value
+
+    def set_trace(self, dev_ptr):
+        """Diagnostics: record the launch timeline of the 2-D step into a device u64 buffer
+        (mrab_set_trace; dev_ptr 0 turns it off)."""
+        _check(lib().mrab_set_trace(self.h, C.c_void_p(int(dev_ptr)) if dev_ptr else None))
 
     def time_kernel(self, kernel, g, reps=20, flush_l2=True):
         """(ms per launch, algorithmic bytes per launch) of kernel 0 = fused RHS+SAT+AB,
