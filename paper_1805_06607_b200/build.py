@@ -10,7 +10,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libmrab.so")
-SOURCES = ["mrab_api.cu", "kernels.cu", "kernels2d.cu", "kernels2d_tma.cu", "kernels2d_stream.cu", "host_setup.cpp"]
+SOURCES = ["mrab_api.cu", "kernels.cu", "kernels2d.cu", "kernels2d_tma.cu", "kernels2d_stream.cu", "kernels2d_march.cu",
+           "host_setup.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
@@ -32,19 +33,32 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
-    objs = []
-    for s in SOURCES:
+    # headers are shared by every translation unit: a changed header rebuilds all objects
+    hdrs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
+    hdrs.append(os.path.join(os.path.dirname(HERE), "include", "mrab.h"))
+    newest_hdr = max(os.path.getmtime(h) for h in hdrs)
+
+    def compile_one(s):
         src = os.path.join(CSRC, s)
         obj = os.path.join(LIBDIR, s + ".o")
+        if (not force and os.path.exists(obj)
+                and os.path.getmtime(obj) > max(os.path.getmtime(src), newest_hdr)):
+            return obj, ""
         cmd = [NVCC, *FLAGS, "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {s}:\n{r.stderr}")
-        if verbose:
-            sys.stderr.write(r.stderr)
         with open(os.path.join(LIBDIR, s + ".ptxas.log"), "w") as f:
             f.write(r.stderr)
-        objs.append(obj)
+        return obj, r.stderr
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        res = list(ex.map(compile_one, SOURCES))
+    objs = [o for o, _ in res]
+    if verbose:
+        for _, e in res:
+            sys.stderr.write(e)
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", LIB,
            "-Xcompiler", "-fopenmp", "-cudart", "static"]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -35,7 +35,7 @@ __device__ __forceinline__ void prim(const double* __restrict__ Q, int64_t q, in
                                      double gamma, double& rho, double* u, double& p,
                                      double& E) {
     rho = __ldg(Q + q);
-    double ir = 1.0 / rho;
+    double ir = rcp64(rho);
     double ke = 0.0;
 #pragma unroll
     for (int i = 0; i < D; ++i) {
@@ -410,7 +410,7 @@ __global__ void __launch_bounds__(NT3, 2) k_rhs3d(DevMesh m, const double* __res
             const int t = tid + r * NT3;
             if (t >= (T3X + 2 * ex) * (T3Y + 2 * ey) * (T3Z + 2 * ez)) break;
             const double rho = lq[r][0];
-            const double ir = 1.0 / rho;
+            const double ir = rcp64(rho);
             const double u[3] = {lq[r][1] * ir, lq[r][2] * ir, lq[r][3] * ir};
             const double E = lq[r][4];
             const double pr = g.gm1 * (E - 0.5 * (lq[r][1] * u[0] + lq[r][2] * u[1] + lq[r][3] * u[2]));
@@ -586,7 +586,7 @@ __global__ void __launch_bounds__(NT3, 2) k_visc3d(DevMesh m, const double* __re
         for (int r = 0; r < KR3; ++r) {
             const int t = tid + r * NT3;
             if (t >= REG3) break;
-            const double ir = 1.0 / lq[r][0];
+            const double ir = rcp64(lq[r][0]);
             const double u = lq[r][1] * ir, v = lq[r][2] * ir, w = lq[r][3] * ir;
             pv[0][t] = u;
             pv[1][t] = v;

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 namespace mrab {
 
@@ -29,6 +30,9 @@ struct DevMesh {
     // bit 31 set = interior tile (see rhs2d_interior_tile); NULL = decide in the kernel
     const int32_t* tlist;
     int ntl;
+    // 2-D viscous, large meshes: per-point SAT viscous-flux scratch [6][npts] of the
+    // row-marching kernel (kernels2d_march.cu); NULL = tile kernel
+    double* satv;
 };
 
 struct Gas {
@@ -69,6 +73,8 @@ void rhs2d_tile_shape(int* tx, int* ty);
 // tile is full, its primitive halo (H = 6 viscous / 3 Euler) lies inside the mesh without
 // periodic wrap, and every flux point (tile + 3) is interior in both directions
 bool rhs2d_interior_tile(const int* n, const uint16_t* cls, int viscous, int bx, int by);
+// host: whether a 2-D mesh takes the row-marching RHS kernel (kernels2d_march.cu)
+bool rhs2d_march_wanted(const int* n, int viscous);
 
 struct Box {
     int lo[3];
@@ -149,6 +155,16 @@ void launch_l2_scrub(void* a, void* b, size_t bytes, int tag, cudaStream_t st);
 void launch_finite(const double* a, size_t n, int* flag, cudaStream_t st);
 
 #ifdef __CUDACC__
+// 1/x in fp64 without the IEEE division sequence: MUFU reciprocal seed refined by two
+// Newton steps (error ~1 ulp; the parity tolerances are 1e-10).  Measured on
+// B200: IEEE double division 128 cycles dependent latency, this ~4 DFMA + MUFU.
+__device__ __forceinline__ double rcp64(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    y = fma(y, fma(-x, y, 1.0), y);
+    y = fma(y, fma(-x, y, 1.0), y);
+    return y;
+}
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

@@ -34,15 +34,18 @@ constexpr int G3 = 3;
 constexpr double kP0 = 17.0 / 48.0;
 using namespace k2d;
 
-template <bool VISC, int TY>
+template <bool VISC, int TY, bool CART = true>
 struct Geo {
     static constexpr int H = VISC ? 6 : 3;
     static constexpr int AX = TX + 2 * H, AY = TY + 2 * H;
     static constexpr int FX = TX + 2 * G3, FY = TY + 2 * G3;
     static constexpr int NA = AX * AY, NF = FX * FY;
     // shared layout: uv[NA] (double2), fh[4][NF] (double2: xi (F0,F1), xi (F2,F3),
-    // eta (F0,F1), eta (F2,F3)), rho[NA], T[NA], cls[NA] (uint16)
-    static constexpr size_t bytes = 16 * (size_t)NA + 64 * (size_t)NF + 16 * (size_t)NA + 2 * (size_t)NA;
+    // eta (F0,F1), eta (F2,F3)), rho[NA], T[NA], curvilinear only: met[5][NF] (J, Mxx, Mxy,
+    // Myx, Myy of the flux points, staged by cp.async in phase A), cls[NA] (uint16)
+    static constexpr int NMET = CART ? 0 : 5 * NF;
+    static constexpr size_t bytes = 16 * (size_t)NA + 64 * (size_t)NF + 16 * (size_t)NA +
+                                    8 * (size_t)NMET + 2 * (size_t)NA;
 };
 
 // Lagrange gather of the donor state and Cartesian viscous fluxes at receiver
@@ -108,14 +111,15 @@ template <bool VISC, bool CART, int TY, int NTH>
 __device__ __forceinline__ void rhs2d_tile(const DevMesh& m, const double* __restrict__ Q,
                                            const Gas& g, const Epilogue& ep, int bx, int by,
                                            int tfast, double* smem, unsigned long long* tph) {
-    using GG = Geo<VISC, TY>;
+    using GG = Geo<VISC, TY, CART>;
     constexpr int H = GG::H, AX = GG::AX, FX = GG::FX;
     constexpr int NA = GG::NA, NF = GG::NF;
     double2* sh_uv = reinterpret_cast<double2*>(smem);
     double2* fh = sh_uv + NA;                       // [4][NF]
     double* sh_r = reinterpret_cast<double*>(fh + 4 * NF);
     double* sh_T = sh_r + NA;
-    uint16_t* sh_c = reinterpret_cast<uint16_t*>(sh_T + NA);
+    double* sh_met = sh_T + NA;                     // [5][NF] (curvilinear)
+    uint16_t* sh_c = reinterpret_cast<uint16_t*>(sh_met + GG::NMET);
 
     const int n0 = m.n[0], n1 = m.n[1];
     const int64_t N = m.npts;
@@ -138,6 +142,21 @@ __device__ __forceinline__ void rhs2d_tile(const DevMesh& m, const double* __res
                 for (int k = 0; k < 3; ++k)
                     if (k < ep.nsrc) prefetch_l2(ep.src[k] + o);
             }
+        }
+    }
+
+    // ---- curvilinear: metrics of the flux points -> shared memory (async, no registers)
+    if (!CART) {
+        const unsigned uN = (unsigned)N;
+        for (int t = tid; t < NF; t += NTH) {
+            const int b = t / FX, a = t - b * FX;
+            int gi = i0 - G3 + a, gj = j0 - G3 + b;
+            if (gi < 0 || gi >= n0) gi = m.periodic[0] ? (gi < 0 ? gi + n0 : gi - n0) : min(max(gi, 0), n0 - 1);
+            if (gj < 0 || gj >= n1) gj = m.periodic[1] ? (gj < 0 ? gj + n1 : gj - n1) : min(max(gj, 0), n1 - 1);
+            const unsigned q = (unsigned)gi + (unsigned)n0 * (unsigned)gj;
+            cp_async8(sh_met + t, m.J + q);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) cp_async8(sh_met + (1 + c) * NF + t, m.M + (c * uN + q));
         }
     }
 
@@ -168,7 +187,7 @@ __device__ __forceinline__ void rhs2d_tile(const DevMesh& m, const double* __res
             const int t = tid + k * NTH;
             if (t >= NA) break;
             const double r = ld[k][0];
-            const double ir = 1.0 / r;
+            const double ir = rcp64(r);
             const double u = ld[k][1] * ir;
             const double v = ld[k][2] * ir;
             const double T = g.gamma * g.gm1 * (ld[k][3] - 0.5 * (ld[k][1] * u + ld[k][2] * v)) * ir;
@@ -214,7 +233,7 @@ __device__ __forceinline__ void rhs2d_tile(const DevMesh& m, const double* __res
             // branch-free: holes carry valid (initial) states and points outside the mesh
             // rho = 1, so the primitives are finite; no active stencil reads them
             const double r = ld[k][0];
-            const double ir = 1.0 / r;
+            const double ir = rcp64(r);
             const double u = ld[k][1] * ir;
             const double v = ld[k][2] * ir;
             const double T = g.gamma * g.gm1 * (ld[k][3] - 0.5 * (ld[k][1] * u + ld[k][2] * v)) * ir;
@@ -230,6 +249,7 @@ __device__ __forceinline__ void rhs2d_tile(const DevMesh& m, const double* __res
         }
     }
     if (tfast == 0) allint = 0;
+    if (!CART) cp_async_wait_all();
     const int fast = __syncthreads_and(allint);
     if (ep.trace && threadIdx.x == 0) tph[0] = gtimer();
 
@@ -245,16 +265,13 @@ __device__ __forceinline__ void rhs2d_tile(const DevMesh& m, const double* __res
             const double E = p * g.igm1 + 0.5 * r * (u * u + v * v);
             double Ix[4] = {r * u, r * u * u + p, r * u * v, (E + p) * u};
             double Iy[4] = {r * v, r * u * v, r * v * v + p, (E + p) * v};
-            int64_t q = 0;
-            if (!CART) {
-                int gi = i0 - G3 + a, gj = j0 - G3 + b;
-                if (gi < 0) gi += n0; else if (gi >= n0) gi -= n0;
-                if (gj < 0) gj += n1; else if (gj >= n1) gj -= n1;
-                q = gi + (int64_t)n0 * gj;
-            }
+            double met[5] = {0, 0, 0, 0, 0};
+            if (!CART)
+#pragma unroll
+                for (int c = 0; c < 5; ++c) met[c] = sh_met[c * NF + t];
             if (VISC) {
                 double Vx[4], Vy[4];
-                visc_at_int<CART, AX>(sh_uv, sh_T, s, m, q, g, Vx, Vy);
+                visc_at_int<CART, AX>(sh_uv, sh_T, s, m, 0, g, Vx, Vy, met);
 #pragma unroll
                 for (int c = 1; c < 4; ++c) {
                     Ix[c] -= Vx[c];
@@ -269,8 +286,7 @@ __device__ __forceinline__ void rhs2d_tile(const DevMesh& m, const double* __res
                     fy[c] = m.cM[1] * Iy[c];
                 }
             } else {
-                const double Mxx = __ldg(m.M + q), Mxy = __ldg(m.M + N + q);
-                const double Myx = __ldg(m.M + 2 * N + q), Myy = __ldg(m.M + 3 * N + q);
+                const double Mxx = met[1], Mxy = met[2], Myx = met[3], Myy = met[4];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     fx[c] = Mxx * Ix[c] + Mxy * Iy[c];
@@ -296,16 +312,13 @@ __device__ __forceinline__ void rhs2d_tile(const DevMesh& m, const double* __res
             const double E = p * g.igm1 + 0.5 * r * (u * u + v * v);
             double Ix[4] = {r * u, r * u * u + p, r * u * v, (E + p) * u};
             double Iy[4] = {r * v, r * u * v, r * v * v + p, (E + p) * v};
-            int64_t q = 0;
-            if (!CART) {
-                int gi = i0 - G3 + a, gj = j0 - G3 + b;
-                if (gi < 0) gi += n0; else if (gi >= n0) gi -= n0;
-                if (gj < 0) gj += n1; else if (gj >= n1) gj -= n1;
-                q = gi + (int64_t)n0 * gj;
-            }
+            double met[5] = {0, 0, 0, 0, 0};
+            if (!CART)
+#pragma unroll
+                for (int c = 0; c < 5; ++c) met[c] = sh_met[c * NF + t];
             if (VISC) {
                 double Vx[4], Vy[4];
-                visc_at<CART, AX>(sh_uv, sh_T, s, code, m, q, g, Vx, Vy);
+                visc_at<CART, AX>(sh_uv, sh_T, s, code, m, 0, g, Vx, Vy, met);
 #pragma unroll
                 for (int c = 1; c < 4; ++c) {
                     Ix[c] -= Vx[c];
@@ -319,8 +332,7 @@ __device__ __forceinline__ void rhs2d_tile(const DevMesh& m, const double* __res
                     fy[c] = m.cM[1] * Iy[c];
                 }
             } else {
-                const double Mxx = __ldg(m.M + q), Mxy = __ldg(m.M + N + q);
-                const double Myx = __ldg(m.M + 2 * N + q), Myy = __ldg(m.M + 3 * N + q);
+                const double Mxx = met[1], Mxy = met[2], Myx = met[3], Myy = met[4];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     fx[c] = Mxx * Ix[c] + Mxy * Iy[c];
@@ -363,7 +375,7 @@ __device__ __forceinline__ void rhs2d_tile(const DevMesh& m, const double* __res
             }
             const double2 x01 = d_int2(fh, f, 1), x23 = d_int2(fh + NF, f, 1);
             const double2 y01 = d_int2(fh + 2 * NF, f, FX), y23 = d_int2(fh + 3 * NF, f, FX);
-            const double Jp = CART ? m.cJ : __ldg(m.J + up);
+            const double Jp = CART ? m.cJ : sh_met[f];
             double R[4];
             R[0] = -Jp * (x01.x + y01.x);
             R[1] = -Jp * (x01.y + y01.y);
@@ -432,7 +444,7 @@ __device__ __forceinline__ void rhs2d_tile(const DevMesh& m, const double* __res
                 y01 = d_gen2(fh + 2 * NF, f, FX, cy);
                 y23 = d_gen2(fh + 3 * NF, f, FX, cy);
             }
-            const double Jp = CART ? m.cJ : __ldg(m.J + p);
+            const double Jp = CART ? m.cJ : sh_met[f];
             R[0] = -Jp * (x01.x + y01.x);
             R[1] = -Jp * (x01.y + y01.y);
             R[2] = -Jp * (x23.x + y23.x);
@@ -443,7 +455,13 @@ __device__ __forceinline__ void rhs2d_tile(const DevMesh& m, const double* __res
 #pragma unroll
                 for (int c = 0; c < 4; ++c) q[c] = __ldg(Q + c * N + p);
                 double Vx[4] = {0, 0, 0, 0}, Vy[4] = {0, 0, 0, 0};
-                if (VISC) visc_at<CART, AX>(sh_uv, sh_T, s, code, m, p, g, Vx, Vy);
+                if (VISC) {
+                    double met[5] = {0, 0, 0, 0, 0};
+                    if (!CART)
+#pragma unroll
+                        for (int c = 0; c < 5; ++c) met[c] = sh_met[c * NF + f];
+                    visc_at<CART, AX>(sh_uv, sh_T, s, code, m, p, g, Vx, Vy, met);
+                }
                 // donor data gathered by k_donor2d for this receiver
                 const int slot = m.recv_slot[p];
                 double qi[4] = {0, 0, 0, 0}, fvi[6] = {0, 0, 0, 0, 0, 0};
@@ -563,7 +581,7 @@ __device__ __forceinline__ void src_prim(const SrcSet& ss, int h, int64_t N, int
                                          const Gas& g, double& u, double& v, double& T) {
     const double r = src_val(ss, h, 0, N, q), mu = src_val(ss, h, 1, N, q);
     const double mv = src_val(ss, h, 2, N, q), E = src_val(ss, h, 3, N, q);
-    const double ir = 1.0 / r;
+    const double ir = rcp64(r);
     u = mu * ir;
     v = mv * ir;
     T = g.gamma * g.gm1 * (E - 0.5 * (mu * u + mv * v)) * ir;
@@ -755,7 +773,7 @@ __global__ void __launch_bounds__(128) k_donor2d_r(RecvTask rt, SrcSets sets, Me
             if (VISC) {
                 double u = 0.0, v = 0.0, T = 0.0;
                 if (ok[s4]) {
-                    const double ir = 1.0 / ld[s4][0];
+                    const double ir = rcp64(ld[s4][0]);
                     u = ld[s4][1] * ir;
                     v = ld[s4][2] * ir;
                     T = g.gamma * g.gm1 * (ld[s4][3] - 0.5 * (ld[s4][1] * u + ld[s4][2] * v)) * ir;
@@ -897,7 +915,7 @@ static void launch_t(const DevMesh& m, const double* Q, const Gas& g, const Epil
     }
     Epilogue ep = ep0;
     ep.pf = pf;
-    const size_t bytes = Geo<VISC, TY>::bytes;
+    const size_t bytes = Geo<VISC, TY, CART>::bytes;
     if (!init) {
         cudaFuncSetAttribute(k_rhs2d<VISC, CART, TY, MINB, NTH>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -965,7 +983,11 @@ static void launch_v(const DevMesh& m, const double* Q, const Gas& g, const Epil
         case 2: launch_t<VISC, CART, 8, 3, 256>(m, Q, g, ep, ds, st); break;
         case 3: launch_t<VISC, CART, 16, 1, 512>(m, Q, g, ep, ds, st); break;
         case 4: launch_t<VISC, CART, 32, 1, 512>(m, Q, g, ep, ds, st); break;
-        default: launch_t<VISC, CART, 16, 2, 256>(m, Q, g, ep, ds, st); break;
+        // curvilinear meshes stage their metrics too (one CTA per SM): no register cap
+        default:
+            if (CART) launch_t<VISC, CART, 16, 2, 256>(m, Q, g, ep, ds, st);
+            else launch_t<VISC, CART, 16, 1, 256>(m, Q, g, ep, ds, st);
+            break;
     }
 }
 
@@ -975,8 +997,13 @@ bool rhs2d_tma_possible(const DevMesh& m, const Epilogue& ep, const double* Q);
 bool launch_rhs2d_tma(const DevMesh& m, const double* Q, const Gas& g, const Epilogue& ep,
                       cudaStream_t st);
 
+bool launch_rhs2d_march(const DevMesh& m, const double* Q, const Gas& g, const Epilogue& ep,
+                        cudaStream_t st);
+
 void launch_rhs2d(const DevMesh& m, const double* Q, const Gas& g, const Epilogue& ep,
                   const DonorSet& ds, cudaStream_t st) {
+    // row-marching kernel for large viscous meshes (whole-mesh launches)
+    if (launch_rhs2d_march(m, Q, g, ep, st)) return;
     // persistent TMA-pipelined kernel whenever its layout constraints hold (opt-in)
     if (rhs2d_tma_possible(m, ep, Q) && launch_rhs2d_tma(m, Q, g, ep, st)) return;
     // y-streaming tiles for meshes with more than one wave of tiles

@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(NTH, 2) k_rhs2d_s(DevMesh m, const double* __r
                 if (t >= nA) break;
                 const int o = rowA0 * AX + t;
                 const double r = ld[k][0];
-                const double ir = 1.0 / r;
+                const double ir = rcp64(r);
                 const double u = ld[k][1] * ir;
                 const double v = ld[k][2] * ir;
                 sh_c[o] = (uint16_t)cd[k];

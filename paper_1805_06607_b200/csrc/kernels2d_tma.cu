@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(NTH, 1)
             if (code) {
                 r = rq[t];
                 const double mu = rq[NA + t], mv = rq[2 * NA + t], E = rq[3 * NA + t];
-                const double ir = 1.0 / r;
+                const double ir = rcp64(r);
                 u = mu * ir;
                 v = mv * ir;
                 T = g.gamma * g.gm1 * (E - 0.5 * (mu * u + mv * v)) * ir;

@@ -62,6 +62,7 @@ struct MeshDev {
     double* fvhat = nullptr;      // [S][d(d+1)][R]
     int32_t* tiles = nullptr;     // 2-D: critical tiles (cover the donor box) then the bulk
     int32_t* tlist = nullptr;     // 2-D: all tiles, non-interior first (bit 31 = interior)
+    double* satv = nullptr;       // [6][N] SAT viscous-flux scratch of the row-marching kernel
     int ncrit = 0, nbulk = 0;
     DevMesh dm{};
 };
@@ -198,6 +199,10 @@ static size_t plan_bytes(const Plan& P, bool dry, mrab_ctx* ctx, Bump* bump, boo
             if (D) {
                 D->tiles = (int32_t*)a;
                 D->tlist = (int32_t*)b;
+            }
+            if (rhs2d_march_wanted(m.n, P.viscous)) {
+                void* e = take((size_t)6 * N * sizeof(double));
+                if (D) D->satv = (double*)e;
             }
         }
     }
@@ -969,6 +974,10 @@ mrab_status mrab_create(const mrab_plan* plan, const double* const* q0, void* d_
             CK(cudaMemcpy(D.tlist, slow.data(), slow.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
             dm.tlist = D.tlist;
             dm.ntl = (int)slow.size();
+            if (D.satv) {
+                CK(cudaMemsetAsync(D.satv, 0, (size_t)6 * N * sizeof(double), c->st));
+                dm.satv = D.satv;
+            }
         }
         dm.nrecv = (int64_t)R;
         c->book.head[g] = P.history_m - 1;   // empty ring: the first push goes to slot 0

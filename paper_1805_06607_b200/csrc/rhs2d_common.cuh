@@ -68,7 +68,8 @@ static __device__ __forceinline__ void kchar2(const double* q, const double* n, 
 template <bool CART, int AX>
 static __device__ __forceinline__ void visc_at(const double2* __restrict__ sh_uv, const double* __restrict__ sh_T,
                                         int s, unsigned code, const DevMesh& m, int64_t p,
-                                        const Gas& g, double* Fx, double* Fy) {
+                                        const Gas& g, double* Fx, double* Fy,
+                                        const double* met = nullptr) {
     const int cx = code & 15, cy = (code >> 4) & 15;
     double2 uvx, uvy;
     double Tx, Ty;
@@ -93,9 +94,14 @@ static __device__ __forceinline__ void visc_at(const double2* __restrict__ sh_uv
         dudy = sy * uvy.x; dvdy = sy * uvy.y; dTdy = sy * Ty;
     } else {
         const int64_t N = m.npts;
-        const double J = __ldg(m.J + p);
-        const double Mxx = __ldg(m.M + p), Mxy = __ldg(m.M + N + p);
-        const double Myx = __ldg(m.M + 2 * N + p), Myy = __ldg(m.M + 3 * N + p);
+        double J, Mxx, Mxy, Myx, Myy;
+        if (met) {
+            J = met[0]; Mxx = met[1]; Mxy = met[2]; Myx = met[3]; Myy = met[4];
+        } else {
+            J = __ldg(m.J + p);
+            Mxx = __ldg(m.M + p); Mxy = __ldg(m.M + N + p);
+            Myx = __ldg(m.M + 2 * N + p); Myy = __ldg(m.M + 3 * N + p);
+        }
         dudx = J * (Mxx * uvx.x + Myx * uvy.x); dudy = J * (Mxy * uvx.x + Myy * uvy.x);
         dvdx = J * (Mxx * uvx.y + Myx * uvy.y); dvdy = J * (Mxy * uvx.y + Myy * uvy.y);
         dTdx = J * (Mxx * Tx + Myx * Ty); dTdy = J * (Mxy * Tx + Myy * Ty);
@@ -108,6 +114,13 @@ static __device__ __forceinline__ void visc_at(const double2* __restrict__ sh_uv
     Fx[0] = 0.0; Fx[1] = txx; Fx[2] = txy; Fx[3] = uv.x * txx + uv.y * txy + g.kT * dTdx;
     Fy[0] = 0.0; Fy[1] = txy; Fy[2] = tyy; Fy[3] = uv.x * txy + uv.y * tyy + g.kT * dTdy;
 }
+
+// asynchronous 8-byte global -> shared copy (LDGSTS; no register staging)
+static __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gsrc));
+}
+static __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 
 // SAT penalties (eq:int P:279-299; corners sum both directions) at a segment-end
@@ -189,7 +202,8 @@ template <bool CART, int AX>
 static __device__ __forceinline__ void visc_at_int(const double2* __restrict__ sh_uv,
                                                    const double* __restrict__ sh_T, int s,
                                                    const DevMesh& m, int64_t p, const Gas& g,
-                                                   double* Fx, double* Fy) {
+                                                   double* Fx, double* Fy,
+                                                   const double* met = nullptr) {
     const double2 uvx = d_int2(sh_uv, s, 1), uvy = d_int2(sh_uv, s, AX);
     const double Tx = d_int(sh_T, s, 1), Ty = d_int(sh_T, s, AX);
     double dudx, dudy, dvdx, dvdy, dTdx, dTdy;
@@ -199,9 +213,14 @@ static __device__ __forceinline__ void visc_at_int(const double2* __restrict__ s
         dudy = sy * uvy.x; dvdy = sy * uvy.y; dTdy = sy * Ty;
     } else {
         const int64_t N = m.npts;
-        const double J = __ldg(m.J + p);
-        const double Mxx = __ldg(m.M + p), Mxy = __ldg(m.M + N + p);
-        const double Myx = __ldg(m.M + 2 * N + p), Myy = __ldg(m.M + 3 * N + p);
+        double J, Mxx, Mxy, Myx, Myy;
+        if (met) {
+            J = met[0]; Mxx = met[1]; Mxy = met[2]; Myx = met[3]; Myy = met[4];
+        } else {
+            J = __ldg(m.J + p);
+            Mxx = __ldg(m.M + p); Mxy = __ldg(m.M + N + p);
+            Myx = __ldg(m.M + 2 * N + p); Myy = __ldg(m.M + 3 * N + p);
+        }
         dudx = J * (Mxx * uvx.x + Myx * uvy.x); dudy = J * (Mxy * uvx.x + Myy * uvy.x);
         dvdx = J * (Mxx * uvx.y + Myx * uvy.y); dvdy = J * (Mxy * uvx.y + Myy * uvy.y);
         dTdx = J * (Mxx * Tx + Myx * Ty); dTdy = J * (Mxy * Tx + Myy * Ty);

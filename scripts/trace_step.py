@@ -38,6 +38,14 @@ for rep in range(int(os.environ.get("REPS", "2"))):
         d = sorted((x[1] - x[0]) / 1e3 for x in v)
         print(f"{KIND.get(tag >> 12, tag >> 12):6s} mesh {(tag >> 8) & 15} j {tag & 255:2d}: "
               f"{len(v):5d} CTAs  {s:7.1f} -> {e:7.1f} us ({e - s:6.1f})  CTA median {d[len(d) // 2]:.1f} max {d[-1]:.1f} us")
+        if os.environ.get("MARCH_MAP") and 300 < len(v) < 1000 and rep == 0:
+            # row-marching launch: CTA b = item b = (row chunk b // ns, strip b % ns)
+            ns = int(os.environ.get("MARCH_NS", "9"))
+            dur = {x[2]: (x[1] - x[0]) / 1e3 for x in v}
+            nch = (max(dur) + ns) // ns
+            print("    CTA duration (us) by row chunk (rows) x strip (columns):")
+            for ch in range(nch):
+                print("    " + " ".join(f"{dur.get(ch * ns + s_, 0):5.0f}" for s_ in range(ns)))
         if len(v) > 1000 and rep == 0:
             # list order = non-interior tiles first: durations by CTA index bucket
             byidx = sorted(((x[2], (x[1] - x[0]) / 1e3, x[0] / 1e3, x[3], x[4]) for x in v))
