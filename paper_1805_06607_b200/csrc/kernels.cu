@@ -126,40 +126,44 @@ __global__ void __launch_bounds__(256) k_visc(DevMesh m, const double* __restric
 template <int D>
 __device__ __forceinline__ void kchar(const double* q, const double* n, double side,
                                       const double* dq, double gamma, double* out) {
+    // divisions as reciprocal multiplies (rcp64: the IEEE divide costs 128 cycles of latency)
     const double rho = q[0];
+    const double irho = rcp64(rho);
     double u[D], ke = 0.0;
 #pragma unroll
     for (int i = 0; i < D; ++i) {
-        u[i] = q[1 + i] / rho;
+        u[i] = q[1 + i] * irho;
         ke += u[i] * u[i];
     }
     const double p = (gamma - 1.0) * (q[D + 1] - 0.5 * rho * ke);
-    const double c2 = gamma * p / rho;
+    const double c2 = gamma * p * irho;
     const double c = sqrt(c2);
-    const double H = (q[D + 1] + p) / rho;
+    const double ic2 = rcp64(c2);
+    const double H = (q[D + 1] + p) * irho;
     double nn = 0.0;
 #pragma unroll
     for (int i = 0; i < D; ++i) nn += n[i] * n[i];
     nn = sqrt(nn);
+    const double inn = rcp64(nn);
     double nh[D], un = 0.0;
 #pragma unroll
     for (int i = 0; i < D; ++i) {
-        nh[i] = n[i] / nn;
+        nh[i] = n[i] * inn;
         un += u[i] * nh[i];
     }
     double du[D], udm = 0.0;
 #pragma unroll
     for (int i = 0; i < D; ++i) {
-        du[i] = (dq[1 + i] - u[i] * dq[0]) / rho;
+        du[i] = (dq[1 + i] - u[i] * dq[0]) * irho;
         udm += u[i] * dq[1 + i];
     }
     const double dp = (gamma - 1.0) * (dq[D + 1] - udm + 0.5 * ke * dq[0]);
     double dun = 0.0;
 #pragma unroll
     for (int i = 0; i < D; ++i) dun += du[i] * nh[i];
-    const double ap = (dp + rho * c * dun) / (2.0 * c2);
-    const double am = (dp - rho * c * dun) / (2.0 * c2);
-    const double a0 = dq[0] - dp / c2;
+    const double ap = (dp + rho * c * dun) * (0.5 * ic2);
+    const double am = (dp - rho * c * dun) * (0.5 * ic2);
+    const double a0 = dq[0] - dp * ic2;
     const double l0 = fmax(side * un * nn, 0.0);
     const double lp = fmax(side * (un + c) * nn, 0.0);
     const double lm = fmax(side * (un - c) * nn, 0.0);
@@ -225,7 +229,7 @@ __device__ __forceinline__ void sat_point(const DevMesh& m, const double* __rest
                 sig1 *= 0.5 / g.Re;
             }
 #pragma unroll
-            for (int c = 0; c < NC; ++c) R[c] -= (0.5 * kd[c] + sig1 * dq[c]) / kP0;
+            for (int c = 0; c < NC; ++c) R[c] -= (0.5 * kd[c] + sig1 * dq[c]) * (1.0 / kP0);
             if (VISC && typ != MRAB_BC_WALL) {
                 // F^V_kappa - Fhat^V_kappa contracted with grad(kappa)
 #pragma unroll
@@ -237,7 +241,7 @@ __device__ __forceinline__ void sat_point(const DevMesh& m, const double* __rest
                         if (typ == MRAB_BC_OVERSET)
                             fh += nv[i] * m.fvhat[(int64_t)(i * (D + 1) + j) * m.nrecv + slot];
                     }
-                    R[1 + j] += 0.5 * side * (fk - fh) / kP0;
+                    R[1 + j] += 0.5 * side * (fk - fh) * (1.0 / kP0);
                 }
             }
         }

@@ -62,6 +62,8 @@ struct Epilogue {
     int pf;
     // 2-D with a tile list: at most `persist` CTAs walk the list (0 = one CTA per tile)
     int persist;
+    // 2-D: interior tiles take the lean path (set by the launcher; MRAB_LEAN=0 disables)
+    int lean;
     // launch timeline (mrab_set_trace; NULL = off): one record per CTA, see trace_rec
     unsigned long long* trace;
     int trace_tag;
@@ -70,9 +72,10 @@ struct Epilogue {
 // tile grid of the 2-D RHS kernel (for building tile lists on the host)
 void rhs2d_tile_shape(int* tx, int* ty);
 // host: true if tile (bx, by) of a 2-D mesh may take the kernel's interior fast path: the
-// tile is full, its primitive halo (H = 6 viscous / 3 Euler) lies inside the mesh without
-// periodic wrap, and every flux point (tile + 3) is interior in both directions
-bool rhs2d_interior_tile(const int* n, const uint16_t* cls, int viscous, int bx, int by);
+// tile is full, its primitive halo (H = 6 viscous / 3 Euler) lies inside the mesh (or wraps
+// across a periodic seam), and every flux point (tile + 3) is interior in both directions
+bool rhs2d_interior_tile(const int* n, const int* periodic, const uint16_t* cls, int viscous,
+                         int bx, int by);
 // host: whether a 2-D mesh takes the row-marching RHS kernel (kernels2d_march.cu)
 bool rhs2d_march_wanted(const int* n, int viscous);
 

@@ -91,6 +91,14 @@ __device__ __forceinline__ void prefetch_l2(const double* p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
+// element offset of (gi, gj) on an interior tile's halo, which may cross a periodic seam
+// (the host flags such tiles interior only in periodic directions)
+__device__ __forceinline__ unsigned wrap_idx(int gi, int gj, int n0, int n1) {
+    if (gi < 0) gi += n0; else if (gi >= n0) gi -= n0;
+    if (gj < 0) gj += n1; else if (gj >= n1) gj -= n1;
+    return (unsigned)gi + (unsigned)n0 * (unsigned)gj;
+}
+
 template <int NS>
 __device__ __forceinline__ double epi_sum(const Epilogue& ep, unsigned uN, unsigned up, int c) {
     const unsigned o = c * uN + up;
@@ -167,6 +175,7 @@ __device__ __forceinline__ void rhs2d_tile(const DevMesh& m, const double* __res
         // interior tile: halo inside the mesh, no class codes needed by phases B / C
         const unsigned uN = (unsigned)N;
         const unsigned q0 = (unsigned)(i0 - H) + (unsigned)n0 * (unsigned)(j0 - H);
+        const bool wrap = i0 - H < 0 || j0 - H < 0 || i0 + TX + H > n0 || j0 + TY + H > n1;
         double ld[KA][4];
 #pragma unroll
         for (int k = 0; k < KA; ++k) {
@@ -175,7 +184,8 @@ __device__ __forceinline__ void rhs2d_tile(const DevMesh& m, const double* __res
             ld[k][1] = ld[k][2] = ld[k][3] = 0.0;
             if (t < NA) {
                 const int bb = t / AX, a = t - bb * AX;
-                const unsigned q = q0 + (unsigned)a + (unsigned)n0 * (unsigned)bb;
+                const unsigned q = wrap ? wrap_idx(i0 - H + a, j0 - H + bb, n0, n1)
+                                        : q0 + (unsigned)a + (unsigned)n0 * (unsigned)bb;
                 ld[k][0] = __ldg(Q + q);
                 ld[k][1] = __ldg(Q + (uN + q));
                 ld[k][2] = __ldg(Q + (2 * uN + q));
@@ -426,6 +436,23 @@ __device__ __forceinline__ void rhs2d_tile(const DevMesh& m, const double* __res
 #pragma unroll
                 for (int c = 0; c < 4; ++c) yb[c] += ep.csrc[k] * __ldg(ep.src[k] + c * N + p);
         }
+        // SAT inputs of segment-end points requested before the divergence is formed
+        const bool satp = code && (((code & 15) == CLS_L0) || ((code & 15) == CLS_R0) ||
+                                   (((code >> 4) & 15) == CLS_L0) || (((code >> 4) & 15) == CLS_R0));
+        double q[4] = {0, 0, 0, 0}, qi[4] = {0, 0, 0, 0}, fvi[6] = {0, 0, 0, 0, 0, 0};
+        if (satp) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) q[c] = __ldg(Q + c * N + p);
+            // donor data gathered by k_donor2d for this receiver
+            const int slot = m.recv_slot[p];
+            if (slot >= 0) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) qi[c] = m.qhat[c * m.nrecv + slot];
+                if (VISC)
+#pragma unroll
+                    for (int c = 0; c < 6; ++c) fvi[c] = m.fvhat[c * m.nrecv + slot];
+            }
+        }
         double R[4] = {0, 0, 0, 0};
         if (code) {
             const int cx = code & 15, cy = (code >> 4) & 15;
@@ -450,10 +477,7 @@ __device__ __forceinline__ void rhs2d_tile(const DevMesh& m, const double* __res
             R[2] = -Jp * (x23.x + y23.x);
             R[3] = -Jp * (x23.y + y23.y);
             // ---- SAT ----
-            if (cx == CLS_L0 || cx == CLS_R0 || cy == CLS_L0 || cy == CLS_R0) {
-                double q[4];
-#pragma unroll
-                for (int c = 0; c < 4; ++c) q[c] = __ldg(Q + c * N + p);
+            if (satp) {
                 double Vx[4] = {0, 0, 0, 0}, Vy[4] = {0, 0, 0, 0};
                 if (VISC) {
                     double met[5] = {0, 0, 0, 0, 0};
@@ -461,16 +485,6 @@ __device__ __forceinline__ void rhs2d_tile(const DevMesh& m, const double* __res
 #pragma unroll
                         for (int c = 0; c < 5; ++c) met[c] = sh_met[c * NF + f];
                     visc_at<CART, AX>(sh_uv, sh_T, s, code, m, p, g, Vx, Vy, met);
-                }
-                // donor data gathered by k_donor2d for this receiver
-                const int slot = m.recv_slot[p];
-                double qi[4] = {0, 0, 0, 0}, fvi[6] = {0, 0, 0, 0, 0, 0};
-                if (slot >= 0) {
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) qi[c] = m.qhat[c * m.nrecv + slot];
-                    if (VISC)
-#pragma unroll
-                        for (int c = 0; c < 6; ++c) fvi[c] = m.fvhat[c * m.nrecv + slot];
                 }
                 const int idx[2] = {gi, gj};
 #pragma unroll
@@ -486,8 +500,8 @@ __device__ __forceinline__ void rhs2d_tile(const DevMesh& m, const double* __res
                         nv[0] = k == 0 ? m.cJ * m.cM[0] : 0.0;
                         nv[1] = k == 1 ? m.cJ * m.cM[1] : 0.0;
                     } else {
-                        nv[0] = Jp * __ldg(m.M + (2 * k) * N + p);
-                        nv[1] = Jp * __ldg(m.M + (2 * k + 1) * N + p);
+                        nv[0] = Jp * sh_met[(1 + 2 * k) * NF + f];
+                        nv[1] = Jp * sh_met[(2 + 2 * k) * NF + f];
                     }
                     double qh[4];
                     if (typ == MRAB_BC_OVERSET) {
@@ -509,14 +523,14 @@ __device__ __forceinline__ void rhs2d_tile(const DevMesh& m, const double* __res
                     double sig1 = 0.0;
                     if (VISC) sig1 = 0.5 * (nv[0] * nv[0] + nv[1] * nv[1]) * g.iRe;
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) R[c] -= (0.5 * kd[c] + sig1 * dq[c]) / kP0;
+                    for (int c = 0; c < 4; ++c) R[c] -= (0.5 * kd[c] + sig1 * dq[c]) * (1.0 / kP0);
                     if (VISC && typ != MRAB_BC_WALL) {
 #pragma unroll
                         for (int j = 0; j < 3; ++j) {
                             const double fk = nv[0] * Vx[1 + j] + nv[1] * Vy[1 + j];
                             double fhv = 0.0;
                             if (typ == MRAB_BC_OVERSET) fhv = nv[0] * fvi[j] + nv[1] * fvi[3 + j];
-                            R[1 + j] += 0.5 * side * (fk - fhv) / kP0;
+                            R[1 + j] += 0.5 * side * (fk - fhv) * (1.0 / kP0);
                         }
                     }
                 }
@@ -533,6 +547,209 @@ __device__ __forceinline__ void rhs2d_tile(const DevMesh& m, const double* __res
     }
 }
 
+
+
+// ------------------------------------------------------------------------------------
+// Lean interior tile (host-flagged: halo inside the mesh, every flux point interior in both
+// directions).  Interior stencils reach 2, so the primitive halo is 4 (not 6) and the flux
+// halo 2 (not 3); Fhat_xi is kept only on the x-extended rows and Fhat_eta only on the
+// y-extended columns; all loop trip counts and offsets are compile-time; the epilogue loads of
+// both output points of a thread are issued together before the divergence is formed.
+// Same arithmetic as the general path.
+// ------------------------------------------------------------------------------------
+template <bool VISC, int TY>
+struct GeoL {
+    static constexpr int H = VISC ? 4 : 2, G = 2;
+    static constexpr int AX = TX + 2 * H, AY = TY + 2 * H, NA = AX * AY;
+    static constexpr int FX = TX + 2 * G, FY = TY + 2 * G, NF = FX * FY;
+    static constexpr int NXI = FX * TY, NETA = TX * FY;    // Fhat_xi / Fhat_eta points
+    // uv[NA] double2, T[NA], rho[NA], fxi[2][NXI] double2, feta[2][NETA] double2, met[5][NF]
+    static constexpr size_t bytes(bool cart) {
+        return 32 * (size_t)NA + 32 * (size_t)NXI + 32 * (size_t)NETA + (cart ? 0 : 40 * (size_t)NF);
+    }
+};
+
+template <bool VISC, bool CART, int TY, int NTH, int NS>
+__device__ __forceinline__ void rhs2d_tile_lean(const DevMesh& m, const double* __restrict__ Q,
+                                                const Gas& g, const Epilogue& ep, int bx, int by,
+                                                double* smem, unsigned long long* tph) {
+    using GL = GeoL<VISC, TY>;
+    constexpr int H = GL::H, G = GL::G, AX = GL::AX, NA = GL::NA, FX = GL::FX, NF = GL::NF;
+    constexpr int NXI = GL::NXI, NETA = GL::NETA;
+    double2* sh_uv = reinterpret_cast<double2*>(smem);
+    double* sh_T = reinterpret_cast<double*>(sh_uv + NA);
+    double* sh_r = sh_T + NA;
+    double2* fxi = reinterpret_cast<double2*>(sh_r + NA);     // [2][NXI]: (F0,F1), (F2,F3)
+    double2* feta = fxi + 2 * NXI;                             // [2][NETA]
+    double* sh_met = reinterpret_cast<double*>(feta + 2 * NETA);   // [5][NF]
+    const int n0 = m.n[0], n1 = m.n[1];
+    const unsigned uN = (unsigned)m.npts, un0 = (unsigned)n0;
+    const int i0 = bx * TX, j0 = by * TY;
+    const int tid = threadIdx.x;
+    // halo across a periodic seam (tile-uniform)
+    const bool wrap = i0 - H < 0 || j0 - H < 0 || i0 + TX + H > n0 || j0 + TY + H > n1;
+    // ---- curvilinear metrics of the flux points (async)
+    if (!CART) {
+        const unsigned qf0 = (unsigned)(i0 - G) + un0 * (unsigned)(j0 - G);
+        for (int t = tid; t < NF; t += NTH) {
+            const int b = t / FX, a = t - b * FX;
+            const unsigned q = wrap ? wrap_idx(i0 - G + a, j0 - G + b, n0, n1)
+                                    : qf0 + (unsigned)a + un0 * (unsigned)b;
+            cp_async8(sh_met + t, m.J + q);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) cp_async8(sh_met + (1 + c) * NF + t, m.M + (c * uN + q));
+        }
+    }
+    // ---- phase A: primitives of tile + H
+    {
+        constexpr int KA = (NA + NTH - 1) / NTH;
+        const unsigned q0 = (unsigned)(i0 - H) + un0 * (unsigned)(j0 - H);
+        double ld[KA][4];
+#pragma unroll
+        for (int k = 0; k < KA; ++k) {
+            const int t = tid + k * NTH;
+            ld[k][0] = 1.0;
+            ld[k][1] = ld[k][2] = ld[k][3] = 0.0;
+            if (t < NA) {
+                const int b = t / AX, a = t - b * AX;
+                const unsigned q = wrap ? wrap_idx(i0 - H + a, j0 - H + b, n0, n1)
+                                        : q0 + (unsigned)a + un0 * (unsigned)b;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) ld[k][c] = __ldg(Q + (c * uN + q));
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < KA; ++k) {
+            const int t = tid + k * NTH;
+            if (t < NA) {
+                const double r = ld[k][0];
+                const double ir = rcp64(r);
+                const double u = ld[k][1] * ir, v = ld[k][2] * ir;
+                sh_uv[t] = make_double2(u, v);
+                sh_T[t] = g.gamma * g.gm1 * (ld[k][3] - 0.5 * (ld[k][1] * u + ld[k][2] * v)) * ir;
+                sh_r[t] = r;
+            }
+        }
+    }
+    if (!CART) cp_async_wait_all();
+    __syncthreads();
+    if (ep.trace && threadIdx.x == 0) tph[0] = gtimer();
+    // ---- phase B: fluxes at tile + G (Fhat_xi on the x-extended rows, Fhat_eta on the
+    // y-extended columns; the 4 x 4 corner blocks are not needed)
+    {
+        constexpr int KF = (NF + NTH - 1) / NTH;
+#pragma unroll 1
+        for (int k = 0; k < KF; ++k) {
+            const int t = tid + k * NTH;
+            if (t >= NF) break;
+            const int b = t / FX, a = t - b * FX;
+            const bool inx = b >= G && b < G + TY, iny = a >= G && a < G + TX;
+            if (!inx && !iny) continue;
+            const int s = (b + H - G) * AX + (a + H - G);
+            const double r = sh_r[s];
+            const double2 uv = sh_uv[s];
+            const double u = uv.x, v = uv.y;
+            const double p = r * sh_T[s] * g.igamma;
+            const double E = p * g.igm1 + 0.5 * r * (u * u + v * v);
+            double Ix[4] = {r * u, r * u * u + p, r * u * v, (E + p) * u};
+            double Iy[4] = {r * v, r * u * v, r * v * v + p, (E + p) * v};
+            double met[5] = {0, 0, 0, 0, 0};
+            if (!CART)
+#pragma unroll
+                for (int c = 0; c < 5; ++c) met[c] = sh_met[c * NF + t];
+            if (VISC) {
+                double Vx[4], Vy[4];
+                visc_at_int<CART, AX>(sh_uv, sh_T, s, m, 0, g, Vx, Vy, met);
+#pragma unroll
+                for (int c = 1; c < 4; ++c) {
+                    Ix[c] -= Vx[c];
+                    Iy[c] -= Vy[c];
+                }
+            }
+            if (inx) {
+                double fx[4];
+                if (CART) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) fx[c] = m.cM[0] * Ix[c];
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) fx[c] = met[1] * Ix[c] + met[2] * Iy[c];
+                }
+                const int o = (b - G) * FX + a;
+                fxi[o] = make_double2(fx[0], fx[1]);
+                fxi[NXI + o] = make_double2(fx[2], fx[3]);
+            }
+            if (iny) {
+                double fy[4];
+                if (CART) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) fy[c] = m.cM[1] * Iy[c];
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) fy[c] = met[3] * Ix[c] + met[4] * Iy[c];
+                }
+                const int o = b * TX + (a - G);
+                feta[o] = make_double2(fy[0], fy[1]);
+                feta[NETA + o] = make_double2(fy[2], fy[3]);
+            }
+        }
+    }
+    __syncthreads();
+    if (ep.trace && threadIdx.x == 0) tph[1] = gtimer();
+    // ---- phase C: divergence and epilogue; both points' epilogue loads issued first
+    {
+        constexpr int KC = TX * TY / NTH;
+        const unsigned qc0 = (unsigned)i0 + un0 * (unsigned)j0;
+        double yb[KC][4] = {};
+        if (NS >= 0) {
+            double v[KC][NS >= 0 ? NS + 1 : 1][4];
+#pragma unroll
+            for (int k = 0; k < KC; ++k) {
+                const int t = tid + k * NTH;
+                const unsigned up = qc0 + (unsigned)(t % TX) + un0 * (unsigned)(t / TX);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    v[k][0][c] = __ldg(ep.base + (c * uN + up));
+#pragma unroll
+                    for (int s2 = 0; s2 < (NS > 0 ? NS : 0); ++s2) v[k][1 + s2][c] = __ldg(ep.src[s2] + (c * uN + up));
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < KC; ++k)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    double y = v[k][0][c];
+#pragma unroll
+                    for (int s2 = 0; s2 < (NS > 0 ? NS : 0); ++s2) y += ep.csrc[s2] * v[k][1 + s2][c];
+                    yb[k][c] = y;
+                }
+        }
+#pragma unroll
+        for (int k = 0; k < KC; ++k) {
+            const int t = tid + k * NTH;
+            const int a = t % TX, b = t / TX;
+            const unsigned up = qc0 + (unsigned)a + un0 * (unsigned)b;
+            const int ox = b * FX + (a + G);
+            const int oy = (b + G) * TX + a;
+            const double2 x01 = d_int2(fxi, ox, 1), x23 = d_int2(fxi + NXI, ox, 1);
+            const double2 y01 = d_int2(feta, oy, TX), y23 = d_int2(feta + NETA, oy, TX);
+            const double Jp = CART ? m.cJ : sh_met[(b + G) * FX + (a + G)];
+            double R[4];
+            R[0] = -Jp * (x01.x + y01.x);
+            R[1] = -Jp * (x01.y + y01.y);
+            R[2] = -Jp * (x23.x + y23.x);
+            R[3] = -Jp * (x23.y + y23.y);
+            if (ep.r_out) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) ep.r_out[c * uN + up] = R[c];
+            }
+            if (NS >= 0) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) ep.y_out[c * uN + up] = yb[k][c] + ep.c_new * R[c];
+            }
+        }
+    }
+}
 
 // tile lists (host-built, mrab_api.cu): bit 31 marks an interior tile -- full, halo inside
 // the mesh without periodic wrap, every flux point interior in both directions.  With
@@ -556,7 +773,14 @@ __global__ void __launch_bounds__(NTH, MINB) k_rhs2d(DevMesh m, const double* __
             bx = tl - by * ntx;
             tf = (int)(raw >> 31);
         }
-        rhs2d_tile<VISC, CART, TY, NTH>(m, Q, g, ep, bx, by, tf, smem, tph);
+        const int nsl = ep.y_out ? ep.nsrc : -1;
+        if (tf == 1 && ep.lean && (nsl == 2 || nsl == 3 || nsl == -1)) {
+            if (nsl == 2) rhs2d_tile_lean<VISC, CART, TY, NTH, 2>(m, Q, g, ep, bx, by, smem, tph);
+            else if (nsl == 3) rhs2d_tile_lean<VISC, CART, TY, NTH, 3>(m, Q, g, ep, bx, by, smem, tph);
+            else rhs2d_tile_lean<VISC, CART, TY, NTH, -1>(m, Q, g, ep, bx, by, smem, tph);
+        } else {
+            rhs2d_tile<VISC, CART, TY, NTH>(m, Q, g, ep, bx, by, tf, smem, tph);
+        }
         it += gridDim.x;
         if (!tlist || it >= ntl) break;
         __syncthreads();   // the previous tile's shared data is dead
@@ -722,6 +946,28 @@ __global__ void __launch_bounds__(128) k_donor2d_r(RecvTask rt, SrcSets sets, Me
     const int n0 = m.n[0], n1 = m.n[1];
     const unsigned uN = (unsigned)m.npts;
     const int ns = ss.nsrc[h];
+    // this lane's stencil point: weights, class code and metrics requested together with the
+    // region loads below (one memory round trip after the receiver's base is known)
+    const int ai = a & 3, aj = a >> 2;
+    double W = 0.0, Jq = 0.0, Mq[4] = {0, 0, 0, 0};
+    unsigned code = 0;
+    unsigned qown = 0;
+    if (live) {
+        int ii = ib + ai, jj = jb + aj;
+        if (ii >= n0) ii -= n0;
+        if (jj >= n1) jj -= n1;
+        qown = (unsigned)ii + (unsigned)n0 * (unsigned)jj;
+        const double* w = rt.rw[rm] + 12 * r;
+        W = w[ai] * w[4 + aj];
+        if (VISC) {
+            code = m.cls[qown];
+            if (!m.cart) {
+                Jq = __ldg(m.J + qown);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) Mq[c] = __ldg(m.M + (c * uN + qown));
+            }
+        }
+    }
     // ---- stage the region ----
     if (live) {
         double ld[4][4];
@@ -789,17 +1035,9 @@ __global__ void __launch_bounds__(128) k_donor2d_r(RecvTask rt, SrcSets sets, Me
 #pragma unroll
     for (int c = 0; c < 10; ++c) acc[c] = 0.0;
     if (live) {
-        const int ai = a & 3, aj = a >> 2;
-        int ii = ib + ai, jj = jb + aj;
-        if (ii >= n0) ii -= n0;
-        if (jj >= n1) jj -= n1;
-        const double* w = rt.rw[rm] + 12 * r;
-        const double W = w[ai] * w[4 + aj];
 #pragma unroll
         for (int c = 0; c < 4; ++c) acc[c] = W * sh_q[slot][c][a];
         if (VISC) {
-            const unsigned q = (unsigned)ii + (unsigned)n0 * (unsigned)jj;
-            const unsigned code = m.cls[q];
             const int cl[2] = {(int)(code & 15), (int)((code >> 4) & 15)};
             const int e0 = (aj + 3) * RG + (ai + 3);
             const int stride[2] = {1, RG};
@@ -825,9 +1063,7 @@ __global__ void __launch_bounds__(128) k_donor2d_r(RecvTask rt, SrcSets sets, Me
                     gy[f] = sy * d[1][f];
                 }
             } else {
-                const double J = __ldg(m.J + q);
-                const double Mxx = __ldg(m.M + q), Mxy = __ldg(m.M + uN + q);
-                const double Myx = __ldg(m.M + 2 * uN + q), Myy = __ldg(m.M + 3 * uN + q);
+                const double J = Jq, Mxx = Mq[0], Mxy = Mq[1], Myx = Mq[2], Myy = Mq[3];
 #pragma unroll
                 for (int f = 0; f < 3; ++f) {
                     gx[f] = J * (Mxx * d[0][f] + Myx * d[1][f]);
@@ -915,7 +1151,13 @@ static void launch_t(const DevMesh& m, const double* Q, const Gas& g, const Epil
     }
     Epilogue ep = ep0;
     ep.pf = pf;
-    const size_t bytes = Geo<VISC, TY, CART>::bytes;
+    static int lean = -1;
+    if (lean < 0) {
+        const char* e = getenv("MRAB_LEAN");
+        lean = e ? atoi(e) : 1;
+    }
+    ep.lean = lean;
+    const size_t bytes = std::max(Geo<VISC, TY, CART>::bytes, GeoL<VISC, TY>::bytes(CART));
     if (!init) {
         cudaFuncSetAttribute(k_rhs2d<VISC, CART, TY, MINB, NTH>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -955,17 +1197,23 @@ static int k2d_variant() {
     return v;
 }
 
-bool rhs2d_interior_tile(const int* n, const uint16_t* cls, int viscous, int bx, int by) {
+bool rhs2d_interior_tile(const int* n, const int* periodic, const uint16_t* cls, int viscous,
+                         int bx, int by) {
     int tx, ty;
     rhs2d_tile_shape(&tx, &ty);
     const int H = viscous ? Geo<true, 16>::H : Geo<false, 16>::H;
     const int i0 = bx * tx, j0 = by * ty;
     if (i0 + tx > n[0] || j0 + ty > n[1]) return false;
-    if (i0 - H < 0 || j0 - H < 0 || i0 + tx + H > n[0] || j0 + ty + H > n[1]) return false;
+    // the halo may cross a seam only in periodic directions (and at most once)
+    if (n[0] < tx + 2 * H || n[1] < ty + 2 * H) return false;
+    if (!periodic[0] && (i0 - H < 0 || i0 + tx + H > n[0])) return false;
+    if (!periodic[1] && (j0 - H < 0 || j0 + ty + H > n[1])) return false;
     const unsigned want = CLS_INT | (CLS_INT << 4);
     for (int j = j0 - G3; j < j0 + ty + G3; ++j)
-        for (int i = i0 - G3; i < i0 + tx + G3; ++i)
-            if (cls[i + (size_t)n[0] * j] != want) return false;
+        for (int i = i0 - G3; i < i0 + tx + G3; ++i) {
+            const int ii = (i + n[0]) % n[0], jj = (j + n[1]) % n[1];
+            if (cls[ii + (size_t)n[0] * jj] != want) return false;
+        }
     return true;
 }
 

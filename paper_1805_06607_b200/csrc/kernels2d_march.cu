@@ -132,14 +132,14 @@ __device__ __forceinline__ void sat2d_m(const DevMesh& m, const double* __restri
         kchar2(q, nv, side, dq, g, kd);
         const double sig1 = 0.5 * (nv[0] * nv[0] + nv[1] * nv[1]) * g.iRe;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) R[c] -= (0.5 * kd[c] + sig1 * dq[c]) / kP0m;
+        for (int c = 0; c < 4; ++c) R[c] -= (0.5 * kd[c] + sig1 * dq[c]) * (1.0 / kP0m);
         if (typ != MRAB_BC_WALL) {
 #pragma unroll
             for (int j = 0; j < 3; ++j) {
                 const double fk = nv[0] * Vx[j] + nv[1] * Vy[j];
                 double fhv = 0.0;
                 if (typ == MRAB_BC_OVERSET) fhv = nv[0] * fvi[j] + nv[1] * fvi[3 + j];
-                R[1 + j] += 0.5 * side * (fk - fhv) / kP0m;
+                R[1 + j] += 0.5 * side * (fk - fhv) * (1.0 / kP0m);
             }
         }
     }

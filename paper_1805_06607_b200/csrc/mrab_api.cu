@@ -957,7 +957,7 @@ mrab_status mrab_create(const mrab_plan* plan, const double* const* q0, void* d_
             }();
             for (int by = 0; by < nty; ++by)
                 for (int bx = 0; bx < ntx; ++bx) {
-                    const bool interior = tag && rhs2d_interior_tile(m.n, m.cls.data(), P.viscous, bx, by);
+                    const bool interior = tag && rhs2d_interior_tile(m.n, m.periodic, m.cls.data(), P.viscous, bx, by);
                     const int32_t t = (by * ntx + bx) | (interior ? (int32_t)0x80000000u : 0);
                     const bool meets = m.is_donor && bx * tx <= m.st_hi[0] &&
                                        bx * tx + tx - 1 >= m.st_lo[0] && by * ty <= m.st_hi[1] &&

@@ -38,21 +38,25 @@ static __device__ __forceinline__ double2 d_gen2(const double2* f, int s, int st
 // characteristic SAT penalty (same algebra as kernels.cu kchar<2>)
 static __device__ __forceinline__ void kchar2(const double* q, const double* n, double side,
                                        const double* dq, const Gas& g, double* out) {
+    // divisions as reciprocal multiplies (rcp64: the IEEE divide costs 128 cycles of latency)
     const double rho = q[0];
-    const double u0 = q[1] / rho, u1 = q[2] / rho;
+    const double irho = rcp64(rho);
+    const double u0 = q[1] * irho, u1 = q[2] * irho;
     const double ke = u0 * u0 + u1 * u1;
     const double p = g.gm1 * (q[3] - 0.5 * rho * ke);
-    const double c2 = g.gamma * p / rho, c = sqrt(c2);
-    const double H = (q[3] + p) / rho;
+    const double c2 = g.gamma * p * irho, c = sqrt(c2);
+    const double ic2 = rcp64(c2);
+    const double H = (q[3] + p) * irho;
     const double nn = sqrt(n[0] * n[0] + n[1] * n[1]);
-    const double n0 = n[0] / nn, n1 = n[1] / nn;
+    const double inn = rcp64(nn);
+    const double n0 = n[0] * inn, n1 = n[1] * inn;
     const double un = u0 * n0 + u1 * n1;
-    const double du0 = (dq[1] - u0 * dq[0]) / rho, du1 = (dq[2] - u1 * dq[0]) / rho;
+    const double du0 = (dq[1] - u0 * dq[0]) * irho, du1 = (dq[2] - u1 * dq[0]) * irho;
     const double dp = g.gm1 * (dq[3] - (u0 * dq[1] + u1 * dq[2]) + 0.5 * ke * dq[0]);
     const double dun = du0 * n0 + du1 * n1;
-    const double ap = (dp + rho * c * dun) / (2.0 * c2);
-    const double am = (dp - rho * c * dun) / (2.0 * c2);
-    const double a0 = dq[0] - dp / c2;
+    const double ap = (dp + rho * c * dun) * (0.5 * ic2);
+    const double am = (dp - rho * c * dun) * (0.5 * ic2);
+    const double a0 = dq[0] - dp * ic2;
     const double l0 = fmax(side * un * nn, 0.0);
     const double lp = fmax(side * (un + c) * nn, 0.0);
     const double lm = fmax(side * (un - c) * nn, 0.0);
@@ -184,14 +188,14 @@ static __device__ __forceinline__ void sat2d(const DevMesh& m, const double* __r
         double sig1 = 0.0;
         if (VISC) sig1 = 0.5 * (nv[0] * nv[0] + nv[1] * nv[1]) * g.iRe;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) R[c] -= (0.5 * kd[c] + sig1 * dq[c]) / kP0;
+        for (int c = 0; c < 4; ++c) R[c] -= (0.5 * kd[c] + sig1 * dq[c]) * (1.0 / kP0);
         if (VISC && typ != MRAB_BC_WALL) {
 #pragma unroll
             for (int j = 0; j < 3; ++j) {
                 const double fk = nv[0] * Vx[1 + j] + nv[1] * Vy[1 + j];
                 double fhv = 0.0;
                 if (typ == MRAB_BC_OVERSET) fhv = nv[0] * fvi[j] + nv[1] * fvi[3 + j];
-                R[1 + j] += 0.5 * side * (fk - fhv) / kP0;
+                R[1 + j] += 0.5 * side * (fk - fhv) * (1.0 / kP0);
             }
         }
     }

@@ -46,6 +46,15 @@ for rep in range(int(os.environ.get("REPS", "2"))):
             print("    CTA duration (us) by row chunk (rows) x strip (columns):")
             for ch in range(nch):
                 print("    " + " ".join(f"{dur.get(ch * ns + s_, 0):5.0f}" for s_ in range(ns)))
+        if os.environ.get("SMALL_MAP") and 100 <= len(v) <= 300 and rep == 0 and (tag >> 12) == 1:
+            byidx = sorted(((x[2], (x[1] - x[0]) / 1e3, x[3], x[4]) for x in v))
+            for lo in range(0, len(byidx), 32):
+                ch = byidx[lo:lo + 32]
+                ds = sorted(c[1] for c in ch)
+                pa = sorted(c[2] for c in ch)[len(ch) // 2]
+                pb = sorted(c[3] for c in ch)[len(ch) // 2]
+                print(f"    CTAs {lo:4d}..{lo + len(ch) - 1:4d}: dur median {ds[len(ds) // 2]:5.1f} max {ds[-1]:5.1f}  "
+                      f"phase A {pa:5.1f} B {pb:5.1f} C {ds[len(ds) // 2] - pa - pb:5.1f}")
         if len(v) > 1000 and rep == 0:
             # list order = non-interior tiles first: durations by CTA index bucket
             byidx = sorted(((x[2], (x[1] - x[0]) / 1e3, x[0] / 1e3, x[3], x[4]) for x in v))
