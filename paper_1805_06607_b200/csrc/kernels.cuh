@@ -125,6 +125,7 @@ struct RecvTask {
     int set[8];                     // which SrcSet (evaluation time) each entry reads
     unsigned long long* trace;      // launch timeline (NULL = off)
     int trace_tag;
+    int raw_k;                      // set by the launcher: 1 + max history terms of the sets
 };
 
 struct SrcSets {

@@ -946,6 +946,17 @@ __global__ void __launch_bounds__(128) k_donor2d_r(RecvTask rt, SrcSets sets, Me
     const int n0 = m.n[0], n1 = m.n[1];
     const unsigned uN = (unsigned)m.npts;
     const int ns = ss.nsrc[h];
+    // kernel parameters indexed by the donor mesh are read once into registers: the parameter
+    // block (~10 KB) exceeds the constant cache, so re-reading it inside loops serialises
+    const int per0 = m.periodic[0], per1 = m.periodic[1];
+    const double* bp = ss.base[h];
+    const double* sp[6];
+    double cw[6];
+#pragma unroll
+    for (int t = 0; t < 6; ++t) {
+        sp[t] = t < ns ? ss.src[h][t] : bp;
+        cw[t] = t < ns ? ss.c[h][t] : 0.0;
+    }
     // this lane's stencil point: weights, class code and metrics requested together with the
     // region loads below (one memory round trip after the receiver's base is known)
     const int ai = a & 3, aj = a >> 2;
@@ -968,9 +979,11 @@ __global__ void __launch_bounds__(128) k_donor2d_r(RecvTask rt, SrcSets sets, Me
             }
         }
     }
-    // ---- stage the region ----
+    // ---- stage the region: every raw value (base and history terms) is copied to shared
+    // memory asynchronously (one memory round trip, no register staging), then combined
     if (live) {
-        double ld[4][4];
+        extern __shared__ double raw[];   // [8 receivers][rt.raw_k arrays][4 comps][64 points]
+        double* my = raw + (size_t)slot * rt.raw_k * 256;
         bool ok[4];
         int di[4], dj[4];
 #pragma unroll
@@ -984,27 +997,41 @@ __global__ void __launch_bounds__(128) k_donor2d_r(RecvTask rt, SrcSets sets, Me
                 di[s4] = kk & 3;
                 dj[s4] = r6 < 3 ? r6 - 3 : r6 + 1;
             }
+            ok[s4] = true;
             if (!VISC && !(dj[s4] >= 0 && dj[s4] < 4 && di[s4] >= 0 && di[s4] < 4)) {
                 ok[s4] = false;
                 continue;
             }
             int ii = ib + di[s4], jj = jb + dj[s4];
-            ok[s4] = true;
             if (ii < 0 || ii >= n0) {
-                if (m.periodic[0]) ii = ii < 0 ? ii + n0 : ii - n0; else ok[s4] = false;
+                if (per0) ii = ii < 0 ? ii + n0 : ii - n0; else ok[s4] = false;
             }
             if (jj < 0 || jj >= n1) {
-                if (m.periodic[1]) jj = jj < 0 ? jj + n1 : jj - n1; else ok[s4] = false;
+                if (per1) jj = jj < 0 ? jj + n1 : jj - n1; else ok[s4] = false;
             }
+            if (!ok[s4]) continue;
             const unsigned q = (unsigned)ii + (unsigned)n0 * (unsigned)jj;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                cp_async8(my + c * 64 + k, bp + (c * uN + q));
+#pragma unroll
+                for (int t = 0; t < 6; ++t)
+                    if (t < ns) cp_async8(my + ((1 + t) * 4 + c) * 64 + k, sp[t] + (c * uN + q));
+            }
+        }
+        cp_async_wait_all();
+        double ld[4][4];
+#pragma unroll
+        for (int s4 = 0; s4 < 4; ++s4) {
+            const int k = a + 16 * s4;
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 double v = 0.0;
                 if (ok[s4]) {
-                    v = __ldg(ss.base[h] + (c * uN + q));
+                    v = my[c * 64 + k];
 #pragma unroll
-                    for (int t = 0; t < 4; ++t)
-                        if (t < ns) v += ss.c[h][t] * __ldg(ss.src[h][t] + (c * uN + q));
+                    for (int t = 0; t < 6; ++t)
+                        if (t < ns) v += cw[t] * my[((1 + t) * 4 + c) * 64 + k];
                 }
                 ld[s4][c] = v;
             }
@@ -1106,8 +1133,13 @@ __global__ void __launch_bounds__(128) k_donor2d_r(RecvTask rt, SrcSets sets, Me
     }
 }
 
-void launch_donor2d(const RecvTask& rt, const SrcSets& ss, const MeshTable& mt, const Gas& gas,
+void launch_donor2d(const RecvTask& rt0, const SrcSets& ss, const MeshTable& mt, const Gas& gas,
                     cudaStream_t st) {
+    RecvTask rt = rt0;
+    int nsmax = 0;
+    for (int i = 0; i < rt.nmesh; ++i)
+        for (int h = 0; h < 8; ++h) nsmax = std::max(nsmax, std::min(6, ss.s[rt.set[i]].nsrc[h]));
+    rt.raw_k = 1 + nsmax;
     const int64_t tot = rt.off[rt.nmesh];
     if (tot <= 0) return;
     const unsigned nb = (unsigned)((tot * 16 + 127) / 128);
@@ -1121,6 +1153,8 @@ void launch_donor2d(const RecvTask& rt, const SrcSets& ss, const MeshTable& mt, 
     cfg.gridDim = dim3(nb);
     cfg.blockDim = dim3(128);
     cfg.stream = st;
+    // raw staging of the region-staged variant: 8 receivers x (1 + max history terms) x 4 x 64
+    cfg.dynamicSmemBytes = (size_t)8 * rt.raw_k * 256 * sizeof(double);
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributePriority;
     at[0].val.priority = greatest;
@@ -1132,9 +1166,16 @@ void launch_donor2d(const RecvTask& rt, const SrcSets& ss, const MeshTable& mt, 
         staged = e ? atoi(e) : 1;
     }
     if (staged) {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_donor2d_r<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+            cudaFuncSetAttribute(k_donor2d_r<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+            attr = true;
+        }
         if (gas.viscous) cudaLaunchKernelEx(&cfg, k_donor2d_r<true>, rt, ss, mt, gas);
         else cudaLaunchKernelEx(&cfg, k_donor2d_r<false>, rt, ss, mt, gas);
     } else {
+        cfg.dynamicSmemBytes = 0;
         if (gas.viscous) cudaLaunchKernelEx(&cfg, k_donor2d<true>, rt, ss, mt, gas);
         else cudaLaunchKernelEx(&cfg, k_donor2d<false>, rt, ss, mt, gas);
     }
