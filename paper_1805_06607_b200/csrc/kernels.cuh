@@ -64,6 +64,8 @@ struct Epilogue {
     int persist;
     // 2-D: interior tiles take the lean path (set by the launcher; MRAB_LEAN=0 disables)
     int lean;
+    // 2-D: `tiles` are all interior: launch the lean-only kernel (k_rhs2d_lean)
+    int lean_only;
     // launch timeline (mrab_set_trace; NULL = off): one record per CTA, see trace_rec
     unsigned long long* trace;
     int trace_tag;

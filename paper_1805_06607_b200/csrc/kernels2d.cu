@@ -1299,11 +1299,66 @@ bool rhs2d_tma_possible(const DevMesh& m, const Epilogue& ep, const double* Q);
 bool launch_rhs2d_tma(const DevMesh& m, const double* Q, const Gas& g, const Epilogue& ep,
                       cudaStream_t st);
 
+// Lean-only kernel over a list of interior tiles: with the general path compiled out it needs
+// 69.6 KB of shared memory (Cartesian) and 80 registers (three CTAs per SM).  Diagnostic only
+// (mrab_time_kernel kernel 3; kernel 4 = the same tiles in the mixed kernel): measured 53.6 us
+// vs 48.4 us for the mixed kernel on the config-3 interior tiles, i.e. occupancy is not what
+// limits the lean path (its L1/LSU data pipe runs at 63 % of peak).
+template <bool VISC, bool CART, int NS>
+__global__ void __launch_bounds__(256, CART ? 3 : 2) k_rhs2d_lean(DevMesh m, const double* __restrict__ Q,
+                                                                  Gas g, Epilogue ep) {
+    extern __shared__ __align__(16) double smem[];
+    unsigned long long t0 = 0, tph[2] = {0, 0};
+    if (ep.trace && threadIdx.x == 0) t0 = gtimer();
+    const int ntx = (m.n[0] + TX - 1) / TX;
+    const int tl = (int)((unsigned)ep.tiles[blockIdx.x] & 0x7fffffffu);
+    const int by = tl / ntx, bx = tl - by * ntx;
+    rhs2d_tile_lean<VISC, CART, 16, 256, NS>(m, Q, g, ep, bx, by, smem, tph);
+    if (ep.trace) {
+        __syncthreads();
+        if (threadIdx.x == 0) trace_rec(ep.trace, ep.trace_tag, t0, tph[0], tph[1]);
+    }
+}
+
+template <bool VISC, bool CART, int NS>
+static void launch_lean(const DevMesh& m, const double* Q, const Gas& g, const Epilogue& ep, cudaStream_t st) {
+    static bool init = false;
+    const size_t bytes = GeoL<VISC, 16>::bytes(CART);
+    if (!init) {
+        cudaFuncSetAttribute(k_rhs2d_lean<VISC, CART, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        init = true;
+    }
+    k_rhs2d_lean<VISC, CART, NS><<<ep.ntiles, 256, bytes, st>>>(m, Q, g, ep);
+}
+
+static void launch_rhs2d_lean(const DevMesh& m, const double* Q, const Gas& g, const Epilogue& ep0,
+                              cudaStream_t st) {
+    if (ep0.ntiles <= 0) return;
+    Epilogue ep = ep0;
+    ep.lean = 1;
+    const int ns = ep.y_out ? ep.nsrc : -1;
+#define MRAB_LEANL(V, C)                                          \
+    if (ns == 2) launch_lean<V, C, 2>(m, Q, g, ep, st);           \
+    else if (ns == 3) launch_lean<V, C, 3>(m, Q, g, ep, st);      \
+    else launch_lean<V, C, -1>(m, Q, g, ep, st);
+    if (g.viscous) {
+        if (m.cart) { MRAB_LEANL(true, true) } else { MRAB_LEANL(true, false) }
+    } else {
+        if (m.cart) { MRAB_LEANL(false, true) } else { MRAB_LEANL(false, false) }
+    }
+#undef MRAB_LEANL
+}
+
 bool launch_rhs2d_march(const DevMesh& m, const double* Q, const Gas& g, const Epilogue& ep,
                         cudaStream_t st);
 
 void launch_rhs2d(const DevMesh& m, const double* Q, const Gas& g, const Epilogue& ep,
                   const DonorSet& ds, cudaStream_t st) {
+    // interior tiles only: the lean kernel
+    if (ep.lean_only) {
+        launch_rhs2d_lean(m, Q, g, ep, st);
+        return;
+    }
     // row-marching kernel for large viscous meshes (whole-mesh launches)
     if (launch_rhs2d_march(m, Q, g, ep, st)) return;
     // persistent TMA-pipelined kernel whenever its layout constraints hold (opt-in)

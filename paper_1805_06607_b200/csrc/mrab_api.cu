@@ -64,6 +64,7 @@ struct MeshDev {
     int32_t* tlist = nullptr;     // 2-D: all tiles, non-interior first (bit 31 = interior)
     double* satv = nullptr;       // [6][N] SAT viscous-flux scratch of the row-marching kernel
     int ncrit = 0, nbulk = 0;
+    int ngen = 0;                 // non-interior tiles at the head of tlist
     DevMesh dm{};
 };
 
@@ -983,6 +984,7 @@ mrab_status mrab_create(const mrab_plan* plan, const double* const* q0, void* d_
                 }
             D.ncrit = (int)crit.size();
             D.nbulk = (int)bulk.size();
+            D.ngen = (int)slow.size();
             crit.insert(crit.end(), bulk.begin(), bulk.end());
             CK(cudaMemcpy(D.tiles, crit.data(), crit.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
             // the longer non-interior tiles go first so they do not form the tail
@@ -1168,7 +1170,7 @@ mrab_status mrab_launches_per_macro_step(mrab_ctx* c, int64_t* launches) {
 
 mrab_status mrab_time_kernel(mrab_ctx* c, int kernel, int mesh, int reps, int flush_l2,
                              double* ms_per_launch, double* algorithmic_bytes) {
-    if (!c || mesh < 0 || mesh >= (int)c->md.size() || reps < 1 || kernel < 0 || kernel > 2)
+    if (!c || mesh < 0 || mesh >= (int)c->md.size() || reps < 1 || kernel < 0 || kernel > 4)
         return fail(MRAB_E_INVALID, "bad arguments");
     const Plan& P = *c->P;
     const MeshPlan& mp = P.meshes[mesh];
@@ -1190,7 +1192,7 @@ mrab_status mrab_time_kernel(mrab_ctx* c, int kernel, int mesh, int reps, int fl
     for (int r = 0; r < reps; ++r) {
         if (flush) launch_l2_scrub(flush, (char*)flush + fbytes, fbytes, r, c->st);
         CK(cudaEventRecord(e0, c->st));
-        if (kernel == 0) {
+        if (kernel == 0 || kernel >= 3) {
             Epilogue ep{};
             ep.r_out = D.kbuf[0];
             ep.y_out = D.kbuf[1];
@@ -1201,9 +1203,20 @@ mrab_status mrab_time_kernel(mrab_ctx* c, int kernel, int mesh, int reps, int fl
                 ep.src[k] = D.ring[k];
                 ep.csrc[k] = P.h * mp.s * P.coef[mesh][mp.s][k];
             }
+            double Nk = N;
+            if (kernel >= 3 && d == 2) {
+                // diagnostics: only the interior tiles, in the lean-only kernel (3) or in the
+                // mixed kernel (4)
+                ep.tiles = D.tlist + D.ngen;
+                ep.ntiles = D.dm.ntl - D.ngen;
+                ep.lean_only = kernel == 3;
+                int tx, ty;
+                rhs2d_tile_shape(&tx, &ty);
+                Nk = (double)ep.ntiles * tx * ty;
+            }
             launch_rhs(d, D.dm, Q, D.FV, c->gas, ep, make_ds(c, state_of.data()), c->st);
             // Q read, R written, (m-1) ring reads, state written, metrics if curvilinear
-            bytes = 8.0 * N * (nc * (m + 2) + (mp.cartesian ? 0 : 1 + d * d));
+            bytes = 8.0 * Nk * (nc * (m + 2) + (mp.cartesian ? 0 : 1 + d * d));
         } else if (kernel == 1) {
             // the box the MRAB step uses: whole mesh (3-D), donor box (2-D)
             Box b = (d == 3 || !mp.is_donor) ? whole_box(mp) : make_box(mp.fv_lo, mp.fv_hi);
