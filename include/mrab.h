@@ -146,7 +146,9 @@ mrab_status mrab_launches_per_macro_step(mrab_ctx* ctx, int64_t* launches);
 
 /* Live timing of one hot kernel of mesh `mesh` exactly as the MRAB step launches it, but
  * writing to scratch buffers (the integrator state is not changed): kernel 0 = fused
- * RHS + SAT + AB update, 1 = viscous-flux pass, 2 = donor gather of this mesh's receivers.
+ * RHS + SAT + AB update, 1 = viscous-flux pass, 2 = donor gather of this mesh's receivers;
+ * 2-D diagnostics: 3 = the interior tiles alone in the lean-only kernel, 4 = the same tiles in
+ * the mixed kernel (their algorithmic bytes only).
  * Each of `reps` launches is bracketed by CUDA events on the context stream; with
  * flush_l2 != 0 a 256 MiB buffer is written between launches (outside the events).
  * Outputs: mean ms per launch, and the kernel's ALGORITHMIC bytes per launch.
