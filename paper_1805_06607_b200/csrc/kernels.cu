@@ -362,11 +362,16 @@ __global__ void __launch_bounds__(NT3, 2) k_rhs3d(DevMesh m, const double* __res
     const int i0 = blockIdx.x * T3X, j0 = blockIdx.y * T3Y, k0 = blockIdx.z * T3Z;
     const int tid = threadIdx.x;
 
-    for (int t = tid; t < T3N; t += NT3) {
+    // class codes requested now, stored to shared memory only after the first region loads
+    // are in flight (storing them at once serialised a memory round trip before those loads)
+    unsigned clsv[PPT3];
+#pragma unroll
+    for (int s = 0; s < PPT3; ++s) {
+        const int t = tid + s * NT3;
         const int x = t & 7, y = (t >> 3) & 7, z = t >> 6;
         const int gi = i0 + x, gj = j0 + y, gk = k0 + z;
         const bool live = gi < n0 && gj < n1 && gk < n2;
-        sc[t] = live ? m.cls[gi + s1 * gj + s2 * gk] : (uint16_t)0;
+        clsv[s] = live ? m.cls[gi + s1 * gj + s2 * gk] : 0u;
 #pragma unroll
         for (int c = 0; c < NC; ++c) racc[c * T3N + t] = 0.0;
     }
@@ -454,6 +459,9 @@ __global__ void __launch_bounds__(NT3, 2) k_rhs3d(DevMesh m, const double* __res
 #pragma unroll
             for (int c = 0; c < NC; ++c) fb[c * REG3 + t] = fh[c];
         }
+        if (kap == 0)
+#pragma unroll
+            for (int s = 0; s < PPT3; ++s) sc[tid + s * NT3] = (uint16_t)clsv[s];
         __syncthreads();
         // ---- D_kappa of the staged fluxes at the tile points
         const int sk = kap == 0 ? 1 : (kap == 1 ? RX : RX * RY);
@@ -561,10 +569,14 @@ __global__ void __launch_bounds__(NT3, 2) k_visc3d(DevMesh m, const double* __re
     const int i0 = box.lo[0] + blockIdx.x * T3X, j0 = box.lo[1] + blockIdx.y * T3Y,
               k0 = box.lo[2] + blockIdx.z * T3Z;
     const int tid = threadIdx.x;
-    for (int t = tid; t < T3N; t += NT3) {
+    // class codes: stored to shared memory after the first region loads are issued
+    unsigned clsv[PPT3];
+#pragma unroll
+    for (int s = 0; s < PPT3; ++s) {
+        const int t = tid + s * NT3;
         const int gi = i0 + (t & 7), gj = j0 + ((t >> 3) & 7), gk = k0 + (t >> 6);
         const bool live = gi <= box.hi[0] && gj <= box.hi[1] && gk <= box.hi[2];
-        sc[t] = live ? m.cls[gi + s1 * gj + s2 * gk] : (uint16_t)0;
+        clsv[s] = live ? m.cls[gi + s1 * gj + s2 * gk] : 0u;
     }
     double d[PPT3][3][4];   // d[s][kappa][u,v,w,T]
 #pragma unroll
@@ -599,6 +611,9 @@ __global__ void __launch_bounds__(NT3, 2) k_visc3d(DevMesh m, const double* __re
             pv[2][t] = w;
             pv[3][t] = g.gamma * g.gm1 * (lq[r][4] - 0.5 * (lq[r][1] * u + lq[r][2] * v + lq[r][3] * w)) * ir;
         }
+        if (kap == 0)
+#pragma unroll
+            for (int s = 0; s < PPT3; ++s) sc[tid + s * NT3] = (uint16_t)clsv[s];
         __syncthreads();
         const int sk = kap == 0 ? 1 : (kap == 1 ? RX : RX * RY);
 #pragma unroll
