@@ -683,6 +683,160 @@ __global__ void __launch_bounds__(NT3, 2) k_visc3d(DevMesh m, const double* __re
 }
 
 // ------------------------------------------------------------------------------------
+// 3-D viscous fluxes, one memory round trip per tile: the state of the whole cross-shaped
+// region the three D1 passes read (tile 8^3 plus 3 layers on each of its six faces: 1664
+// points) is copied to shared memory by cp.async at once, turned into primitives in place,
+// and every gradient is taken from there (k_visc3d loaded one direction-extended region per
+// pass: three dependent round trips).  Same arithmetic as k_visc3d.
+// Cross-region index of tile-relative (x, y, z): the tile itself x + 8 y + 64 z, then the six
+// 3-deep face slabs (x-, x+, y-, y+, z-, z+) of 192 points each.
+// ------------------------------------------------------------------------------------
+constexpr int XREG = 512 + 6 * 192;   // 1664
+__device__ __forceinline__ int xreg_idx(int x, int y, int z) {
+    if (x < 0) return 512 + (x + 3) + 3 * (y + 8 * z);
+    if (x >= 8) return 512 + 192 + (x - 8) + 3 * (y + 8 * z);
+    if (y < 0) return 512 + 2 * 192 + (y + 3) + 3 * (x + 8 * z);
+    if (y >= 8) return 512 + 3 * 192 + (y - 8) + 3 * (x + 8 * z);
+    if (z < 0) return 512 + 4 * 192 + (z + 3) + 3 * (x + 8 * y);
+    if (z >= 8) return 512 + 5 * 192 + (z - 8) + 3 * (x + 8 * y);
+    return x + 8 * y + 64 * z;
+}
+__device__ __forceinline__ void xreg_xyz(int t, int& x, int& y, int& z) {
+    if (t < 512) {
+        x = t & 7; y = (t >> 3) & 7; z = t >> 6;
+        return;
+    }
+    const int k = t - 512, side = k / 192, w = k - side * 192;
+    const int a = w % 3, b = (w / 3) & 7, c = w / 24;
+    const int lo = a - 3, hi = 8 + a;
+    switch (side) {
+        case 0: x = lo; y = b; z = c; break;
+        case 1: x = hi; y = b; z = c; break;
+        case 2: y = lo; x = b; z = c; break;
+        case 3: y = hi; x = b; z = c; break;
+        case 4: z = lo; x = b; y = c; break;
+        default: z = hi; x = b; y = c; break;
+    }
+}
+constexpr size_t SMEMX = sizeof(double) * 5 * XREG;
+
+template <bool CART>
+__global__ void __launch_bounds__(NT3, 2) k_visc3d_x(DevMesh m, const double* __restrict__ Q,
+                                                    double* __restrict__ FV, Box box, Gas g) {
+    extern __shared__ __align__(16) double xr[];   // [5][XREG]: state, then (rho, u, v, w, T)
+    __shared__ uint16_t sc[T3N];
+    const int n0 = m.n[0], n1 = m.n[1], n2 = m.n[2];
+    const int64_t N = m.npts;
+    const int64_t s1 = n0, s2 = (int64_t)n0 * n1;
+    const int i0 = box.lo[0] + blockIdx.x * T3X, j0 = box.lo[1] + blockIdx.y * T3Y,
+              k0 = box.lo[2] + blockIdx.z * T3Z;
+    const int tid = threadIdx.x;
+    const int per0 = m.periodic[0], per1 = m.periodic[1], per2 = m.periodic[2];
+    // ---- one round trip: the whole cross region (points outside a non-periodic mesh are
+    // clamped to a valid address; no active stencil reads them)
+    for (int t = tid; t < XREG; t += NT3) {
+        int x, y, z;
+        xreg_xyz(t, x, y, z);
+        int gi = i0 + x, gj = j0 + y, gk = k0 + z;
+        if (gi < 0) gi = per0 ? gi + n0 : 0; else if (gi >= n0) gi = per0 ? gi - n0 : n0 - 1;
+        if (gj < 0) gj = per1 ? gj + n1 : 0; else if (gj >= n1) gj = per1 ? gj - n1 : n1 - 1;
+        if (gk < 0) gk = per2 ? gk + n2 : 0; else if (gk >= n2) gk = per2 ? gk - n2 : n2 - 1;
+        const int64_t q = gi + s1 * gj + s2 * gk;
+#pragma unroll
+        for (int c = 0; c < 5; ++c) {
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(xr + c * XREG + t);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(Q + c * N + q));
+        }
+    }
+    unsigned clsv[PPT3];
+#pragma unroll
+    for (int s = 0; s < PPT3; ++s) {
+        const int t = tid + s * NT3;
+        const int gi = i0 + (t & 7), gj = j0 + ((t >> 3) & 7), gk = k0 + (t >> 6);
+        const bool live = gi <= box.hi[0] && gj <= box.hi[1] && gk <= box.hi[2];
+        clsv[s] = live ? m.cls[gi + s1 * gj + s2 * gk] : 0u;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    // ---- primitives in place
+    for (int t = tid; t < XREG; t += NT3) {
+        const double r = xr[t], mu = xr[XREG + t], mv = xr[2 * XREG + t], mw = xr[3 * XREG + t];
+        const double E = xr[4 * XREG + t];
+        const double ir = rcp64(r);
+        const double u = mu * ir, v = mv * ir, w = mw * ir;
+        xr[XREG + t] = u;
+        xr[2 * XREG + t] = v;
+        xr[3 * XREG + t] = w;
+        xr[4 * XREG + t] = g.gamma * g.gm1 * (E - 0.5 * (mu * u + mv * v + mw * w)) * ir;
+    }
+#pragma unroll
+    for (int s = 0; s < PPT3; ++s) sc[tid + s * NT3] = (uint16_t)clsv[s];
+    __syncthreads();
+    const double* pf = xr + XREG;   // [4][XREG]: u, v, w, T
+#pragma unroll
+    for (int s = 0; s < PPT3; ++s) {
+        const int t = tid + s * NT3;
+        const unsigned code = sc[t];
+        if (!code) continue;
+        const int x = t & 7, y = (t >> 3) & 7, z = t >> 6;
+        double d[3][4];   // d[kappa][u, v, w, T]
+#pragma unroll
+        for (int kap = 0; kap < 3; ++kap) {
+            const int cl = (code >> (4 * kap)) & 15;
+            auto at = [&](int o) {
+                return kap == 0 ? xreg_idx(x + o, y, z) : (kap == 1 ? xreg_idx(x, y + o, z) : xreg_idx(x, y, z + o));
+            };
+            if (cl == CLS_INT) {
+                const int a1 = at(1), b1 = at(-1), a2 = at(2), b2 = at(-2);
+#pragma unroll
+                for (int f = 0; f < 4; ++f) {
+                    const double* a = pf + f * XREG;
+                    d[kap][f] = (2.0 / 3.0) * (a[a1] - a[b1]) - (1.0 / 12.0) * (a[a2] - a[b2]);
+                }
+            } else {
+#pragma unroll
+                for (int f = 0; f < 4; ++f) d[kap][f] = 0.0;
+                const int ns = c_nst[cl];
+                for (int tt = 0; tt < ns; ++tt) {
+                    const double cf = c_cf[cl][tt];
+                    const int o = at(c_off[cl][tt]);
+#pragma unroll
+                    for (int f = 0; f < 4; ++f) d[kap][f] += cf * pf[f * XREG + o];
+                }
+            }
+        }
+        const double u[3] = {pf[t], pf[XREG + t], pf[2 * XREG + t]};
+        const int64_t p = (i0 + x) + s1 * (j0 + y) + s2 * (k0 + z);
+        double gr[4][3];   // gr[f][i] = d phi_f / d x_i
+#pragma unroll
+        for (int f = 0; f < 4; ++f)
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                if (CART) {
+                    gr[f][i] = m.cJ * (m.cM[i] * d[i][f]);
+                } else {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) acc += __ldg(m.M + (k * 3 + i) * N + p) * d[k][f];
+                    gr[f][i] = __ldg(m.J + p) * acc;
+                }
+            }
+        const double div = gr[0][0] + gr[1][1] + gr[2][2];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            double e = 0.0;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const double tau = (gr[i][j] + gr[j][i] - (i == j ? (2.0 / 3.0) * div : 0.0)) * g.iRe;
+                FV[(int64_t)(i * 4 + j) * N + p] = tau;
+                e += u[j] * tau;
+            }
+            FV[(int64_t)(i * 4 + 3) * N + p] = e + g.kT * gr[3][i];
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
 // intermediate states on a box: out = base + sum_k c_k src_k (all components)
 // ------------------------------------------------------------------------------------
 struct CombineArgs {
@@ -780,8 +934,20 @@ void launch_visc(int dim, const DevMesh& m, const double* Q, double* FV, const B
     if (dim == 3 && !direct) {
         dim3 grid((box.hi[0] - box.lo[0] + T3X) / T3X, (box.hi[1] - box.lo[1] + T3Y) / T3Y,
                   (box.hi[2] - box.lo[2] + T3Z) / T3Z);
-        if (m.cart) k_visc3d<true><<<grid, NT3, 0, st>>>(m, Q, FV, box, gas);
-        else k_visc3d<false><<<grid, NT3, 0, st>>>(m, Q, FV, box, gas);
+        static int xr = -1;
+        if (xr < 0) {
+            const char* e = getenv("MRAB_VISC3D_X");
+            xr = e ? atoi(e) : 1;
+            cudaFuncSetAttribute(k_visc3d_x<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEMX);
+            cudaFuncSetAttribute(k_visc3d_x<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEMX);
+        }
+        if (xr) {
+            if (m.cart) k_visc3d_x<true><<<grid, NT3, SMEMX, st>>>(m, Q, FV, box, gas);
+            else k_visc3d_x<false><<<grid, NT3, SMEMX, st>>>(m, Q, FV, box, gas);
+        } else {
+            if (m.cart) k_visc3d<true><<<grid, NT3, 0, st>>>(m, Q, FV, box, gas);
+            else k_visc3d<false><<<grid, NT3, 0, st>>>(m, Q, FV, box, gas);
+        }
         return;
     }
     if (dim == 2) {
