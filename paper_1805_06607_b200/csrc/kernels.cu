@@ -915,6 +915,67 @@ __global__ void __launch_bounds__(128) k_interp(RecvList rl, DonorSet ds) {
         for (int c = 0; c < NF; ++c) rl.fvhat[c * rl.n + r] = fa[c];
 }
 
+// 3-D gather, four lanes per receiver: lane a0 takes the stencil column i = b0 + a0, so the
+// four lanes of a receiver read 32 contiguous bytes per (j, k) row (one sector instead of four
+// scattered ones); the column sums are reduced over the quad with two shuffles per value.
+template <bool VISC>
+__global__ void __launch_bounds__(128) k_interp3q(RecvList rl, DonorSet ds) {
+    constexpr int NC = 5, NF = 12;
+    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 2;
+    const int a0 = threadIdx.x & 3;
+    const bool live = r < rl.n;
+    double qa[NC], fa[VISC ? NF : 1];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) qa[c] = 0.0;
+    if (VISC)
+#pragma unroll
+        for (int c = 0; c < NF; ++c) fa[c] = 0.0;
+    if (live) {
+        const int dm = rl.donor[r];
+        const int b0 = rl.base[r * 3 + 0], b1 = rl.base[r * 3 + 1], b2 = rl.base[r * 3 + 2];
+        const int n0 = ds.n[dm][0], n1 = ds.n[dm][1], n2 = ds.n[dm][2];
+        const int64_t N = ds.npts[dm];
+        const double* __restrict__ S = ds.state[dm];
+        const double* __restrict__ F = ds.fv[dm];
+        const double* w = rl.w + r * 12;
+        int ii = b0 + a0;
+        if (ii >= n0) ii -= n0;
+        const double w0 = w[a0];
+#pragma unroll 4
+        for (int a = 0; a < 16; ++a) {
+            const int a1 = a & 3, a2 = a >> 2;
+            int jj = b1 + a1, kk = b2 + a2;
+            if (jj >= n1) jj -= n1;
+            if (kk >= n2) kk -= n2;
+            const double W = w0 * w[4 + a1] * w[8 + a2];
+            const int64_t q = ii + (int64_t)n0 * (jj + (int64_t)n1 * kk);
+#pragma unroll
+            for (int c = 0; c < NC; ++c) qa[c] += W * __ldg(S + c * N + q);
+            if (VISC)
+#pragma unroll
+                for (int c = 0; c < NF; ++c) fa[c] += W * __ldg(F + c * N + q);
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        qa[c] += __shfl_xor_sync(0xffffffffu, qa[c], 1);
+        qa[c] += __shfl_xor_sync(0xffffffffu, qa[c], 2);
+    }
+    if (VISC)
+#pragma unroll
+        for (int c = 0; c < NF; ++c) {
+            fa[c] += __shfl_xor_sync(0xffffffffu, fa[c], 1);
+            fa[c] += __shfl_xor_sync(0xffffffffu, fa[c], 2);
+        }
+    if (live && a0 == 0) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) rl.qhat[c * rl.n + r] = qa[c];
+        if (VISC)
+#pragma unroll
+            for (int c = 0; c < NF; ++c) rl.fvhat[c * rl.n + r] = fa[c];
+    }
+}
+
 // ------------------------------------------------------------------------------------
 // launchers
 // ------------------------------------------------------------------------------------
@@ -1059,8 +1120,19 @@ void launch_interp(int dim, int viscous, const RecvList& rl, const DonorSet& ds,
         if (viscous) k_interp<2, true><<<nb, 128, 0, st>>>(rl, ds);
         else k_interp<2, false><<<nb, 128, 0, st>>>(rl, ds);
     } else {
-        if (viscous) k_interp<3, true><<<nb, 128, 0, st>>>(rl, ds);
-        else k_interp<3, false><<<nb, 128, 0, st>>>(rl, ds);
+        static int quad = -1;
+        if (quad < 0) {
+            const char* e = getenv("MRAB_INTERP_QUAD");
+            quad = e ? atoi(e) : 1;
+        }
+        if (quad) {
+            const unsigned nbq = (unsigned)((rl.n * 4 + 127) / 128);
+            if (viscous) k_interp3q<true><<<nbq, 128, 0, st>>>(rl, ds);
+            else k_interp3q<false><<<nbq, 128, 0, st>>>(rl, ds);
+        } else {
+            if (viscous) k_interp<3, true><<<nb, 128, 0, st>>>(rl, ds);
+            else k_interp<3, false><<<nb, 128, 0, st>>>(rl, ds);
+        }
     }
 }
 
