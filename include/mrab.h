@@ -148,7 +148,7 @@ mrab_status mrab_launches_per_macro_step(mrab_ctx* ctx, int64_t* launches);
  * writing to scratch buffers (the integrator state is not changed): kernel 0 = fused
  * RHS + SAT + AB update, 1 = viscous-flux pass, 2 = donor gather of this mesh's receivers;
  * 2-D diagnostics: 3 = the interior tiles alone in the lean-only kernel, 4 = the same tiles in
- * the mixed kernel (their algorithmic bytes only).
+ * the mixed kernel, 5 = the non-interior tiles alone (their algorithmic bytes only).
  * Each of `reps` launches is bracketed by CUDA events on the context stream; with
  * flush_l2 != 0 a 256 MiB buffer is written between launches (outside the events).
  * Outputs: mean ms per launch, and the kernel's ALGORITHMIC bytes per launch.

@@ -1170,7 +1170,7 @@ mrab_status mrab_launches_per_macro_step(mrab_ctx* c, int64_t* launches) {
 
 mrab_status mrab_time_kernel(mrab_ctx* c, int kernel, int mesh, int reps, int flush_l2,
                              double* ms_per_launch, double* algorithmic_bytes) {
-    if (!c || mesh < 0 || mesh >= (int)c->md.size() || reps < 1 || kernel < 0 || kernel > 4)
+    if (!c || mesh < 0 || mesh >= (int)c->md.size() || reps < 1 || kernel < 0 || kernel > 5)
         return fail(MRAB_E_INVALID, "bad arguments");
     const Plan& P = *c->P;
     const MeshPlan& mp = P.meshes[mesh];
@@ -1206,9 +1206,9 @@ mrab_status mrab_time_kernel(mrab_ctx* c, int kernel, int mesh, int reps, int fl
             double Nk = N;
             if (kernel >= 3 && d == 2) {
                 // diagnostics: only the interior tiles, in the lean-only kernel (3) or in the
-                // mixed kernel (4)
-                ep.tiles = D.tlist + D.ngen;
-                ep.ntiles = D.dm.ntl - D.ngen;
+                // mixed kernel (4); only the non-interior tiles (5)
+                ep.tiles = kernel == 5 ? D.tlist : D.tlist + D.ngen;
+                ep.ntiles = kernel == 5 ? D.ngen : D.dm.ntl - D.ngen;
                 ep.lean_only = kernel == 3;
                 int tx, ty;
                 rhs2d_tile_shape(&tx, &ty);
