@@ -837,6 +837,332 @@ __global__ void __launch_bounds__(NT3, 2) k_visc3d_x(DevMesh m, const double* __
 }
 
 // ------------------------------------------------------------------------------------
+// 3-D RHS in two passes (opt-in, MRAB_3D_SPLIT=1; default k_visc3d_x + k_rhs3d):
+//   k_flux3d  per tile: the cross-shaped state region staged by cp.async in one round trip
+//             (as k_visc3d_x), primitives in place, D1 gradients at the tile points, then the
+//             full contravariant fluxes Fhat_kappa = sum_i M_kappa,i (F^I_i - F^V_i) of every
+//             point written once ([3][5][N]); the Cartesian viscous fluxes F^V are written only
+//             in tiles that hold SAT points or donor stencils (the SAT term and the gathers
+//             read them there);
+//   k_div3d   per tile: the three kappa-extended regions of Fhat_kappa staged by cp.async in
+//             one round trip, D_kappa by class code (segment closures), R = -J sum_kappa,
+//             SAT, AB / RK epilogue.
+// k_rhs3d formed every flux on the tile extended by 3 along each direction from Q and F^V
+// (three dependent round trips, 1.75x redundant flux work).
+// ------------------------------------------------------------------------------------
+template <bool VISC, bool CART>
+__global__ void __launch_bounds__(NT3, 2) k_flux3d(DevMesh m, const double* __restrict__ Q,
+                                                  double* __restrict__ FH, double* __restrict__ FV,
+                                                  const uint8_t* __restrict__ fvtile, Gas g) {
+    extern __shared__ __align__(16) double xr[];   // [5][XREG]: state, then (rho, u, v, w, T)
+    __shared__ uint16_t sc[T3N];
+    const int n0 = m.n[0], n1 = m.n[1], n2 = m.n[2];
+    const int64_t N = m.npts;
+    const int64_t s1 = n0, s2 = (int64_t)n0 * n1;
+    const int i0 = blockIdx.x * T3X, j0 = blockIdx.y * T3Y, k0 = blockIdx.z * T3Z;
+    const int tid = threadIdx.x;
+    const int per0 = m.periodic[0], per1 = m.periodic[1], per2 = m.periodic[2];
+    const bool wfv = VISC && fvtile[blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)];
+    const int nreg = VISC ? XREG : T3N;   // Euler: no gradients, the tile itself suffices
+    for (int t = tid; t < nreg; t += NT3) {
+        int x, y, z;
+        xreg_xyz(t, x, y, z);
+        int gi = i0 + x, gj = j0 + y, gk = k0 + z;
+        if (gi < 0) gi = per0 ? gi + n0 : 0; else if (gi >= n0) gi = per0 ? gi - n0 : n0 - 1;
+        if (gj < 0) gj = per1 ? gj + n1 : 0; else if (gj >= n1) gj = per1 ? gj - n1 : n1 - 1;
+        if (gk < 0) gk = per2 ? gk + n2 : 0; else if (gk >= n2) gk = per2 ? gk - n2 : n2 - 1;
+        const int64_t q = gi + s1 * gj + s2 * gk;
+#pragma unroll
+        for (int c = 0; c < 5; ++c) {
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(xr + c * XREG + t);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(Q + c * N + q));
+        }
+    }
+    unsigned clsv[PPT3];
+#pragma unroll
+    for (int s = 0; s < PPT3; ++s) {
+        const int t = tid + s * NT3;
+        const int gi = i0 + (t & 7), gj = j0 + ((t >> 3) & 7), gk = k0 + (t >> 6);
+        const bool live = gi < n0 && gj < n1 && gk < n2;
+        clsv[s] = live ? m.cls[gi + s1 * gj + s2 * gk] : 0u;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    for (int t = tid; t < nreg; t += NT3) {
+        const double r = xr[t], mu = xr[XREG + t], mv = xr[2 * XREG + t], mw = xr[3 * XREG + t];
+        const double E = xr[4 * XREG + t];
+        const double ir = rcp64(r);
+        const double u = mu * ir, v = mv * ir, w = mw * ir;
+        xr[XREG + t] = u;
+        xr[2 * XREG + t] = v;
+        xr[3 * XREG + t] = w;
+        xr[4 * XREG + t] = g.gamma * g.gm1 * (E - 0.5 * (mu * u + mv * v + mw * w)) * ir;
+    }
+#pragma unroll
+    for (int s = 0; s < PPT3; ++s) sc[tid + s * NT3] = (uint16_t)clsv[s];
+    __syncthreads();
+    const double* pf = xr + XREG;   // [4][XREG]: u, v, w, T
+#pragma unroll
+    for (int s = 0; s < PPT3; ++s) {
+        const int t = tid + s * NT3;
+        const int x = t & 7, y = (t >> 3) & 7, z = t >> 6;
+        if (i0 + x >= n0 || j0 + y >= n1 || k0 + z >= n2) continue;
+        const int64_t p = (i0 + x) + s1 * (j0 + y) + s2 * (k0 + z);
+        const unsigned code = sc[t];
+        if (!code) {
+#pragma unroll
+            for (int c = 0; c < 15; ++c) FH[(int64_t)c * N + p] = 0.0;
+            continue;
+        }
+        const double r = xr[t];
+        const double u[3] = {pf[t], pf[XREG + t], pf[2 * XREG + t]};
+        const double T = pf[3 * XREG + t];
+        const double pr = r * T * g.igamma;
+        const double E = pr * g.igm1 + 0.5 * r * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+        double fv[3][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}, {0, 0, 0, 0}};
+        double Jp = 0.0, Mp[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+        if (!CART) {
+            Jp = __ldg(m.J + p);
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+#pragma unroll
+                for (int i = 0; i < 3; ++i) Mp[k][i] = __ldg(m.M + (k * 3 + i) * N + p);
+        }
+        if (VISC) {
+            double d[3][4];   // d[kappa][u, v, w, T]
+#pragma unroll
+            for (int kap = 0; kap < 3; ++kap) {
+                const int cl = (code >> (4 * kap)) & 15;
+                auto at = [&](int o) {
+                    return kap == 0 ? xreg_idx(x + o, y, z) : (kap == 1 ? xreg_idx(x, y + o, z) : xreg_idx(x, y, z + o));
+                };
+                if (cl == CLS_INT) {
+                    const int a1 = at(1), b1 = at(-1), a2 = at(2), b2 = at(-2);
+#pragma unroll
+                    for (int f = 0; f < 4; ++f) {
+                        const double* a = pf + f * XREG;
+                        d[kap][f] = (2.0 / 3.0) * (a[a1] - a[b1]) - (1.0 / 12.0) * (a[a2] - a[b2]);
+                    }
+                } else {
+#pragma unroll
+                    for (int f = 0; f < 4; ++f) d[kap][f] = 0.0;
+                    const int ns = c_nst[cl];
+                    for (int tt = 0; tt < ns; ++tt) {
+                        const double cf = c_cf[cl][tt];
+                        const int o = at(c_off[cl][tt]);
+#pragma unroll
+                        for (int f = 0; f < 4; ++f) d[kap][f] += cf * pf[f * XREG + o];
+                    }
+                }
+            }
+            double gr[4][3];
+#pragma unroll
+            for (int f = 0; f < 4; ++f)
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    if (CART) {
+                        gr[f][i] = m.cJ * (m.cM[i] * d[i][f]);
+                    } else {
+                        double acc = 0.0;
+#pragma unroll
+                        for (int k = 0; k < 3; ++k) acc += Mp[k][i] * d[k][f];
+                        gr[f][i] = Jp * acc;
+                    }
+                }
+            const double div = gr[0][0] + gr[1][1] + gr[2][2];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                double e = 0.0;
+#pragma unroll
+                for (int j = 0; j < 3; ++j) {
+                    const double tau = (gr[i][j] + gr[j][i] - (i == j ? (2.0 / 3.0) * div : 0.0)) * g.iRe;
+                    fv[i][j] = tau;
+                    e += u[j] * tau;
+                }
+                fv[i][3] = e + g.kT * gr[3][i];
+            }
+            if (wfv)
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) FV[(int64_t)(i * 4 + j) * N + p] = fv[i][j];
+        }
+        // Cartesian fluxes F_i = F^I_i - F^V_i, then Fhat_kappa
+        double F[3][5];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const double mi = r * u[i];
+            F[i][0] = mi;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) F[i][1 + j] = mi * u[j] + (i == j ? pr : 0.0) - fv[i][j];
+            F[i][4] = (E + pr) * u[i] - fv[i][3];
+        }
+#pragma unroll
+        for (int kap = 0; kap < 3; ++kap)
+#pragma unroll
+            for (int c = 0; c < 5; ++c) {
+                double fh;
+                if (CART) fh = m.cM[kap] * F[kap][c];
+                else fh = Mp[kap][0] * F[0][c] + Mp[kap][1] * F[1][c] + Mp[kap][2] * F[2][c];
+                FH[(int64_t)(kap * 5 + c) * N + p] = fh;
+            }
+    }
+}
+
+constexpr int REGD = 14 * 8 * 8;                    // one kappa-extended region
+constexpr size_t SMEMD = sizeof(double) * 3 * 5 * REGD;
+
+template <bool VISC, bool CART>
+__global__ void __launch_bounds__(NT3, 2) k_div3d(DevMesh m, const double* __restrict__ Q,
+                                                 const double* __restrict__ FH,
+                                                 const double* __restrict__ FV, Gas g, Epilogue ep) {
+    constexpr int NC = 5;
+    extern __shared__ __align__(16) double fb[];     // [kappa][c][REGD]
+    __shared__ uint16_t sc[T3N];
+    const int n0 = m.n[0], n1 = m.n[1], n2 = m.n[2];
+    const int64_t N = m.npts;
+    const int64_t s1 = n0, s2 = (int64_t)n0 * n1;
+    const int i0 = blockIdx.x * T3X, j0 = blockIdx.y * T3Y, k0 = blockIdx.z * T3Z;
+    const int tid = threadIdx.x;
+    const int per0 = m.periodic[0], per1 = m.periodic[1], per2 = m.periodic[2];
+    // ---- the three extended regions of Fhat_kappa in one round trip
+    // y- and z-extended regions: x-runs of 8 doubles, 16-byte copies when rows are 16-byte
+    // aligned (even n0; tiles start at multiples of 8)
+    const bool pair = (n0 & 1) == 0 && i0 + 8 <= n0;
+#pragma unroll
+    for (int kap = 1; kap < 3; ++kap) {
+        if (!pair) break;
+        const int ey = kap == 1 ? 3 : 0, ez = kap == 2 ? 3 : 0;
+        const int RY = T3Y + 2 * ey;
+        for (int t = tid; t < REGD / 2; t += NT3) {
+            const int x2 = t & 3, y = (t >> 2) % RY, z = (t >> 2) / RY;
+            int gj = j0 - ey + y, gk = k0 - ez + z;
+            if (gj < 0) gj = per1 ? gj + n1 : 0; else if (gj >= n1) gj = per1 ? gj - n1 : n1 - 1;
+            if (gk < 0) gk = per2 ? gk + n2 : 0; else if (gk >= n2) gk = per2 ? gk - n2 : n2 - 1;
+            const int64_t q = i0 + 2 * x2 + s1 * gj + s2 * gk;
+            const int e = 2 * x2 + T3X * (y + RY * z);
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                const unsigned sa = (unsigned)__cvta_generic_to_shared(fb + (kap * NC + c) * REGD + e);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(FH + (int64_t)(kap * NC + c) * N + q));
+            }
+        }
+    }
+#pragma unroll
+    for (int kap = 0; kap < 3; ++kap) {
+        if (kap > 0 && pair) break;
+        const int ex = kap == 0 ? 3 : 0, ey = kap == 1 ? 3 : 0, ez = kap == 2 ? 3 : 0;
+        const int RX = T3X + 2 * ex, RY = T3Y + 2 * ey;
+        for (int t = tid; t < REGD; t += NT3) {
+            const int x = t % RX, y = (t / RX) % RY, z = t / (RX * RY);
+            int gi = i0 - ex + x, gj = j0 - ey + y, gk = k0 - ez + z;
+            if (gi < 0) gi = per0 ? gi + n0 : 0; else if (gi >= n0) gi = per0 ? gi - n0 : n0 - 1;
+            if (gj < 0) gj = per1 ? gj + n1 : 0; else if (gj >= n1) gj = per1 ? gj - n1 : n1 - 1;
+            if (gk < 0) gk = per2 ? gk + n2 : 0; else if (gk >= n2) gk = per2 ? gk - n2 : n2 - 1;
+            const int64_t q = gi + s1 * gj + s2 * gk;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                const unsigned sa = (unsigned)__cvta_generic_to_shared(fb + (kap * NC + c) * REGD + t);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(FH + (int64_t)(kap * NC + c) * N + q));
+            }
+        }
+    }
+    unsigned clsv[PPT3];
+#pragma unroll
+    for (int s = 0; s < PPT3; ++s) {
+        const int t = tid + s * NT3;
+        const int gi = i0 + (t & 7), gj = j0 + ((t >> 3) & 7), gk = k0 + (t >> 6);
+        const bool live = gi < n0 && gj < n1 && gk < n2;
+        clsv[s] = live ? m.cls[gi + s1 * gj + s2 * gk] : 0u;
+    }
+    // epilogue inputs requested while the regions land
+    double yb[PPT3][NC];
+#pragma unroll
+    for (int s = 0; s < PPT3; ++s)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) yb[s][c] = 0.0;
+    if (ep.y_out) {
+#pragma unroll
+        for (int s = 0; s < PPT3; ++s) {
+            const int t = tid + s * NT3;
+            const int gi = min(i0 + (t & 7), n0 - 1), gj = min(j0 + ((t >> 3) & 7), n1 - 1), gk = min(k0 + (t >> 6), n2 - 1);
+            const int64_t p = gi + s1 * gj + s2 * gk;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                double y = __ldg(ep.base + c * N + p);
+                for (int k = 0; k < ep.nsrc; ++k) y += ep.csrc[k] * __ldg(ep.src[k] + c * N + p);
+                yb[s][c] = y;
+            }
+        }
+    }
+#pragma unroll
+    for (int s = 0; s < PPT3; ++s) sc[tid + s * NT3] = (uint16_t)clsv[s];
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < PPT3; ++s) {
+        const int t = tid + s * NT3;
+        const int x = t & 7, y = (t >> 3) & 7, z = t >> 6;
+        const int gi = i0 + x, gj = j0 + y, gk = k0 + z;
+        if (gi >= n0 || gj >= n1 || gk >= n2) continue;
+        const int64_t p = gi + s1 * gj + s2 * gk;
+        const unsigned code = sc[t];
+        double Rs[NC] = {0, 0, 0, 0, 0};
+        if (code) {
+            double acc[NC] = {0, 0, 0, 0, 0};
+#pragma unroll
+            for (int kap = 0; kap < 3; ++kap) {
+                const int ex = kap == 0 ? 3 : 0, ey = kap == 1 ? 3 : 0, ez = kap == 2 ? 3 : 0;
+                const int RX = T3X + 2 * ex, RY = T3Y + 2 * ey;
+                const int rr = (x + ex) + RX * ((y + ey) + RY * (z + ez));
+                const int sk = kap == 0 ? 1 : (kap == 1 ? RX : RX * RY);
+                const double* f = fb + kap * NC * REGD;
+                const int cl = (code >> (4 * kap)) & 15;
+                if (cl == CLS_INT) {
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) {
+                        const double* fc = f + c * REGD;
+                        acc[c] += (2.0 / 3.0) * (fc[rr + sk] - fc[rr - sk]) - (1.0 / 12.0) * (fc[rr + 2 * sk] - fc[rr - 2 * sk]);
+                    }
+                } else {
+                    const int ns = c_nst[cl];
+                    double a2[NC] = {0, 0, 0, 0, 0};
+                    for (int tt = 0; tt < ns; ++tt) {
+                        const double cf = c_cf[cl][tt];
+                        const int o = rr + c_off[cl][tt] * sk;
+#pragma unroll
+                        for (int c = 0; c < NC; ++c) a2[c] += cf * f[c * REGD + o];
+                    }
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) acc[c] += a2[c];
+                }
+            }
+            const double Jp = CART ? m.cJ : __ldg(m.J + p);
+#pragma unroll
+            for (int c = 0; c < NC; ++c) Rs[c] = -Jp * acc[c];
+            bool sat = false;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const int cl = (code >> (4 * k)) & 15;
+                sat = sat || cl == CLS_L0 || cl == CLS_R0;
+            }
+            if (sat) {
+                const int idx[3] = {gi, gj, gk};
+                sat_point<3, VISC, CART>(m, Q, FV, g, p, idx, code, Jp, Rs);
+            }
+        }
+        if (ep.r_out) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) ep.r_out[c * N + p] = Rs[c];
+        }
+        if (ep.y_out) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) ep.y_out[c * N + p] = yb[s][c] + ep.c_new * Rs[c];
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
 // intermediate states on a box: out = base + sum_k c_k src_k (all components)
 // ------------------------------------------------------------------------------------
 struct CombineArgs {
@@ -1023,10 +1349,61 @@ void launch_visc(int dim, const DevMesh& m, const double* Q, double* FV, const B
 void launch_rhs2d(const DevMesh& m, const double* Q, const Gas& g, const Epilogue& ep,
                   const DonorSet& ds, cudaStream_t st);
 
+bool rhs3d_split() {
+    static int v = -1;
+    if (v < 0) {
+        // opt-in (MRAB_3D_SPLIT=1): parity-green, measured slower on config 4 (block RHS 1.51
+        // ms for both passes vs 1.20 ms for k_visc3d_x + k_rhs3d)
+        const char* e = getenv("MRAB_3D_SPLIT");
+        const char* d = getenv("MRAB_3D_DIRECT");
+        v = (e && e[0] == '1') && !(d && d[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+
+void launch_flux3d(const DevMesh& m, const double* Q, double* FH, double* FV, const Gas& gas,
+                   cudaStream_t st) {
+    static bool init = false;
+    if (!init) {
+        cudaFuncSetAttribute(k_flux3d<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEMX);
+        cudaFuncSetAttribute(k_flux3d<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEMX);
+        cudaFuncSetAttribute(k_flux3d<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEMX);
+        cudaFuncSetAttribute(k_flux3d<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEMX);
+        init = true;
+    }
+    dim3 grid((m.n[0] + T3X - 1) / T3X, (m.n[1] + T3Y - 1) / T3Y, (m.n[2] + T3Z - 1) / T3Z);
+    if (gas.viscous) {
+        if (m.cart) k_flux3d<true, true><<<grid, NT3, SMEMX, st>>>(m, Q, FH, FV, m.fvtile, gas);
+        else k_flux3d<true, false><<<grid, NT3, SMEMX, st>>>(m, Q, FH, FV, m.fvtile, gas);
+    } else {
+        if (m.cart) k_flux3d<false, true><<<grid, NT3, SMEMX, st>>>(m, Q, FH, FV, m.fvtile, gas);
+        else k_flux3d<false, false><<<grid, NT3, SMEMX, st>>>(m, Q, FH, FV, m.fvtile, gas);
+    }
+}
+
 void launch_rhs(int dim, const DevMesh& m, const double* Q, const double* FV, const Gas& gas,
                 const Epilogue& ep, const DonorSet& ds, cudaStream_t st) {
     if (dim == 2) {
         launch_rhs2d(m, Q, gas, ep, ds, st);
+        return;
+    }
+    if (m.fh && rhs3d_split()) {
+        static bool init = false;
+        if (!init) {
+            cudaFuncSetAttribute(k_div3d<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEMD);
+            cudaFuncSetAttribute(k_div3d<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEMD);
+            cudaFuncSetAttribute(k_div3d<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEMD);
+            cudaFuncSetAttribute(k_div3d<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEMD);
+            init = true;
+        }
+        dim3 grid((m.n[0] + T3X - 1) / T3X, (m.n[1] + T3Y - 1) / T3Y, (m.n[2] + T3Z - 1) / T3Z);
+        if (gas.viscous) {
+            if (m.cart) k_div3d<true, true><<<grid, NT3, SMEMD, st>>>(m, Q, m.fh, FV, gas, ep);
+            else k_div3d<true, false><<<grid, NT3, SMEMD, st>>>(m, Q, m.fh, FV, gas, ep);
+        } else {
+            if (m.cart) k_div3d<false, true><<<grid, NT3, SMEMD, st>>>(m, Q, m.fh, FV, gas, ep);
+            else k_div3d<false, false><<<grid, NT3, SMEMD, st>>>(m, Q, m.fh, FV, gas, ep);
+        }
         return;
     }
     static int direct = -1;

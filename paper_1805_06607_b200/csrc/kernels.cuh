@@ -30,6 +30,10 @@ struct DevMesh {
     // bit 31 set = interior tile (see rhs2d_interior_tile); NULL = decide in the kernel
     const int32_t* tlist;
     int ntl;
+    // 3-D two-pass RHS: contravariant fluxes [3][5][npts] (k_flux3d -> k_div3d) and the per
+    // 8^3-tile flag "write the Cartesian viscous fluxes here" (SAT points / donor stencils)
+    const double* fh;
+    const uint8_t* fvtile;
     // 2-D viscous, large meshes: per-point SAT viscous-flux scratch [6][npts] of the
     // row-marching kernel (kernels2d_march.cu); NULL = tile kernel
     double* satv;
@@ -146,6 +150,11 @@ void launch_donor2d(const RecvTask& rt, const SrcSets& ss, const MeshTable& mt, 
 
 void launch_visc(int dim, const DevMesh& m, const double* Q, double* FV, const Box& box,
                  const Gas& gas, cudaStream_t st);
+// 3-D two-pass RHS (opt-in): whether it is on, and its flux pass (writes m.fh, and F^V in the
+// flagged tiles); launch_rhs then runs the divergence pass
+bool rhs3d_split();
+void launch_flux3d(const DevMesh& m, const double* Q, double* FH, double* FV, const Gas& gas,
+                   cudaStream_t st);
 // 3-D: direct kernel reading FV and the gathered qhat/fvhat; 2-D: tiled kernel that forms
 // its own viscous fluxes and gathers donor data inline at its receivers from `ds`.
 void launch_rhs(int dim, const DevMesh& m, const double* Q, const double* FV, const Gas& gas,

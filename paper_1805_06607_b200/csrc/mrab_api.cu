@@ -47,6 +47,8 @@ struct MeshDev {
     double* Q[2] = {nullptr, nullptr};
     double* ring[kMaxHist] = {nullptr};
     double* FV = nullptr;
+    double* FH = nullptr;         // 3-D: contravariant fluxes [3][5][N] (two-pass RHS)
+    uint8_t* fvtile = nullptr;    // 3-D: per 8^3 tile, write F^V there (SAT points, donor stencils)
     double* dstate = nullptr;
     double* kbuf[4] = {nullptr, nullptr, nullptr, nullptr};
     double* ystage = nullptr;
@@ -145,6 +147,15 @@ static size_t plan_bytes(const Plan& P, bool dry, mrab_ctx* ctx, Bump* bump, boo
         {
             void* p = take((size_t)d * (d + 1) * N * sizeof(double));
             if (D) D->FV = (double*)p;
+        }
+        if (d == 3) {
+            const size_t nt = (size_t)((m.n[0] + 7) / 8) * ((m.n[1] + 7) / 8) * ((m.n[2] + 7) / 8);
+            void* a = take((size_t)15 * N * sizeof(double));
+            void* b = take(nt);
+            if (D) {
+                D->FH = (double*)a;
+                D->fvtile = (uint8_t*)b;
+            }
         }
         {
             void* p = take(S);
@@ -342,7 +353,12 @@ static void issue_visc(mrab_ctx* c, int g, const double* Q, const Box& box) {
 static void issue_step_visc(mrab_ctx* c, int g, const double* Q) {
     const Plan& P = *c->P;
     const MeshPlan& mp = P.meshes[g];
-    if (P.dim == 3)
+    if (P.dim == 3 && rhs3d_split()) {
+        // two-pass 3-D RHS: the flux pass (contravariant fluxes everywhere, F^V where read)
+        MeshDev& D = c->md[g];
+        launch_flux3d(D.dm, Q, D.FH, D.FV, c->gas, c->st);
+        c->launch_counter++;
+    } else if (P.dim == 3)
         issue_visc(c, g, Q, whole_box(mp));
     else if (mp.is_donor)
         issue_visc(c, g, Q, make_box(mp.fv_lo, mp.fv_hi));
@@ -935,6 +951,38 @@ mrab_status mrab_create(const mrab_plan* plan, const double* const* q0, void* d_
             CK(cudaMemcpy(D.M, m.M.data(), (size_t)d * d * N * sizeof(double), cudaMemcpyHostToDevice));
         }
         CK(cudaMemcpy(D.cls, m.cls.data(), N * sizeof(uint16_t), cudaMemcpyHostToDevice));
+        if (d == 3) {
+            // F^V is read at SAT points (the viscous penalty) and at donor stencils (gathers)
+            const int tx = (m.n[0] + 7) / 8, ty = (m.n[1] + 7) / 8, tz = (m.n[2] + 7) / 8;
+            std::vector<uint8_t> fl((size_t)tx * ty * tz, 0);
+            for (int k = 0; k < m.n[2]; ++k)
+                for (int jj = 0; jj < m.n[1]; ++jj)
+                    for (int i = 0; i < m.n[0]; ++i) {
+                        const unsigned cc = m.cls[m.idx(i, jj, k)];
+                        bool need = false;
+                        for (int a = 0; a < 3; ++a) {
+                            const int cl = (cc >> (4 * a)) & 15;
+                            need = need || cl == CLS_L0 || cl == CLS_R0;
+                        }
+                        if (need) fl[(size_t)(i / 8) + tx * ((size_t)(jj / 8) + (size_t)ty * (k / 8))] = 1;
+                    }
+            // the exact donor stencils (4^3 points) of every receiver this mesh donates to
+            for (size_t h = 0; h < P.meshes.size(); ++h) {
+                const MeshPlan& mh = P.meshes[h];
+                for (size_t r = 0; r < mh.rdonor.size(); ++r) {
+                    if (mh.rdonor[r] != g) continue;
+                    for (int a2 = 0; a2 < 4; ++a2)
+                        for (int a1 = 0; a1 < 4; ++a1)
+                            for (int a0 = 0; a0 < 4; ++a0) {
+                                const int i = (mh.rbase[3 * r] + a0) % m.n[0];
+                                const int jj = (mh.rbase[3 * r + 1] + a1) % m.n[1];
+                                const int k = (mh.rbase[3 * r + 2] + a2) % m.n[2];
+                                fl[(size_t)(i / 8) + tx * ((size_t)(jj / 8) + (size_t)ty * (k / 8))] = 1;
+                            }
+                }
+            }
+            CK(cudaMemcpy(D.fvtile, fl.data(), fl.size(), cudaMemcpyHostToDevice));
+        }
         CK(cudaMemcpy(D.recv_slot, m.recv_slot.data(), N * sizeof(int32_t), cudaMemcpyHostToDevice));
         if (R) {
             CK(cudaMemcpy(D.rpoint, m.rpoint.data(), R * sizeof(int64_t), cudaMemcpyHostToDevice));
@@ -962,6 +1010,8 @@ mrab_status mrab_create(const mrab_plan* plan, const double* const* q0, void* d_
         dm.rdonor = D.rdonor;
         dm.rbase = D.rbase;
         dm.rw = D.rw;
+        dm.fh = D.FH;
+        dm.fvtile = D.fvtile;
         if (d == 2) {
             // tile lists: tiles meeting the donor state box first (critical), then the rest
             int tx, ty;
@@ -1214,6 +1264,8 @@ mrab_status mrab_time_kernel(mrab_ctx* c, int kernel, int mesh, int reps, int fl
                 rhs2d_tile_shape(&tx, &ty);
                 Nk = (double)ep.ntiles * tx * ty;
             }
+            if (d == 3 && rhs3d_split() && kernel == 0)
+                launch_flux3d(D.dm, Q, D.FH, D.FV, c->gas, c->st);   // the RHS is both passes
             launch_rhs(d, D.dm, Q, D.FV, c->gas, ep, make_ds(c, state_of.data()), c->st);
             // Q read, R written, (m-1) ring reads, state written, metrics if curvilinear
             bytes = 8.0 * Nk * (nc * (m + 2) + (mp.cartesian ? 0 : 1 + d * d));
