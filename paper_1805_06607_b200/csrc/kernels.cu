@@ -502,7 +502,18 @@ __global__ void __launch_bounds__(NT3, 2) k_rhs3d(DevMesh m, const double* __res
         const int64_t p = gi + s1 * gj + s2 * gk;
         const unsigned code = sc[t];
         double yb[NC];
-        if (ep.y_out) {
+        if (ep.y_out && ep.nsrc == 2) {
+            // AB3 steps: base + two history terms, all loads issued together
+            double v[3][NC];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                v[0][c] = __ldg(ep.base + c * N + p);
+                v[1][c] = __ldg(ep.src[0] + c * N + p);
+                v[2][c] = __ldg(ep.src[1] + c * N + p);
+            }
+#pragma unroll
+            for (int c = 0; c < NC; ++c) yb[c] = v[0][c] + ep.csrc[0] * v[1][c] + ep.csrc[1] * v[2][c];
+        } else if (ep.y_out) {
             // all history loads issued together (unused slots re-read `base` with weight 0)
             const double* sp[4];
             double cw[4];
