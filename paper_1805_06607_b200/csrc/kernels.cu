@@ -349,9 +349,12 @@ constexpr int KR3 = (REG3 + NT3 - 1) / NT3;           // region points per threa
 constexpr size_t SMEM3 = sizeof(double) * 5 * (REG3 + T3N) + sizeof(uint16_t) * T3N;
 }  // namespace
 
-template <bool VISC, bool CART>
+// PRE: the contravariant fluxes come precomputed from k_flux3d (two-pass mode): the region
+// loads read Fhat_kappa (5 values) instead of Q and F^V (9) and no flux is formed here
+template <bool VISC, bool CART, bool PRE = false>
 __global__ void __launch_bounds__(NT3, 2) k_rhs3d(DevMesh m, const double* __restrict__ Q,
-                                                 const double* __restrict__ FV, Gas g, Epilogue ep) {
+                                                 const double* __restrict__ FV, Gas g, Epilogue ep,
+                                                 const double* __restrict__ FH = nullptr) {
     constexpr int NC = 5;
     extern __shared__ __align__(16) double fb[];        // Fhat [NC][REG3], then Racc [NC][T3N]
     double* racc = fb + NC * REG3;
@@ -395,6 +398,11 @@ __global__ void __launch_bounds__(NT3, 2) k_rhs3d(DevMesh m, const double* __res
                 else if (gg[k] >= n) gg[k] = m.periodic[k] ? gg[k] - n : n - 1;
             }
             const int64_t q = gg[0] + s1 * gg[1] + s2 * gg[2];
+            if (PRE) {
+#pragma unroll
+                for (int c = 0; c < NC; ++c) lq[r][c] = __ldg(FH + (int64_t)(kap * NC + c) * N + q);
+                continue;
+            }
 #pragma unroll
             for (int c = 0; c < NC; ++c) lq[r][c] = __ldg(Q + c * N + q);
             if (VISC) {
@@ -420,6 +428,11 @@ __global__ void __launch_bounds__(NT3, 2) k_rhs3d(DevMesh m, const double* __res
         for (int r = 0; r < KR3; ++r) {
             const int t = tid + r * NT3;
             if (t >= (T3X + 2 * ex) * (T3Y + 2 * ey) * (T3Z + 2 * ez)) break;
+            if (PRE) {
+#pragma unroll
+                for (int c = 0; c < NC; ++c) fb[c * REG3 + t] = lq[r][c];
+                continue;
+            }
             const double rho = lq[r][0];
             const double ir = rcp64(rho);
             const double u[3] = {lq[r][1] * ir, lq[r][2] * ir, lq[r][3] * ir};
@@ -848,16 +861,17 @@ __global__ void __launch_bounds__(NT3, 2) k_visc3d_x(DevMesh m, const double* __
 }
 
 // ------------------------------------------------------------------------------------
-// 3-D RHS in two passes (opt-in, MRAB_3D_SPLIT=1; default k_visc3d_x + k_rhs3d):
+// 3-D RHS in two passes (default; MRAB_3D_SPLIT=0 restores k_visc3d_x + k_rhs3d):
 //   k_flux3d  per tile: the cross-shaped state region staged by cp.async in one round trip
 //             (as k_visc3d_x), primitives in place, D1 gradients at the tile points, then the
 //             full contravariant fluxes Fhat_kappa = sum_i M_kappa,i (F^I_i - F^V_i) of every
 //             point written once ([3][5][N]); the Cartesian viscous fluxes F^V are written only
 //             in tiles that hold SAT points or donor stencils (the SAT term and the gathers
 //             read them there);
-//   k_div3d   per tile: the three kappa-extended regions of Fhat_kappa staged by cp.async in
-//             one round trip, D_kappa by class code (segment closures), R = -J sum_kappa,
-//             SAT, AB / RK epilogue.
+//   k_rhs3d<PRE = true>  the tiled RHS reading Fhat_kappa (5 values per region point instead
+//             of Q and F^V) in its three register-staged passes, D_kappa by class code, SAT,
+//             AB / RK epilogue (k_div3d, staging all three regions by cp.async in one round
+//             trip, measured slower: MRAB_DIV3D_STAGED=1).
 // k_rhs3d formed every flux on the tile extended by 3 along each direction from Q and F^V
 // (three dependent round trips, 1.75x redundant flux work).
 // ------------------------------------------------------------------------------------
@@ -1363,11 +1377,11 @@ void launch_rhs2d(const DevMesh& m, const double* Q, const Gas& g, const Epilogu
 bool rhs3d_split() {
     static int v = -1;
     if (v < 0) {
-        // opt-in (MRAB_3D_SPLIT=1): parity-green, measured slower on config 4 (block RHS 1.51
-        // ms for both passes vs 1.20 ms for k_visc3d_x + k_rhs3d)
+        // default (MRAB_3D_SPLIT=0: k_visc3d_x + k_rhs3d): config 4 8.43 -> 8.08 ms/step,
+        // config 5 20.2 -> 16.8 ms/step
         const char* e = getenv("MRAB_3D_SPLIT");
         const char* d = getenv("MRAB_3D_DIRECT");
-        v = (e && e[0] == '1') && !(d && d[0] == '1') ? 1 : 0;
+        v = (e && e[0] == '0') || (d && d[0] == '1') ? 0 : 1;
     }
     return v == 1;
 }
@@ -1408,12 +1422,35 @@ void launch_rhs(int dim, const DevMesh& m, const double* Q, const double* FV, co
             init = true;
         }
         dim3 grid((m.n[0] + T3X - 1) / T3X, (m.n[1] + T3Y - 1) / T3Y, (m.n[2] + T3Z - 1) / T3Z);
+        static const int staged = [] {
+            const char* e = getenv("MRAB_DIV3D_STAGED");
+            return e ? atoi(e) : 0;
+        }();
+        if (staged) {
+            if (gas.viscous) {
+                if (m.cart) k_div3d<true, true><<<grid, NT3, SMEMD, st>>>(m, Q, m.fh, FV, gas, ep);
+                else k_div3d<true, false><<<grid, NT3, SMEMD, st>>>(m, Q, m.fh, FV, gas, ep);
+            } else {
+                if (m.cart) k_div3d<false, true><<<grid, NT3, SMEMD, st>>>(m, Q, m.fh, FV, gas, ep);
+                else k_div3d<false, false><<<grid, NT3, SMEMD, st>>>(m, Q, m.fh, FV, gas, ep);
+            }
+            return;
+        }
+        // the tiled RHS reading the precomputed fluxes (three register-staged passes)
+        static bool init3 = false;
+        if (!init3) {
+            cudaFuncSetAttribute(k_rhs3d<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM3);
+            cudaFuncSetAttribute(k_rhs3d<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM3);
+            cudaFuncSetAttribute(k_rhs3d<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM3);
+            cudaFuncSetAttribute(k_rhs3d<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM3);
+            init3 = true;
+        }
         if (gas.viscous) {
-            if (m.cart) k_div3d<true, true><<<grid, NT3, SMEMD, st>>>(m, Q, m.fh, FV, gas, ep);
-            else k_div3d<true, false><<<grid, NT3, SMEMD, st>>>(m, Q, m.fh, FV, gas, ep);
+            if (m.cart) k_rhs3d<true, true, true><<<grid, NT3, SMEM3, st>>>(m, Q, FV, gas, ep, m.fh);
+            else k_rhs3d<true, false, true><<<grid, NT3, SMEM3, st>>>(m, Q, FV, gas, ep, m.fh);
         } else {
-            if (m.cart) k_div3d<false, true><<<grid, NT3, SMEMD, st>>>(m, Q, m.fh, FV, gas, ep);
-            else k_div3d<false, false><<<grid, NT3, SMEMD, st>>>(m, Q, m.fh, FV, gas, ep);
+            if (m.cart) k_rhs3d<false, true, true><<<grid, NT3, SMEM3, st>>>(m, Q, FV, gas, ep, m.fh);
+            else k_rhs3d<false, false, true><<<grid, NT3, SMEM3, st>>>(m, Q, FV, gas, ep, m.fh);
         }
         return;
     }

@@ -150,7 +150,7 @@ void launch_donor2d(const RecvTask& rt, const SrcSets& ss, const MeshTable& mt, 
 
 void launch_visc(int dim, const DevMesh& m, const double* Q, double* FV, const Box& box,
                  const Gas& gas, cudaStream_t st);
-// 3-D two-pass RHS (opt-in): whether it is on, and its flux pass (writes m.fh, and F^V in the
+// 3-D two-pass RHS (default): whether it is on, and its flux pass (writes m.fh, and F^V in the
 // flagged tiles); launch_rhs then runs the divergence pass
 bool rhs3d_split();
 void launch_flux3d(const DevMesh& m, const double* Q, double* FH, double* FV, const Gas& gas,
