@@ -276,7 +276,8 @@ def run_gpu(args):
         traffic = None
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic,
-            "kernel": f"k_rhs (fused RHS+SAT+AB) on mesh {gdom} ({p.meshes[gdom].name})",
+            "kernel": (f"k_rhs2d (fused RHS+SAT+AB) on mesh {gdom} ({p.meshes[gdom].name})" if p.dim == 2 else
+                       f"k_flux3d + k_rhs3d (RHS in two passes, SAT, AB) on mesh {gdom} ({p.meshes[gdom].name})"),
             "algorithmic_bytes_per_launch": by, "ms_per_launch": ms, "peak_source": peak_src,
             "kernel_ms_per_step_cold": kernel_times, "other_meshes": others}
 
