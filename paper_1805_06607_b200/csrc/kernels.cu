@@ -378,14 +378,12 @@ __global__ void __launch_bounds__(NT3, 2) k_rhs3d(DevMesh m, const double* __res
 #pragma unroll
         for (int c = 0; c < NC; ++c) racc[c * T3N + t] = 0.0;
     }
-    // direction loop unrolled: region extents are compile-time, so the index arithmetic is
-    // constant division (it was runtime integer division, a quarter of all instructions)
-#pragma unroll
-    for (int kap = 0; kap < 3; ++kap) {
-        const int ex = kap == 0 ? 3 : 0, ey = kap == 1 ? 3 : 0, ez = kap == 2 ? 3 : 0;
+    // PRE: the next direction's region loads are issued before the current direction's
+    // stencil, so the three passes' memory round trips overlap the arithmetic
+    double lqp[2][KR3][NC];
+    auto pre_load = [&](int kk, double (&dst)[KR3][NC]) {
+        const int ex = kk == 0 ? 3 : 0, ey = kk == 1 ? 3 : 0, ez = kk == 2 ? 3 : 0;
         const int RX = T3X + 2 * ex, RY = T3Y + 2 * ey;
-        // ---- loads of all region points of this thread (independent, in flight together)
-        double lq[KR3][NC], lv[KR3][4], lm[KR3][3];
 #pragma unroll
         for (int r = 0; r < KR3; ++r) {
             const int t = tid + r * NT3;
@@ -398,11 +396,32 @@ __global__ void __launch_bounds__(NT3, 2) k_rhs3d(DevMesh m, const double* __res
                 else if (gg[k] >= n) gg[k] = m.periodic[k] ? gg[k] - n : n - 1;
             }
             const int64_t q = gg[0] + s1 * gg[1] + s2 * gg[2];
-            if (PRE) {
 #pragma unroll
-                for (int c = 0; c < NC; ++c) lq[r][c] = __ldg(FH + (int64_t)(kap * NC + c) * N + q);
-                continue;
+            for (int c = 0; c < NC; ++c) dst[r][c] = __ldg(FH + (int64_t)(kk * NC + c) * N + q);
+        }
+    };
+    if (PRE) pre_load(0, lqp[0]);
+    // direction loop unrolled: region extents are compile-time, so the index arithmetic is
+    // constant division (it was runtime integer division, a quarter of all instructions)
+#pragma unroll
+    for (int kap = 0; kap < 3; ++kap) {
+        const int ex = kap == 0 ? 3 : 0, ey = kap == 1 ? 3 : 0, ez = kap == 2 ? 3 : 0;
+        const int RX = T3X + 2 * ex, RY = T3Y + 2 * ey;
+        // ---- loads of all region points of this thread (independent, in flight together)
+        double lq[KR3][NC], lv[KR3][4], lm[KR3][3];
+#pragma unroll
+        for (int r = 0; r < KR3; ++r) {
+            if (PRE) break;
+            const int t = tid + r * NT3;
+            const int x = t % RX, y = (t / RX) % RY, z = t / (RX * RY);
+            int gg[3] = {i0 - ex + x, j0 - ey + y, k0 - ez + z};
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const int n = m.n[k];
+                if (gg[k] < 0) gg[k] = m.periodic[k] ? gg[k] + n : 0;
+                else if (gg[k] >= n) gg[k] = m.periodic[k] ? gg[k] - n : n - 1;
             }
+            const int64_t q = gg[0] + s1 * gg[1] + s2 * gg[2];
 #pragma unroll
             for (int c = 0; c < NC; ++c) lq[r][c] = __ldg(Q + c * N + q);
             if (VISC) {
@@ -430,7 +449,7 @@ __global__ void __launch_bounds__(NT3, 2) k_rhs3d(DevMesh m, const double* __res
             if (t >= (T3X + 2 * ex) * (T3Y + 2 * ey) * (T3Z + 2 * ez)) break;
             if (PRE) {
 #pragma unroll
-                for (int c = 0; c < NC; ++c) fb[c * REG3 + t] = lq[r][c];
+                for (int c = 0; c < NC; ++c) fb[c * REG3 + t] = lqp[kap & 1][r][c];
                 continue;
             }
             const double rho = lq[r][0];
@@ -476,6 +495,7 @@ __global__ void __launch_bounds__(NT3, 2) k_rhs3d(DevMesh m, const double* __res
 #pragma unroll
             for (int s = 0; s < PPT3; ++s) sc[tid + s * NT3] = (uint16_t)clsv[s];
         __syncthreads();
+        if (PRE && kap < 2) pre_load(kap + 1, lqp[(kap + 1) & 1]);
         // ---- D_kappa of the staged fluxes at the tile points
         const int sk = kap == 0 ? 1 : (kap == 1 ? RX : RX * RY);
         for (int t = tid; t < T3N; t += NT3) {
