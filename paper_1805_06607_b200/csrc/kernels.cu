@@ -349,6 +349,23 @@ constexpr int KR3 = (REG3 + NT3 - 1) / NT3;           // region points per threa
 constexpr size_t SMEM3 = sizeof(double) * 5 * (REG3 + T3N) + sizeof(uint16_t) * T3N;
 }  // namespace
 
+// 3-D tile order: CTAs walk 4 x 4 x 4 blocks of 8^3 tiles (a 1-D grid), so that tiles sharing
+// halo regions run close together in time and their halo reads hit L2 (a plain x-fastest
+// grid re-read most z-halo planes from DRAM).  Returns false for padding CTAs.
+__device__ __forceinline__ bool tile3_blocked(const DevMesh& m, int& bx, int& by, int& bz) {
+    const int tx = (m.n[0] + T3X - 1) / T3X, ty = (m.n[1] + T3Y - 1) / T3Y, tz = (m.n[2] + T3Z - 1) / T3Z;
+    const int sx = (tx + 3) / 4, sy = (ty + 3) / 4;
+    const int b = blockIdx.x, loc = b & 63, sup = b >> 6;
+    bx = (sup % sx) * 4 + (loc & 3);
+    by = ((sup / sx) % sy) * 4 + ((loc >> 2) & 3);
+    bz = (sup / (sx * sy)) * 4 + (loc >> 4);
+    return bx < tx && by < ty && bz < tz;
+}
+static inline unsigned tile3_blocks(const int* n) {
+    const int tx = (n[0] + T3X - 1) / T3X, ty = (n[1] + T3Y - 1) / T3Y, tz = (n[2] + T3Z - 1) / T3Z;
+    return (unsigned)(((tx + 3) / 4) * ((ty + 3) / 4) * ((tz + 3) / 4) * 64);
+}
+
 // PRE: the contravariant fluxes come precomputed from k_flux3d (two-pass mode): the region
 // loads read Fhat_kappa (5 values) instead of Q and F^V (9) and no flux is formed here
 template <bool VISC, bool CART, bool PRE = false>
@@ -362,7 +379,9 @@ __global__ void __launch_bounds__(NT3, 2) k_rhs3d(DevMesh m, const double* __res
     const int n0 = m.n[0], n1 = m.n[1], n2 = m.n[2];
     const int64_t N = m.npts;
     const int64_t s1 = n0, s2 = (int64_t)n0 * n1;
-    const int i0 = blockIdx.x * T3X, j0 = blockIdx.y * T3Y, k0 = blockIdx.z * T3Z;
+    int tbx, tby, tbz;
+    if (!tile3_blocked(m, tbx, tby, tbz)) return;
+    const int i0 = tbx * T3X, j0 = tby * T3Y, k0 = tbz * T3Z;
     const int tid = threadIdx.x;
 
     // class codes requested now, stored to shared memory only after the first region loads
@@ -904,10 +923,13 @@ __global__ void __launch_bounds__(NT3, 2) k_flux3d(DevMesh m, const double* __re
     const int n0 = m.n[0], n1 = m.n[1], n2 = m.n[2];
     const int64_t N = m.npts;
     const int64_t s1 = n0, s2 = (int64_t)n0 * n1;
-    const int i0 = blockIdx.x * T3X, j0 = blockIdx.y * T3Y, k0 = blockIdx.z * T3Z;
+    int tbx, tby, tbz;
+    if (!tile3_blocked(m, tbx, tby, tbz)) return;
+    const int i0 = tbx * T3X, j0 = tby * T3Y, k0 = tbz * T3Z;
     const int tid = threadIdx.x;
     const int per0 = m.periodic[0], per1 = m.periodic[1], per2 = m.periodic[2];
-    const bool wfv = VISC && fvtile[blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)];
+    const int ntx = (n0 + T3X - 1) / T3X, nty = (n1 + T3Y - 1) / T3Y;
+    const bool wfv = VISC && fvtile[tbx + ntx * (tby + nty * tbz)];
     const int nreg = VISC ? XREG : T3N;   // Euler: no gradients, the tile itself suffices
     for (int t = tid; t < nreg; t += NT3) {
         int x, y, z;
@@ -1416,7 +1438,7 @@ void launch_flux3d(const DevMesh& m, const double* Q, double* FH, double* FV, co
         cudaFuncSetAttribute(k_flux3d<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEMX);
         init = true;
     }
-    dim3 grid((m.n[0] + T3X - 1) / T3X, (m.n[1] + T3Y - 1) / T3Y, (m.n[2] + T3Z - 1) / T3Z);
+    const dim3 grid(tile3_blocks(m.n));
     if (gas.viscous) {
         if (m.cart) k_flux3d<true, true><<<grid, NT3, SMEMX, st>>>(m, Q, FH, FV, m.fvtile, gas);
         else k_flux3d<true, false><<<grid, NT3, SMEMX, st>>>(m, Q, FH, FV, m.fvtile, gas);
@@ -1457,6 +1479,7 @@ void launch_rhs(int dim, const DevMesh& m, const double* Q, const double* FV, co
             return;
         }
         // the tiled RHS reading the precomputed fluxes (three register-staged passes)
+        const dim3 grid1(tile3_blocks(m.n));
         static bool init3 = false;
         if (!init3) {
             cudaFuncSetAttribute(k_rhs3d<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM3);
@@ -1466,11 +1489,11 @@ void launch_rhs(int dim, const DevMesh& m, const double* Q, const double* FV, co
             init3 = true;
         }
         if (gas.viscous) {
-            if (m.cart) k_rhs3d<true, true, true><<<grid, NT3, SMEM3, st>>>(m, Q, FV, gas, ep, m.fh);
-            else k_rhs3d<true, false, true><<<grid, NT3, SMEM3, st>>>(m, Q, FV, gas, ep, m.fh);
+            if (m.cart) k_rhs3d<true, true, true><<<grid1, NT3, SMEM3, st>>>(m, Q, FV, gas, ep, m.fh);
+            else k_rhs3d<true, false, true><<<grid1, NT3, SMEM3, st>>>(m, Q, FV, gas, ep, m.fh);
         } else {
-            if (m.cart) k_rhs3d<false, true, true><<<grid, NT3, SMEM3, st>>>(m, Q, FV, gas, ep, m.fh);
-            else k_rhs3d<false, false, true><<<grid, NT3, SMEM3, st>>>(m, Q, FV, gas, ep, m.fh);
+            if (m.cart) k_rhs3d<false, true, true><<<grid1, NT3, SMEM3, st>>>(m, Q, FV, gas, ep, m.fh);
+            else k_rhs3d<false, false, true><<<grid1, NT3, SMEM3, st>>>(m, Q, FV, gas, ep, m.fh);
         }
         return;
     }
@@ -1482,7 +1505,7 @@ void launch_rhs(int dim, const DevMesh& m, const double* Q, const double* FV, co
     if (!direct) {
         const size_t bytes = SMEM3;
         static bool init[4] = {false, false, false, false};
-        dim3 grid((m.n[0] + T3X - 1) / T3X, (m.n[1] + T3Y - 1) / T3Y, (m.n[2] + T3Z - 1) / T3Z);
+        const dim3 grid(tile3_blocks(m.n));
 #define MRAB_RHS3(V, C, I)                                                                          \
     do {                                                                                            \
         if (!init[I]) {                                                                             \
