@@ -1,0 +1,59 @@
+"""GPU parity of the non-default kernel paths (selected by environment variables that are read
+once per process, so each case runs in a subprocess): the 3-D single-pass RHS (k_visc3d_x +
+k_rhs3d), the 3-D staged divergence kernel, the 2-D general tile path for every tile (no lean
+path), and the serial (non-overlapped) 2-D schedule.  Each must match the oracle like the
+default path (states after N macro steps to 1e-10, RHS to 1e-10)."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import synth
+from oracle import rhs as orhs, timeint
+from paper_1805_06607_b200 import mrab
+cid = {cid}
+p = synth.make_config(cid, "test")
+plan = mrab.Plan(p)
+ctx = mrab.Context(plan, p.q0)
+st = orhs.build(p)
+Rg = ctx.rhs(p.q0)
+Ro = orhs.rhs(p, st, p.q0)
+rel = max(np.max(np.abs(a - b)) for a, b in zip(Rg, Ro)) / max(np.max(np.abs(b)) for b in Ro)
+assert rel <= 1e-10, ("rhs", rel)
+ctx.step(p.history_m - 1 + p.n_macro)
+gpu = [ctx.get_state(g)[0] for g in range(len(p.meshes))]
+orc = timeint.MRAB(p, setup=st)
+orc.run(p.n_macro)
+rel2 = max(np.max(np.abs(a - b)) for a, b in zip(gpu, orc.base)) / max(np.max(np.abs(b)) for b in orc.base)
+assert rel2 <= 1e-10, ("state", rel2)
+print("ok", rel, rel2)
+"""
+
+CASES = [
+    (4, {"MRAB_3D_SPLIT": "0"}),
+    (5, {"MRAB_3D_SPLIT": "0"}),
+    (4, {"MRAB_DIV3D_STAGED": "1"}),
+    (3, {"MRAB_LEAN": "0"}),
+    (3, {"MRAB_TILE_FLAGS": "0"}),
+    (2, {"MRAB_OVERLAP": "0", "MRAB_CURV_HALF": "0"}),
+]
+
+
+@pytest.mark.parametrize("cid,env", CASES, ids=[f"cfg{c}-" + "-".join(f"{k}={v}" for k, v in e.items()) for c, e in CASES])
+def test_alternative_path_parity(cid, env):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    e = dict(os.environ)
+    e.update(env)
+    r = subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT, cid=cid)], env=e,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "ok" in r.stdout, (r.stdout[-2000:], r.stderr[-4000:])
