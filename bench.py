@@ -266,12 +266,14 @@ def run_gpu(args):
             tot += mk * evals_per_step[g]
         kernel_times[name] = tot
     traffic = None
+    fp64_pct = None
     try:
         tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
         ent = tj.get(f"config{args.config}/mesh{gdom}/k_rhs2d" if p.dim == 2
                      else f"config{args.config}/mesh{gdom}/k_rhs3d")
         if ent:
             traffic = ent["total"]
+            fp64_pct = ent.get("fp64_pipe_pct")
     except Exception:
         traffic = None
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -279,7 +281,8 @@ def run_gpu(args):
             "kernel": (f"k_rhs2d (fused RHS+SAT+AB) on mesh {gdom} ({p.meshes[gdom].name})" if p.dim == 2 else
                        f"k_flux3d + k_rhs3d (RHS in two passes, SAT, AB) on mesh {gdom} ({p.meshes[gdom].name})"),
             "algorithmic_bytes_per_launch": by, "ms_per_launch": ms, "peak_source": peak_src,
-            "kernel_ms_per_step_cold": kernel_times, "other_meshes": others}
+            "kernel_ms_per_step_cold": kernel_times, "other_meshes": others,
+            "fp64_pipe_pct_ncu": fp64_pct, "fp64_peak_tflops_measured": 33.7}
 
     # ---- end to end through the C ABI with host buffers --------------------------------
     host = [torch.empty(q.shape, dtype=torch.float64).pin_memory() for q in p.q0]
