@@ -81,7 +81,10 @@ void rhs2d_tile_shape(int* tx, int* ty);
 // tile is full, its primitive halo (H = 6 viscous / 3 Euler) lies inside the mesh (or wraps
 // across a periodic seam), and every flux point (tile + 3) is interior in both directions
 bool rhs2d_interior_tile(const int* n, const int* periodic, const uint16_t* cls, int viscous,
-                         int bx, int by);
+                         int bx, int by, int cart);
+// per-mesh tile shape (32 x 8 for small curvilinear meshes, else 32 x 16)
+void rhs2d_tile_shape_for(const int* n, int cart, int* tx, int* ty);
+int rhs2d_variant_for(const int* n, int cart);
 // host: whether a 2-D mesh takes the row-marching RHS kernel (kernels2d_march.cu)
 bool rhs2d_march_wanted(const int* n, int viscous);
 

@@ -1238,16 +1238,35 @@ static int k2d_variant() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("MRAB_K2D");
-        v = e ? atoi(e) : 0;
-        if (v < 0 || v > 4) v = 0;
+        v = e ? atoi(e) : -2;   // -2: per mesh (rhs2d_variant_for)
+        if (v < -2 || v > 4 || v == -1) v = -2;
     }
     return v;
 }
 
+// per-mesh tile shape: small curvilinear meshes (the config-3 O-grid, 65k points: one wave of
+// latency-bound tiles) take 32 x 8 tiles (twice as many CTAs, shorter per-CTA chains); the
+// rest 32 x 16.  MRAB_K2D=v forces variant v everywhere; MRAB_SMALL_PTS sets the threshold.
+int rhs2d_variant_for(const int* n, int cart) {
+    const int v = k2d_variant();
+    if (v >= 0) return v;
+    static const long small = [] {
+        const char* e = getenv("MRAB_SMALL_PTS");
+        return e ? atol(e) : 100000L;
+    }();
+    return (!cart && (long)n[0] * n[1] <= small) ? 1 : 0;
+}
+
+void rhs2d_tile_shape_for(const int* n, int cart, int* tx, int* ty) {
+    *tx = TX;
+    const int v = rhs2d_variant_for(n, cart);
+    *ty = (v == 0 || v == 3) ? 16 : (v == 4 ? 32 : 8);
+}
+
 bool rhs2d_interior_tile(const int* n, const int* periodic, const uint16_t* cls, int viscous,
-                         int bx, int by) {
+                         int bx, int by, int cart) {
     int tx, ty;
-    rhs2d_tile_shape(&tx, &ty);
+    rhs2d_tile_shape_for(n, cart, &tx, &ty);
     const int H = viscous ? Geo<true, 16>::H : Geo<false, 16>::H;
     const int i0 = bx * tx, j0 = by * ty;
     if (i0 + tx > n[0] || j0 + ty > n[1]) return false;
@@ -1266,14 +1285,14 @@ bool rhs2d_interior_tile(const int* n, const int* periodic, const uint16_t* cls,
 
 void rhs2d_tile_shape(int* tx, int* ty) {
     *tx = TX;
-    const int v = k2d_variant();
+    const int v = k2d_variant() < 0 ? 0 : k2d_variant();
     *ty = (v == 0 || v == 3) ? 16 : (v == 4 ? 32 : 8);
 }
 
 template <bool VISC, bool CART>
 static void launch_v(const DevMesh& m, const double* Q, const Gas& g, const Epilogue& ep,
                      const DonorSet& ds, cudaStream_t st) {
-    switch (k2d_variant()) {
+    switch (rhs2d_variant_for(m.n, m.cart)) {
         case 1: launch_t<VISC, CART, 8, 2, 256>(m, Q, g, ep, ds, st); break;
         case 2: launch_t<VISC, CART, 8, 3, 256>(m, Q, g, ep, ds, st); break;
         case 3: launch_t<VISC, CART, 16, 1, 512>(m, Q, g, ep, ds, st); break;

@@ -204,7 +204,7 @@ static size_t plan_bytes(const Plan& P, bool dry, mrab_ctx* ctx, Bump* bump, boo
         }
         if (d == 2) {
             int tx, ty;
-            rhs2d_tile_shape(&tx, &ty);
+            rhs2d_tile_shape_for(m.n, m.cartesian ? 1 : 0, &tx, &ty);
             const size_t nt = (size_t)((m.n[0] + tx - 1) / tx) * ((m.n[1] + ty - 1) / ty);
             void* a = take(nt * sizeof(int32_t));
             void* b = take(nt * sizeof(int32_t));
@@ -1015,7 +1015,7 @@ mrab_status mrab_create(const mrab_plan* plan, const double* const* q0, void* d_
         if (d == 2) {
             // tile lists: tiles meeting the donor state box first (critical), then the rest
             int tx, ty;
-            rhs2d_tile_shape(&tx, &ty);
+            rhs2d_tile_shape_for(m.n, m.cartesian ? 1 : 0, &tx, &ty);
             const int ntx = (m.n[0] + tx - 1) / tx, nty = (m.n[1] + ty - 1) / ty;
             std::vector<int32_t> crit, bulk, slow, fastl;
             static const bool tag = [] {
@@ -1024,7 +1024,7 @@ mrab_status mrab_create(const mrab_plan* plan, const double* const* q0, void* d_
             }();
             for (int by = 0; by < nty; ++by)
                 for (int bx = 0; bx < ntx; ++bx) {
-                    const bool interior = tag && rhs2d_interior_tile(m.n, m.periodic, m.cls.data(), P.viscous, bx, by);
+                    const bool interior = tag && rhs2d_interior_tile(m.n, m.periodic, m.cls.data(), P.viscous, bx, by, m.cartesian ? 1 : 0);
                     const int32_t t = (by * ntx + bx) | (interior ? (int32_t)0x80000000u : 0);
                     const bool meets = m.is_donor && bx * tx <= m.st_hi[0] &&
                                        bx * tx + tx - 1 >= m.st_lo[0] && by * ty <= m.st_hi[1] &&
@@ -1261,7 +1261,7 @@ mrab_status mrab_time_kernel(mrab_ctx* c, int kernel, int mesh, int reps, int fl
                 ep.ntiles = kernel == 5 ? D.ngen : D.dm.ntl - D.ngen;
                 ep.lean_only = kernel == 3;
                 int tx, ty;
-                rhs2d_tile_shape(&tx, &ty);
+                rhs2d_tile_shape_for(mp.n, mp.cartesian ? 1 : 0, &tx, &ty);
                 Nk = (double)ep.ntiles * tx * ty;
             }
             if (d == 3 && rhs3d_split() && kernel == 0)
