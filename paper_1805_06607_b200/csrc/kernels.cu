@@ -1,12 +1,16 @@
 // CUDA kernels of libmrab.so (sm_100a, fp64, CUDA cores; no tensor cores: the path is a
-// stencil, not a dense contraction).  Round-1 "direct" kernels: one thread per grid point,
-// neighbours read through L1/L2.  DESIGN.md §5 lists each kernel with its roofline.
+// stencil, not a dense contraction).  DESIGN.md §5 lists each kernel with its roofline.
+// This file: the 3-D path and the shared pieces (2-D: kernels2d.cu, kernels2d_march.cu).
 //
-//   k_visc     Cartesian viscous fluxes F^V_i from D1 gradients (R3/R11)
-//   k_rhs      R = -J sum_k D_k Fhat_k + SAT (eq:int P:279-299) fused with the AB / RK
-//              combination epilogue (eq:ab_general P:358-361)
+//   k_flux3d   3-D pass 1: cross-region state staged by cp.async, D1 gradients, F^V (flagged
+//              tiles), contravariant fluxes of every point once (R3/R11)
+//   k_rhs3d    3-D pass 2 (PRE) / single pass: R = -J sum_k D_k Fhat_k + SAT (eq:int
+//              P:279-299) fused with the AB / RK combination epilogue (eq:ab_general P:358-361)
+//   k_visc3d_x Cartesian viscous fluxes on donor boxes at intermediate states (one round trip)
 //   k_combine  intermediate donor states base + sum beta_k R_k (MRAB Steps 2/5)
-//   k_interp   Lagrange gather of donor state and viscous flux at receivers
+//   k_interp3q Lagrange gather of donor state and viscous flux at receivers
+//   k_visc / k_rhs / k_interp  the original one-thread-per-point kernels (MRAB_3D_DIRECT=1,
+//              and the 2-D viscous pass on donor boxes)
 #include <cuda_runtime.h>
 
 #include "kernels.cuh"
