@@ -760,12 +760,13 @@ __global__ void __launch_bounds__(NT3, 2) k_visc3d(DevMesh m, const double* __re
 // ------------------------------------------------------------------------------------
 constexpr int XREG = 512 + 6 * 192;   // 1664
 __device__ __forceinline__ int xreg_idx(int x, int y, int z) {
+    // x slabs: the 3-deep direction fastest; y and z slabs: x fastest (contiguous 8-point rows)
     if (x < 0) return 512 + (x + 3) + 3 * (y + 8 * z);
     if (x >= 8) return 512 + 192 + (x - 8) + 3 * (y + 8 * z);
-    if (y < 0) return 512 + 2 * 192 + (y + 3) + 3 * (x + 8 * z);
-    if (y >= 8) return 512 + 3 * 192 + (y - 8) + 3 * (x + 8 * z);
-    if (z < 0) return 512 + 4 * 192 + (z + 3) + 3 * (x + 8 * y);
-    if (z >= 8) return 512 + 5 * 192 + (z - 8) + 3 * (x + 8 * y);
+    if (y < 0) return 512 + 2 * 192 + x + 8 * ((y + 3) + 3 * z);
+    if (y >= 8) return 512 + 3 * 192 + x + 8 * ((y - 8) + 3 * z);
+    if (z < 0) return 512 + 4 * 192 + x + 8 * y + 64 * (z + 3);
+    if (z >= 8) return 512 + 5 * 192 + x + 8 * y + 64 * (z - 8);
     return x + 8 * y + 64 * z;
 }
 __device__ __forceinline__ void xreg_xyz(int t, int& x, int& y, int& z) {
@@ -774,15 +775,21 @@ __device__ __forceinline__ void xreg_xyz(int t, int& x, int& y, int& z) {
         return;
     }
     const int k = t - 512, side = k / 192, w = k - side * 192;
-    const int a = w % 3, b = (w / 3) & 7, c = w / 24;
-    const int lo = a - 3, hi = 8 + a;
-    switch (side) {
-        case 0: x = lo; y = b; z = c; break;
-        case 1: x = hi; y = b; z = c; break;
-        case 2: y = lo; x = b; z = c; break;
-        case 3: y = hi; x = b; z = c; break;
-        case 4: z = lo; x = b; y = c; break;
-        default: z = hi; x = b; y = c; break;
+    if (side < 2) {
+        const int a = w % 3, b = (w / 3) & 7, c = w / 24;
+        x = side == 0 ? a - 3 : 8 + a;
+        y = b;
+        z = c;
+    } else if (side < 4) {
+        const int a = (w >> 3) % 3, c = (w >> 3) / 3;
+        x = w & 7;
+        y = side == 2 ? a - 3 : 8 + a;
+        z = c;
+    } else {
+        const int a = w >> 6;
+        x = w & 7;
+        y = (w >> 3) & 7;
+        z = side == 4 ? a - 3 : 8 + a;
     }
 }
 constexpr size_t SMEMX = sizeof(double) * 5 * XREG;
@@ -935,18 +942,38 @@ __global__ void __launch_bounds__(NT3, 2) k_flux3d(DevMesh m, const double* __re
     const int ntx = (n0 + T3X - 1) / T3X, nty = (n1 + T3Y - 1) / T3Y;
     const bool wfv = VISC && fvtile[tbx + ntx * (tby + nty * tbz)];
     const int nreg = VISC ? XREG : T3N;   // Euler: no gradients, the tile itself suffices
-    for (int t = tid; t < nreg; t += NT3) {
+    // copies: x-runs of the tile and of the y / z slabs two points at a time (16 bytes) when
+    // the mesh rows are 16-byte aligned; the x slabs (3-point runs) and ragged ends point-wise
+    const int npair = VISC ? (512 + 768) / 2 : 256;
+    for (int u = tid; u < npair + (VISC ? 384 : 0); u += NT3) {
+        int t, w;
+        if (u < npair) {
+            t = 2 * u;
+            if (t >= 512) t += 384;           // skip the x slabs
+            w = 2;
+        } else {
+            t = 512 + (u - npair);            // x slabs, one point
+            w = 1;
+        }
         int x, y, z;
         xreg_xyz(t, x, y, z);
-        int gi = i0 + x, gj = j0 + y, gk = k0 + z;
-        if (gi < 0) gi = per0 ? gi + n0 : 0; else if (gi >= n0) gi = per0 ? gi - n0 : n0 - 1;
+        int gj = j0 + y, gk = k0 + z;
         if (gj < 0) gj = per1 ? gj + n1 : 0; else if (gj >= n1) gj = per1 ? gj - n1 : n1 - 1;
         if (gk < 0) gk = per2 ? gk + n2 : 0; else if (gk >= n2) gk = per2 ? gk - n2 : n2 - 1;
-        const int64_t q = gi + s1 * gj + s2 * gk;
+        const bool pair16 = w == 2 && (n0 & 1) == 0 && i0 + x + 1 < n0;
+        for (int e = 0; e < w; ++e) {
+            if (pair16 && e == 1) break;
+            int gi = i0 + x + e;
+            if (gi < 0) gi = per0 ? gi + n0 : 0; else if (gi >= n0) gi = per0 ? gi - n0 : n0 - 1;
+            const int64_t q = gi + s1 * gj + s2 * gk;
 #pragma unroll
-        for (int c = 0; c < 5; ++c) {
-            const unsigned sa = (unsigned)__cvta_generic_to_shared(xr + c * XREG + t);
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(Q + c * N + q));
+            for (int c = 0; c < 5; ++c) {
+                const unsigned sa = (unsigned)__cvta_generic_to_shared(xr + c * XREG + t + e);
+                if (pair16)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(Q + c * N + q));
+                else
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(Q + c * N + q));
+            }
         }
     }
     unsigned clsv[PPT3];
