@@ -794,6 +794,51 @@ __device__ __forceinline__ void xreg_xyz(int t, int& x, int& y, int& z) {
 }
 constexpr size_t SMEMX = sizeof(double) * 5 * XREG;
 
+// stage the state of the cross-shaped region of the tile at (i0, j0, k0) into xr[5][XREG] by
+// cp.async: x-runs of the tile and of the y / z slabs two points at a time (16 bytes) when the
+// mesh rows are 16-byte aligned, the x slabs (3-point runs) and ragged ends point-wise.  Points
+// outside a non-periodic mesh are clamped to a valid address (no active stencil reads them).
+// full = false: the tile only (Euler: no gradients).
+__device__ __forceinline__ void stage_xregion(double* xr, const DevMesh& m, const double* __restrict__ Q,
+                                              int i0, int j0, int k0, bool full) {
+    const int n0 = m.n[0], n1 = m.n[1], n2 = m.n[2];
+    const int64_t N = m.npts, s1 = n0, s2 = (int64_t)n0 * n1;
+    const int per0 = m.periodic[0], per1 = m.periodic[1], per2 = m.periodic[2];
+    const bool al = (n0 & 1) == 0 && (i0 & 1) == 0;
+    const int npair = full ? (512 + 768) / 2 : 256;
+    for (int u = threadIdx.x; u < npair + (full ? 384 : 0); u += NT3) {
+        int t, w;
+        if (u < npair) {
+            t = 2 * u;
+            if (t >= 512) t += 384;           // skip the x slabs
+            w = 2;
+        } else {
+            t = 512 + (u - npair);            // x slabs, one point
+            w = 1;
+        }
+        int x, y, z;
+        xreg_xyz(t, x, y, z);
+        int gj = j0 + y, gk = k0 + z;
+        if (gj < 0) gj = per1 ? gj + n1 : 0; else if (gj >= n1) gj = per1 ? gj - n1 : n1 - 1;
+        if (gk < 0) gk = per2 ? gk + n2 : 0; else if (gk >= n2) gk = per2 ? gk - n2 : n2 - 1;
+        const bool pair16 = w == 2 && al && i0 + x + 1 < n0;
+        for (int e = 0; e < w; ++e) {
+            if (pair16 && e == 1) break;
+            int gi = i0 + x + e;
+            if (gi < 0) gi = per0 ? gi + n0 : 0; else if (gi >= n0) gi = per0 ? gi - n0 : n0 - 1;
+            const int64_t q = gi + s1 * gj + s2 * gk;
+#pragma unroll
+            for (int c = 0; c < 5; ++c) {
+                const unsigned sa = (unsigned)__cvta_generic_to_shared(xr + c * XREG + t + e);
+                if (pair16)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(Q + c * N + q));
+                else
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(Q + c * N + q));
+            }
+        }
+    }
+}
+
 template <bool CART>
 __global__ void __launch_bounds__(NT3, 2) k_visc3d_x(DevMesh m, const double* __restrict__ Q,
                                                     double* __restrict__ FV, Box box, Gas g) {
@@ -808,20 +853,7 @@ __global__ void __launch_bounds__(NT3, 2) k_visc3d_x(DevMesh m, const double* __
     const int per0 = m.periodic[0], per1 = m.periodic[1], per2 = m.periodic[2];
     // ---- one round trip: the whole cross region (points outside a non-periodic mesh are
     // clamped to a valid address; no active stencil reads them)
-    for (int t = tid; t < XREG; t += NT3) {
-        int x, y, z;
-        xreg_xyz(t, x, y, z);
-        int gi = i0 + x, gj = j0 + y, gk = k0 + z;
-        if (gi < 0) gi = per0 ? gi + n0 : 0; else if (gi >= n0) gi = per0 ? gi - n0 : n0 - 1;
-        if (gj < 0) gj = per1 ? gj + n1 : 0; else if (gj >= n1) gj = per1 ? gj - n1 : n1 - 1;
-        if (gk < 0) gk = per2 ? gk + n2 : 0; else if (gk >= n2) gk = per2 ? gk - n2 : n2 - 1;
-        const int64_t q = gi + s1 * gj + s2 * gk;
-#pragma unroll
-        for (int c = 0; c < 5; ++c) {
-            const unsigned sa = (unsigned)__cvta_generic_to_shared(xr + c * XREG + t);
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(Q + c * N + q));
-        }
-    }
+    stage_xregion(xr, m, Q, i0, j0, k0, true);
     unsigned clsv[PPT3];
 #pragma unroll
     for (int s = 0; s < PPT3; ++s) {
@@ -942,40 +974,7 @@ __global__ void __launch_bounds__(NT3, 2) k_flux3d(DevMesh m, const double* __re
     const int ntx = (n0 + T3X - 1) / T3X, nty = (n1 + T3Y - 1) / T3Y;
     const bool wfv = VISC && fvtile[tbx + ntx * (tby + nty * tbz)];
     const int nreg = VISC ? XREG : T3N;   // Euler: no gradients, the tile itself suffices
-    // copies: x-runs of the tile and of the y / z slabs two points at a time (16 bytes) when
-    // the mesh rows are 16-byte aligned; the x slabs (3-point runs) and ragged ends point-wise
-    const int npair = VISC ? (512 + 768) / 2 : 256;
-    for (int u = tid; u < npair + (VISC ? 384 : 0); u += NT3) {
-        int t, w;
-        if (u < npair) {
-            t = 2 * u;
-            if (t >= 512) t += 384;           // skip the x slabs
-            w = 2;
-        } else {
-            t = 512 + (u - npair);            // x slabs, one point
-            w = 1;
-        }
-        int x, y, z;
-        xreg_xyz(t, x, y, z);
-        int gj = j0 + y, gk = k0 + z;
-        if (gj < 0) gj = per1 ? gj + n1 : 0; else if (gj >= n1) gj = per1 ? gj - n1 : n1 - 1;
-        if (gk < 0) gk = per2 ? gk + n2 : 0; else if (gk >= n2) gk = per2 ? gk - n2 : n2 - 1;
-        const bool pair16 = w == 2 && (n0 & 1) == 0 && i0 + x + 1 < n0;
-        for (int e = 0; e < w; ++e) {
-            if (pair16 && e == 1) break;
-            int gi = i0 + x + e;
-            if (gi < 0) gi = per0 ? gi + n0 : 0; else if (gi >= n0) gi = per0 ? gi - n0 : n0 - 1;
-            const int64_t q = gi + s1 * gj + s2 * gk;
-#pragma unroll
-            for (int c = 0; c < 5; ++c) {
-                const unsigned sa = (unsigned)__cvta_generic_to_shared(xr + c * XREG + t + e);
-                if (pair16)
-                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(Q + c * N + q));
-                else
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(Q + c * N + q));
-            }
-        }
-    }
+    stage_xregion(xr, m, Q, i0, j0, k0, VISC);
     unsigned clsv[PPT3];
 #pragma unroll
     for (int s = 0; s < PPT3; ++s) {
