@@ -13,6 +13,9 @@
 //              and the 2-D viscous pass on donor boxes)
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <vector>
+
 #include "kernels.cuh"
 #include "mrab_internal.h"
 #include "stencil_table.cuh"
@@ -1399,6 +1402,114 @@ __global__ void __launch_bounds__(128) k_interp3q(RecvList rl, DonorSet ds) {
     }
 }
 
+// 3-D gather staged per donor box: one CTA per receiver group (host-built: receivers whose 4^3
+// donor stencils lie in one 7^3 box of the donor mesh).  The box's state and Cartesian viscous
+// fluxes (343 points x 17 values) are copied to shared memory once by cp.async; every receiver
+// of the group then interpolates from there with four lanes (one per stencil column) and a quad
+// shuffle reduction.  Neighbouring receivers share most of their stencils, so the donor data
+// crosses L2 once per box instead of once per receiver (k_interp3q).
+constexpr int IBOX = 7, IBOXN = IBOX * IBOX * IBOX;
+template <bool VISC>
+__global__ void __launch_bounds__(128) k_interp3b(RecvList rl, DonorSet ds) {
+    constexpr int NC = 5, NF = 12, NV = NC + (VISC ? NF : 0);
+    extern __shared__ __align__(16) double bx[];   // [NV][IBOXN]
+    const int* gi6 = rl.ginfo + 6 * blockIdx.x;
+    const int start = gi6[0], count = gi6[1], dm = gi6[2];
+    const int ox = gi6[3], oy = gi6[4], oz = gi6[5];
+    const int n0 = ds.n[dm][0], n1 = ds.n[dm][1], n2 = ds.n[dm][2];
+    const int64_t N = ds.npts[dm];
+    const double* __restrict__ S = ds.state[dm];
+    const double* __restrict__ F = ds.fv[dm];
+    for (int t = threadIdx.x; t < IBOXN; t += blockDim.x) {
+        const int x = t % IBOX, y = (t / IBOX) % IBOX, z = t / (IBOX * IBOX);
+        int i = ox + x, j = oy + y, k = oz + z;
+        // the box may cross a periodic seam (bases are wrapped) or run past a face: wrap, clamp
+        if (i >= n0) i -= n0;
+        if (j >= n1) j -= n1;
+        if (k >= n2) k -= n2;
+        i = min(i, n0 - 1);
+        j = min(j, n1 - 1);
+        k = min(k, n2 - 1);
+        const int64_t q = i + (int64_t)n0 * (j + (int64_t)n1 * k);
+#pragma unroll
+        for (int c = 0; c < NV; ++c) {
+            const double* src = c < NC ? S + c * N + q : F + (int64_t)(c - NC) * N + q;
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(bx + c * IBOXN + t);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(src));
+        }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    const int a0 = threadIdx.x & 3;
+    for (int rr = threadIdx.x >> 2; rr < ((count + 31) / 32) * 32; rr += blockDim.x >> 2) {
+        const bool live = rr < count;
+        double acc[NV];
+#pragma unroll
+        for (int c = 0; c < NV; ++c) acc[c] = 0.0;
+        int r = 0;
+        if (live) {
+            r = rl.gorder[start + rr];
+            int lx = rl.base[3 * r] - ox, ly = rl.base[3 * r + 1] - oy, lz = rl.base[3 * r + 2] - oz;
+            if (lx < 0) lx += n0;
+            if (ly < 0) ly += n1;
+            if (lz < 0) lz += n2;
+            const double* w = rl.w + r * 12;
+            const double w0 = w[a0];
+#pragma unroll 4
+            for (int a = 0; a < 16; ++a) {
+                const int a1 = a & 3, a2 = a >> 2;
+                const double W = w0 * w[4 + a1] * w[8 + a2];
+                const int e = (lx + a0) + IBOX * ((ly + a1) + IBOX * (lz + a2));
+#pragma unroll
+                for (int c = 0; c < NV; ++c) acc[c] += W * bx[c * IBOXN + e];
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < NV; ++c) {
+            acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], 1);
+            acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], 2);
+        }
+        if (live && a0 == 0) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) rl.qhat[c * rl.n + r] = acc[c];
+            if (VISC)
+#pragma unroll
+                for (int c = 0; c < NF; ++c) rl.fvhat[c * rl.n + r] = acc[NC + c];
+        }
+    }
+}
+
+std::vector<int32_t> interp3_groups(int64_t R, const int32_t* donor, const int32_t* base,
+                                    std::vector<int32_t>& order) {
+    struct Key {
+        int d, x, y, z;
+        int64_t r;
+    };
+    std::vector<Key> keys((size_t)R);
+    for (int64_t r = 0; r < R; ++r)
+        keys[r] = {donor[r], base[3 * r] / 4, base[3 * r + 1] / 4, base[3 * r + 2] / 4, r};
+    std::stable_sort(keys.begin(), keys.end(), [](const Key& a, const Key& b) {
+        if (a.d != b.d) return a.d < b.d;
+        if (a.z != b.z) return a.z < b.z;
+        if (a.y != b.y) return a.y < b.y;
+        return a.x < b.x;
+    });
+    order.resize((size_t)R);
+    std::vector<int32_t> info;
+    int64_t i = 0;
+    while (i < R) {
+        int64_t j = i;
+        while (j < R && j - i < 64 && keys[j].d == keys[i].d && keys[j].x == keys[i].x &&
+               keys[j].y == keys[i].y && keys[j].z == keys[i].z)
+            ++j;
+        info.insert(info.end(), {(int32_t)i, (int32_t)(j - i), keys[i].d, 4 * keys[i].x, 4 * keys[i].y,
+                                 4 * keys[i].z});
+        for (int64_t k = i; k < j; ++k) order[k] = (int32_t)keys[k].r;
+        i = j;
+    }
+    return info;
+}
+
 // ------------------------------------------------------------------------------------
 // launchers
 // ------------------------------------------------------------------------------------
@@ -1623,7 +1734,17 @@ void launch_interp(int dim, int viscous, const RecvList& rl, const DonorSet& ds,
             const char* e = getenv("MRAB_INTERP_QUAD");
             quad = e ? atoi(e) : 1;
         }
-        if (quad) {
+        if (rl.ginfo && rl.ngroups > 0) {
+            const size_t bytes = sizeof(double) * (viscous ? 17 : 5) * IBOXN;
+            static bool init = false;
+            if (!init) {
+                cudaFuncSetAttribute(k_interp3b<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double) * 17 * IBOXN));
+                cudaFuncSetAttribute(k_interp3b<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double) * 17 * IBOXN));
+                init = true;
+            }
+            if (viscous) k_interp3b<true><<<rl.ngroups, 128, bytes, st>>>(rl, ds);
+            else k_interp3b<false><<<rl.ngroups, 128, bytes, st>>>(rl, ds);
+        } else if (quad) {
             const unsigned nbq = (unsigned)((rl.n * 4 + 127) / 128);
             if (viscous) k_interp3q<true><<<nbq, 128, 0, st>>>(rl, ds);
             else k_interp3q<false><<<nbq, 128, 0, st>>>(rl, ds);

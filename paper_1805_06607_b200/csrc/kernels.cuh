@@ -102,7 +102,16 @@ struct RecvList {
     const double* w;          // [R][3][4]
     double* qhat;             // [nc][R]
     double* fvhat;            // [d][d+1][R]
+    // 3-D box-staged gather: receivers grouped by donor box (host-built; NULL = per-receiver)
+    const int32_t* gorder;    // [R] receiver indices in group order
+    const int32_t* ginfo;     // [G][6]: start, count, donor mesh, box origin (3)
+    int ngroups;
 };
+// host: group 3-D receivers whose 4^3 donor stencils lie in one 7^3 donor box (origin = base
+// rounded down to a multiple of 4 per axis), at most 64 per group; returns ginfo [G][6] and
+// fills order [R]
+std::vector<int32_t> interp3_groups(int64_t R, const int32_t* donor, const int32_t* base,
+                                    std::vector<int32_t>& order);
 
 struct DonorSet {             // per donor mesh: where to read state / viscous flux
     const double* state[8];

@@ -60,6 +60,9 @@ struct MeshDev {
     int32_t* rdonor = nullptr;
     int32_t* rbase = nullptr;
     double* rw = nullptr;
+    int32_t* gorder = nullptr;    // 3-D: receivers in donor-box group order (box-staged gather)
+    int32_t* ginfo = nullptr;     // 3-D: [G][6] group descriptors
+    int ngroups = 0;
     double* qhat = nullptr;       // [S][nc][R]: one set per micro index j (batched gathers)
     double* fvhat = nullptr;      // [S][d(d+1)][R]
     int32_t* tiles = nullptr;     // 2-D: critical tiles (cover the donor box) then the bulk
@@ -193,7 +196,11 @@ static size_t plan_bytes(const Plan& P, bool dry, mrab_ctx* ctx, Bump* bump, boo
             void* e = take(Rm * 12 * sizeof(double));
             void* f = take((size_t)P.S * Rm * nc * sizeof(double));
             void* h = take((size_t)P.S * Rm * d * (d + 1) * sizeof(double));
+            void* go = d == 3 ? take(Rm * sizeof(int32_t)) : nullptr;
+            void* gf = d == 3 ? take(Rm * 6 * sizeof(int32_t)) : nullptr;
             if (D) {
+                D->gorder = (int32_t*)go;
+                D->ginfo = (int32_t*)gf;
                 D->rpoint = (int64_t*)a;
                 D->rdonor = (int32_t*)b;
                 D->rbase = (int32_t*)c;
@@ -273,6 +280,9 @@ static void issue_interp(mrab_ctx* c, int g, const double* const* state_of, bool
     rl.w = D.rw;
     rl.qhat = D.qhat;
     rl.fvhat = D.fvhat;
+    rl.gorder = D.gorder;
+    rl.ginfo = D.ginfo;
+    rl.ngroups = D.ngroups;
     launch_interp(P.dim, P.viscous, rl, make_ds(c, state_of), c->st);
     c->launch_counter++;
 }
@@ -989,6 +999,17 @@ mrab_status mrab_create(const mrab_plan* plan, const double* const* q0, void* d_
             CK(cudaMemcpy(D.rdonor, m.rdonor.data(), R * sizeof(int32_t), cudaMemcpyHostToDevice));
             CK(cudaMemcpy(D.rbase, m.rbase.data(), R * 3 * sizeof(int32_t), cudaMemcpyHostToDevice));
             CK(cudaMemcpy(D.rw, m.rw.data(), R * 12 * sizeof(double), cudaMemcpyHostToDevice));
+            static const int boxg = [] {
+                const char* e = getenv("MRAB_INTERP_BOX");
+                return e ? atoi(e) : 1;
+            }();
+            if (d == 3 && boxg) {
+                std::vector<int32_t> order;
+                const std::vector<int32_t> info = interp3_groups((int64_t)R, m.rdonor.data(), m.rbase.data(), order);
+                CK(cudaMemcpy(D.gorder, order.data(), R * sizeof(int32_t), cudaMemcpyHostToDevice));
+                CK(cudaMemcpy(D.ginfo, info.data(), info.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+                D.ngroups = (int)(info.size() / 6);
+            }
         }
         DevMesh& dm = D.dm;
         for (int k = 0; k < 3; ++k) {
