@@ -131,6 +131,17 @@ mrab_status mrab_get_state(mrab_ctx* ctx, int mesh, double* dst, double* t);
  * dense [nc][n...]); the RHS histories are kept.  Synchronises. */
 mrab_status mrab_set_state(mrab_ctx* ctx, int mesh, const double* src);
 
+/* Integrator history access for the step-matrix stability procedure (eq:sm, eq:sm_form,
+ * "the stability vector element being perturbed may also be a right-hand side
+ * history element").  At a macro boundary t after the bootstrap the integrator vector of
+ * mesh g is its state plus m-1 committed RHS history entries R(t - (m-1-k) h_g), k = 0
+ * (oldest) .. m-2; R(t) itself is evaluated by the next mrab_step (deferred
+ * RHS).  dst/src: host or device, dense [nc][n...], caller-owned.  Errors: MRAB_E_INVALID
+ * (bad mesh, k outside [0, m-2], NULL pointer), MRAB_E_INSUFFICIENT_HISTORY (called before
+ * the m-1 bootstrap macro steps are done).  Synchronise. */
+mrab_status mrab_get_history(mrab_ctx* ctx, int mesh, int k, double* dst);
+mrab_status mrab_set_history(mrab_ctx* ctx, int mesh, int k, const double* src);
+
 /* Parity hook: one coupled RHS evaluation (eq:int) of every mesh at the given
  * states q[g] (host or device, dense) -> rhs_out[g] (host or device, dense).  Does not
  * change the integrator state.  Synchronises. */

@@ -1182,6 +1182,44 @@ mrab_status mrab_set_state(mrab_ctx* c, int mesh, const double* src) {
     return MRAB_OK;
 }
 
+// committed history entry k (0 = oldest) of mesh g at a macro boundary after the bootstrap:
+// the ring holds R(t - (m-1) h_g) .. R(t - h_g); R(t) is pending (evaluated by the next step)
+static mrab_status history_slot(mrab_ctx* c, int mesh, int k, double** out) {
+    if (!c || mesh < 0 || mesh >= (int)c->md.size()) return fail(MRAB_E_INVALID, "bad arguments");
+    const Plan& P = *c->P;
+    const int m = P.history_m;
+    if (k < 0 || k > m - 2) return fail(MRAB_E_INVALID, "history index out of range [0, m-2]");
+    if (c->macro < m - 1)
+        return fail(MRAB_E_INSUFFICIENT_HISTORY, "history is complete only after the bootstrap");
+    const int slot = ((c->book.head[mesh] - (m - 2) + k) % m + m) % m;
+    *out = c->md[mesh].ring[slot];
+    return MRAB_OK;
+}
+
+mrab_status mrab_get_history(mrab_ctx* c, int mesh, int k, double* dst) {
+    double* src = nullptr;
+    if (!dst) return fail(MRAB_E_INVALID, "bad arguments");
+    mrab_status st = history_slot(c, mesh, k, &src);
+    if (st != MRAB_OK) return st;
+    const size_t bytes = (size_t)c->P->nc * c->P->meshes[mesh].npts * sizeof(double);
+    CK(cudaStreamSynchronize(c->st));
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return MRAB_OK;
+}
+
+mrab_status mrab_set_history(mrab_ctx* c, int mesh, int k, const double* src) {
+    double* dst = nullptr;
+    if (!src) return fail(MRAB_E_INVALID, "bad arguments");
+    mrab_status st = history_slot(c, mesh, k, &dst);
+    if (st != MRAB_OK) return st;
+    const size_t bytes = (size_t)c->P->nc * c->P->meshes[mesh].npts * sizeof(double);
+    CK(cudaStreamSynchronize(c->st));
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return MRAB_OK;
+}
+
 mrab_status mrab_rhs(mrab_ctx* c, const double* const* q, double* const* rhs_out) {
     if (!c || !q || !rhs_out) return fail(MRAB_E_INVALID, "bad arguments");
     const Plan& P = *c->P;

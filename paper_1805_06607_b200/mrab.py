@@ -66,6 +66,8 @@ def lib():
         L.mrab_step.argtypes = [vp, C.c_int]
         L.mrab_get_state.argtypes = [vp, C.c_int, vp, dp]
         L.mrab_set_state.argtypes = [vp, C.c_int, vp]
+        L.mrab_get_history.argtypes = [vp, C.c_int, C.c_int, vp]
+        L.mrab_set_history.argtypes = [vp, C.c_int, C.c_int, vp]
         L.mrab_rhs.argtypes = [vp, C.POINTER(vp), C.POINTER(vp)]
         L.mrab_get_counters.argtypes = [vp, i64p, i64p, i64p]
         L.mrab_launches_per_macro_step.argtypes = [vp, i64p]
@@ -75,7 +77,7 @@ def lib():
         for name in ("mrab_ab_weights", "mrab_plan_create", "mrab_plan_info",
                      "mrab_plan_get_tables", "mrab_plan_get_metrics", "mrab_create",
                      "mrab_step", "mrab_get_state", "mrab_set_state", "mrab_rhs",
-                     "mrab_get_counters", "mrab_launches_per_macro_step", "mrab_time_kernel"):
+                     "mrab_get_history", "mrab_set_history", "mrab_get_counters", "mrab_launches_per_macro_step", "mrab_time_kernel"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -85,7 +87,7 @@ EXPORTED = ["mrab_ab_weights", "mrab_plan_create", "mrab_plan_destroy", "mrab_pl
             "mrab_plan_get_tables", "mrab_plan_get_metrics", "mrab_workspace_bytes",
             "mrab_create", "mrab_destroy", "mrab_step", "mrab_get_state", "mrab_set_state",
             "mrab_rhs", "mrab_get_counters", "mrab_launches_per_macro_step", "mrab_time_kernel",
-            "mrab_set_trace", "mrab_last_error"]
+            "mrab_set_trace", "mrab_last_error", "mrab_get_history", "mrab_set_history"]
 
 
 def _check(st):
@@ -229,6 +231,21 @@ class Context:
         if isinstance(src, np.ndarray):
             assert src.dtype == np.float64 and src.flags.c_contiguous
         _check(lib().mrab_set_state(self.h, g, C.c_void_p(ptr)))
+
+    def get_history(self, g, k, out=None):
+        """Committed RHS history entry k (0 = oldest of m-1) of mesh g at the macro boundary."""
+        shp = (self.plan.nc,) + tuple(reversed(self.plan.shapes[g]))
+        if out is None:
+            out = np.zeros(shp)
+        ptr = out.ctypes.data if isinstance(out, np.ndarray) else out.data_ptr()
+        _check(lib().mrab_get_history(self.h, g, int(k), C.c_void_p(ptr)))
+        return out
+
+    def set_history(self, g, k, src):
+        if isinstance(src, np.ndarray):
+            assert src.dtype == np.float64 and src.flags.c_contiguous
+        ptr = src.ctypes.data if isinstance(src, np.ndarray) else src.data_ptr()
+        _check(lib().mrab_set_history(self.h, g, int(k), C.c_void_p(ptr)))
 
     def rhs(self, states):
         qs = [np.ascontiguousarray(q, dtype=np.float64) for q in states]
