@@ -1,0 +1,79 @@
+"""GPU step-matrix stability procedure against the oracle's (tests/ only call
+oracle/).  Tiny overset problem: the inviscid box-in-box of App. C at N = 17 (4440-element
+integrator vector: 2 meshes x 4 components x (state + 2 history entries)), AB3, rates 2:1.
+Tolerances: the map itself 1e-10 relative (north_star); step-matrix columns formed with
+eps = 1e-5 so that the finite-difference rounding noise (~1e-13 |phi| / eps) stays below the
+1e-6 bar; the power-iteration estimate of rho to 1e-6 relative."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import rhs as orhs, stability as ostab
+from paper_1805_06607_b200 import mrab, stability
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+STEPS = [2, 1]
+
+
+@pytest.fixture(scope="module")
+def setup():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    p = synth.configs.mms_box_in_box(17, "inviscid")
+    p.order_n, p.history_m, p.h = 3, 3, 0.002
+    ctx = mrab.Context(mrab.Plan(p, steps=STEPS), p.q0)
+    with pytest.raises(mrab.MrabError, match="INSUFFICIENT_HISTORY"):
+        ctx.get_history(0, 0)
+    ctx.step(p.history_m - 1)                      # bootstrap
+    smap = stability.StepMap(ctx)
+    phi0 = smap.read()
+    yield p, orhs.build(p), smap, phi0
+    ctx.close()
+
+
+def _omap(p, st):
+    return lambda phi: ostab.macro_map(p, phi, steps=STEPS, setup=st)
+
+
+def test_map_parity(setup):
+    p, st, smap, phi0 = setup
+    assert phi0.size == smap.dim == 4 * (17 * 17 + 9 * 9) * 3
+    g = smap(phi0)
+    o = _omap(p, st)(phi0)
+    assert np.max(np.abs(g - o)) <= 1e-10 * np.max(np.abs(o))
+    # history entries round-trip through set/get unchanged
+    smap.write(phi0)
+    assert np.array_equal(smap.read(), phi0)
+
+
+def test_step_matrix_columns(setup):
+    p, st, smap, phi0 = setup
+    rng = np.random.default_rng(5)
+    n1 = 4 * 17 * 17
+    # state and both history entries of each mesh
+    cols = sorted(set(rng.integers(0, phi0.size, 16).tolist()
+                      + [0, n1 - 1, n1, 2 * n1, 3 * n1, 3 * n1 + 4 * 81, phi0.size - 1]))
+    Gg = stability.step_matrix(smap, phi0, eps=1e-5, cols=cols)
+    om = _omap(p, st)
+    base = om(phi0)
+    for c, j in enumerate(cols):
+        ph = phi0.copy()
+        ph[j] += 1e-5
+        col = (om(ph) - base) / 1e-5
+        assert np.max(np.abs(Gg[:, c] - col)) <= 1e-6 * max(1.0, np.max(np.abs(col))), j
+
+
+def test_power_estimate_parity(setup):
+    p, st, smap, phi0 = setup
+    rg = stability.power_estimate(smap, phi0, iters=20, eps=1e-5, seed=3)
+    om = _omap(p, st)
+    base = om(phi0)
+    v = np.random.default_rng(3).standard_normal(phi0.size)
+    v /= np.linalg.norm(v)
+    for _ in range(20):
+        w = (om(phi0 + 1e-5 * v) - base) / 1e-5
+        ro = float(np.linalg.norm(w))
+        v = w / ro
+    assert abs(rg - ro) <= 1e-6 * ro, (rg, ro)
+    print(f"rho estimate gpu {rg:.9f} oracle {ro:.9f}")
