@@ -77,7 +77,8 @@ def lib():
         for name in ("mrab_ab_weights", "mrab_plan_create", "mrab_plan_info",
                      "mrab_plan_get_tables", "mrab_plan_get_metrics", "mrab_create",
                      "mrab_step", "mrab_get_state", "mrab_set_state", "mrab_rhs",
-                     "mrab_get_history", "mrab_set_history", "mrab_get_counters", "mrab_launches_per_macro_step", "mrab_time_kernel"):
+                     "mrab_get_history", "mrab_set_history", "mrab_get_counters",
+                     "mrab_launches_per_macro_step", "mrab_time_kernel"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -150,6 +151,7 @@ class Plan:
         self.nc = problem.dim + 2
         self.shapes = [tuple(m.shape) for m in problem.meshes]
         self.n_meshes = len(problem.meshes)
+        self.history_m = int(problem.history_m)
 
     def __del__(self):
         if getattr(self, "h", None) and _lib is not None:
