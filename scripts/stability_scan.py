@@ -32,12 +32,18 @@ def main():
     out["dense"] = {"h": 0.002, "rates": [2, 1], "dim": int(phi.size),
                     "rho": stability.spectral_radius(G), "columns_s": tG}
     ctx.close()
+    print(json.dumps(out), flush=True)
     for name, steps in (("srab", [1, 1]), ("mrab_sr2", [2, 1])):
         def rho_of(H):
-            c, s, ph = smap_for(H / max(steps), steps)
-            r = stability.power_estimate(s, ph, iters=60)
-            c.close()
-            return r
+            c = None
+            try:
+                c, s, ph = smap_for(H / max(steps), steps)
+                return stability.power_estimate(s, ph, iters=60)
+            except mrab.MrabError:                 # bootstrap or step blew up: unstable
+                return float("inf")
+            finally:
+                if c is not None:
+                    c.close()
         Hmax = stability.max_stable(rho_of, 0.001, 0.2, tol=1e-4)
         out[name] = {"rates": steps, "max_stable_macro_H": Hmax,
                      "max_stable_micro_h": Hmax / max(steps)}

@@ -78,3 +78,15 @@ def test_plan_errors():
     p.meshes[1].xyz = np.ascontiguousarray(p.meshes[1].xyz[:, :, ::-1])   # left-handed
     with pytest.raises(mrab.MrabError):
         mrab.Plan(p)
+
+
+def test_product_path_is_independent_of_the_oracle():
+    """The package (CUDA binding, stability laboratory) never imports oracle/, and the oracle
+    never imports the package (the two share no code)."""
+    pkg = os.path.join(ROOT, "paper_1805_06607_b200")
+    for d, pat in ((pkg, r"^\s*(from|import)\s+oracle\b"),
+                   (os.path.join(ROOT, "oracle"), r"^\s*(from|import)\s+paper_1805_06607_b200\b")):
+        for f in os.listdir(d):
+            if f.endswith(".py"):
+                src = open(os.path.join(d, f)).read()
+                assert not re.search(pat, src, re.M), f
