@@ -77,3 +77,13 @@ def test_power_estimate_parity(setup):
         v = w / ro
     assert abs(rg - ro) <= 1e-6 * ro, (rg, ro)
     print(f"rho estimate gpu {rg:.9f} oracle {ro:.9f}")
+
+
+def test_history_accessor_errors(setup):
+    p, st, smap, phi0 = setup
+    ctx = smap.ctx
+    for k in (-1, p.history_m - 1):
+        with pytest.raises(mrab.MrabError, match="INVALID"):
+            ctx.get_history(0, k)
+    with pytest.raises(mrab.MrabError, match="INVALID"):
+        ctx.get_history(2, 0)

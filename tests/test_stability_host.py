@@ -1,0 +1,60 @@
+"""Host logic of the GPU stability laboratory without a GPU: StepMap's integrator-vector
+layout (state, then m-1 history entries oldest first, mesh by mesh) against a fake context,
+and the bisection helper."""
+import numpy as np
+
+from paper_1805_06607_b200 import stability
+
+
+class _FakePlan:
+    nc, history_m, n_meshes = 2, 3, 2
+    shapes = [(3, 2), (2, 2)]                      # (ni, nj): arrays are [nc][nj][ni]
+
+
+class _FakeCtx:
+    """Stores state/history; step(1) applies the linear map y -> 2y, H_k -> H_k + k."""
+
+    def __init__(self):
+        self.plan = _FakePlan()
+        rng = np.random.default_rng(1)
+        self.q = [rng.standard_normal((2, 2, 3)), rng.standard_normal((2, 2, 2))]
+        self.H = [[rng.standard_normal(q.shape) for _ in range(2)] for q in self.q]
+
+    def get_state(self, g):
+        return self.q[g].copy(), 0.0
+
+    def set_state(self, g, src):
+        self.q[g] = src.copy()
+
+    def get_history(self, g, k):
+        return self.H[g][k].copy()
+
+    def set_history(self, g, k, src):
+        self.H[g][k] = src.copy()
+
+    def step(self, n):
+        self.q = [2 * q for q in self.q]
+        self.H = [[h + k for k, h in enumerate(Hg)] for Hg in self.H]
+
+
+def test_stepmap_layout_and_columns():
+    ctx = _FakeCtx()
+    sm = stability.StepMap(ctx)
+    assert sm.dim == (12 + 8) * 3
+    phi = sm.read()
+    exp = np.concatenate([ctx.q[0].ravel(), ctx.H[0][0].ravel(), ctx.H[0][1].ravel(),
+                          ctx.q[1].ravel(), ctx.H[1][0].ravel(), ctx.H[1][1].ravel()])
+    assert np.array_equal(phi, exp)
+    G = stability.step_matrix(sm, phi, eps=1e-3)
+    d = np.ones(sm.dim)
+    for o in (0, 36):                               # state blocks of mesh 0 / mesh 1
+        n = 12 if o == 0 else 8
+        d[o:o + n] = 2.0
+    assert np.allclose(G, np.diag(d), atol=1e-9)
+    assert abs(stability.spectral_radius(G) - 2.0) < 1e-9
+
+
+def test_max_stable_bisection():
+    x = stability.max_stable(lambda h: 1.0 + (h - 0.3), 0.0, 1.0, tol=1e-6)
+    assert abs(x - 0.3) < 1e-6
+    assert stability.max_stable(lambda h: 0.5, 0.0, 1.0) == 1.0
