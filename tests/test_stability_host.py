@@ -58,3 +58,11 @@ def test_max_stable_bisection():
     x = stability.max_stable(lambda h: 1.0 + (h - 0.3), 0.0, 1.0, tol=1e-6)
     assert abs(x - 0.3) < 1e-6
     assert stability.max_stable(lambda h: 0.5, 0.0, 1.0) == 1.0
+
+
+def test_krylov_and_power_match_dense_on_fake_linear_map():
+    ctx = _FakeCtx()
+    sm = stability.StepMap(ctx)
+    phi = sm.read()
+    assert abs(stability.spectral_radius_krylov(sm, phi, eps=1e-3, tol=1e-10) - 2.0) < 1e-6
+    assert abs(stability.power_estimate(sm, phi, iters=40, eps=1e-3) - 2.0) < 1e-6
