@@ -107,13 +107,14 @@ def power_estimate(smap: StepMap, phi0, iters=30, eps=EPS, seed=0):
     return est
 
 
-def max_stable(rho_of, lo, hi, tol=1e-4):
-    """Largest x in [lo, hi] with rho_of(x) <= 1 by bisection to tol."""
-    if rho_of(hi) <= 1.0:
+def max_stable(rho_of, lo, hi, tol=1e-4, one=1.0):
+    """Largest x in [lo, hi] with rho_of(x) <= one by bisection to tol.  `one` > 1
+    absorbs the finite-difference noise of eq:sm_form on neutral modes (DESIGN.md R-SM)."""
+    if rho_of(hi) <= one:
         return hi
     while hi - lo > tol:
         mid = 0.5 * (lo + hi)
-        if rho_of(mid) <= 1.0:
+        if rho_of(mid) <= one:
             lo = mid
         else:
             hi = mid
