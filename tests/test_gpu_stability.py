@@ -85,5 +85,6 @@ def test_history_accessor_errors(setup):
     for k in (-1, p.history_m - 1):
         with pytest.raises(mrab.MrabError, match="INVALID"):
             ctx.get_history(0, k)
-    with pytest.raises(mrab.MrabError, match="INVALID"):
-        ctx.get_history(2, 0)
+    buf = np.zeros(16)
+    assert mrab.lib().mrab_get_history(ctx.h, 2, 0, buf.ctypes.data) == 1    # MRAB_E_INVALID
+    assert mrab.lib().mrab_get_history(ctx.h, 0, 0, None) == 1
