@@ -4,9 +4,10 @@
 Contract:
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mrab|reference] [--config C]
 One "step" = one MRAB macro step H = S_max h of the whole hot path (every mesh's fused
-SBP-SAT RHS + AB update at its own rate, donor intermediate states, Lagrange gathers) on the
-cylinder workload, BASELINE.json configs[2] (config 3, full size: every timed number of the
-paper is on its cylinder case) unless --config says otherwise.
+SBP-SAT RHS + AB update at its own rate, donor intermediate states, Lagrange gathers) on
+BASELINE.json configs[3] (config 4, full size: the largest configuration that fits one GPU,
+23.9 M points; BASELINE.json's metric names no config) unless --config says otherwise; the
+cylinder stand-in (config 3) is measured beside it as `secondary`.
 metric = grid-point RHS evaluations per second (sum over meshes of active points x RHS
 evaluations, fp64).  L2 is scrubbed (256 MiB write + 256 MiB read of another buffer)
 between timed steps.  Multi-GPU: one
@@ -31,6 +32,10 @@ import numpy as np  # noqa: E402
 METRIC = "grid-point RHS evals/sec (fp64)"
 UNIT = "point-RHS/s"
 FALLBACK_HBM = 6650.0
+# oracle sample scale per config: configs 4 and 5 at full size need > 15 min of oracle overset
+# setup alone, so their CPU sample is the same workload at the reduced "test" size (identical
+# per-point arithmetic, smaller meshes)
+ORACLE_SCALE = {1: "full", 2: "full", 3: "full", 4: "test", 5: "test"}
 
 
 def _dist():
@@ -47,6 +52,26 @@ def _peaks():
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return FALLBACK_HBM, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def _fp64_peak():
+    """FP64 DFMA throughput measured on this pool's B200 by scripts/probes/fp64_probe.cu."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "r01", "fp64_probe.json")))
+        return float(d["fp64_dfma_tflops"]), "measured (profiles/r01/fp64_probe.json)"
+    except Exception:
+        return None, "unavailable"
+
+
+def _cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
 
 
 class Clocks:
@@ -113,6 +138,32 @@ def _problem(cid, scale, sr=None):
 _ORACLE = {}
 
 
+def _oracle_problem(cid):
+    return _problem(cid, ORACLE_SCALE[cid])
+
+
+def _oracle_worker(args):
+    cid, n_macro, budget_s = args
+    os.environ["OMP_NUM_THREADS"] = "1"
+    return _oracle_sample(_oracle_problem(cid), n_macro, budget_s)
+
+
+def _oracle_cores(cid, budget_s):
+    """Oracle throughput on 1 host core and on every host core (os.cpu_count() independent
+    single-threaded oracle processes running the same bounded sample at once; the aggregate
+    is the sum of their point-RHS over the longest of their times)."""
+    import multiprocessing as mp
+    n = os.cpu_count() or 1
+    pr1, dt1, n1 = _oracle_sample(_oracle_problem(cid), 1000, budget_s)
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(n) as pool:
+        res = pool.map(_oracle_worker, [(cid, n1, 1e9)] * n)
+    pr_all = sum(r[0] for r in res)
+    dt_all = max(r[1] for r in res)
+    return {"value_1_core": pr1 / dt1, "seconds_1_core": dt1, "macro_steps": n1,
+            "value_all_cores": pr_all / dt_all, "cores_all": n, "seconds_all_cores": dt_all}
+
+
 def _oracle_sample(p, n_macro, budget_s):
     """Oracle (plain numpy fp64, oracle/) timed on host cores: `n_macro` macro steps of the
     same workload from a synthetic full history (rings = m copies of R(q0); the arithmetic
@@ -144,7 +195,7 @@ def run_reference(args):
     ws, rank, _ = _dist()
     if rank != 0:
         return 0
-    p = _problem(args.config, "full")
+    p = _oracle_problem(args.config)
     per_step, tot_pr, tot_t = [], 0, 0.0
     for it in range(args.warmup + args.steps):
         pr, dt, _ = _oracle_sample(p, 1, 1e9)
@@ -161,12 +212,56 @@ def run_reference(args):
         "config": {"workload": p.notes["workload"], "config": args.config,
                    "l2": "n/a (host)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "cpu_model": _cpu_model(),
                          "sample": f"{args.steps} oracle MRAB macro steps of config "
-                                   f"{args.config} at full size from a synthetic history"},
+                                   f"{args.config} at {ORACLE_SCALE[args.config]} size "
+                                   f"({p.notes['workload']}) from a synthetic history"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def _secondary(cid, args, stream, l2_flush):
+    """The cylinder stand-in (config 3) measured beside the contract line: value, step time and
+    the roofline fraction of its dominant kernel (same timing rules)."""
+    import torch
+    from paper_1805_06607_b200 import mrab
+    p = _problem(cid, "full")
+    plan = mrab.Plan(p)
+    ctx = mrab.Context(plan, p.q0)
+    G = len(p.meshes)
+    ctx.step(p.history_m - 1)
+    for _ in range(max(args.warmup, 3)):
+        ctx.step(1)
+    torch.cuda.synchronize()
+    ev0, _, _ = ctx.counters()
+    k_steps = max(args.steps, 20)
+    tot = 0.0
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for k in range(k_steps):
+        l2_flush(k)
+        a0.record(stream)
+        ctx.step(1)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        tot += a0.elapsed_time(a1)
+    ev1, _, _ = ctx.counters()
+    active = [plan.info(g)[1] for g in range(G)]
+    pr = sum((ev1[g] - ev0[g]) * active[g] for g in range(G))
+    per = []
+    for g in range(G):
+        ms, by = ctx.time_kernel(0, g, reps=20, flush_l2=True)
+        per.append((by * (ev1[g] - ev0[g]) / k_steps, ms, by, g))
+    _, ms, by, gdom = max(per)
+    peak, _ = _peaks()
+    ctx.close()
+    return {"config": cid, "workload": p.notes["workload"], "value": pr / (tot * 1e-3),
+            "unit": UNIT, "ms_per_step": tot / k_steps, "steps": k_steps,
+            "roofline": {"kernel": f"k_rhs2d on mesh {gdom} ({p.meshes[gdom].name})",
+                         "achieved": by / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": by / (ms * 1e-3) / 1e9 / peak, "ms_per_launch": ms,
+                         "algorithmic_bytes_per_launch": by}}
 
 
 def run_gpu(args):
@@ -282,7 +377,8 @@ def run_gpu(args):
                        f"k_flux3d + k_rhs3d (RHS in two passes, SAT, AB) on mesh {gdom} ({p.meshes[gdom].name})"),
             "algorithmic_bytes_per_launch": by, "ms_per_launch": ms, "peak_source": peak_src,
             "kernel_ms_per_step_cold": kernel_times, "other_meshes": others,
-            "fp64_pipe_pct_ncu": fp64_pct, "fp64_peak_tflops_measured": 33.7}
+            "fp64_pipe_pct_ncu": fp64_pct, "fp64_peak_tflops": _fp64_peak()[0],
+            "fp64_peak_source": _fp64_peak()[1]}
 
     # ---- end to end through the C ABI with host buffers --------------------------------
     host = [torch.empty(q.shape, dtype=torch.float64).pin_memory() for q in p.q0]
@@ -338,12 +434,23 @@ def run_gpu(args):
                     (S * sum(active))}
         ctx_s.close()
 
+    secondary = None
+    if rank == 0 and args.config != 3 and not args.no_secondary:
+        ctx.close()
+        secondary = _secondary(3, args, stream, l2_flush)
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
-        pr_c, dt_c, n_c = _oracle_sample(p, 3, 20.0)
-        cpu = {"value": pr_c / dt_c, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"{n_c} oracle MRAB macro step(s) of config {args.config} at full size "
-                         f"from a synthetic history ({dt_c:.1f} s, OMP_NUM_THREADS=1)"}
+        oc = _oracle_cores(args.config, 15.0)
+        po = _oracle_problem(args.config)
+        cpu = {"value": oc["value_all_cores"], "unit": UNIT, "cores": oc["cores_all"],
+               "kind": "oracle", "cpu_model": _cpu_model(),
+               "value_1_core": oc["value_1_core"],
+               "sample": f"{oc['macro_steps']} oracle MRAB macro step(s) of config {args.config} at "
+                         f"{ORACLE_SCALE[args.config]} size ({po.notes['workload']}) from a "
+                         f"synthetic history, in each of {oc['cores_all']} independent "
+                         f"single-threaded processes at once ({oc['seconds_all_cores']:.1f} s); "
+                         f"1 process alone: {oc['seconds_1_core']:.1f} s"}
 
     if rank == 0:
         line = {
@@ -359,6 +466,7 @@ def run_gpu(args):
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches * args.steps), "launches_per_step": launches,
             "clocks": clk, "bootstrap_ms": boot_ms, "mrab_vs_srab": srab,
+            "secondary": secondary,
         }
         print(json.dumps(line), flush=True)
     ctx.close()
@@ -373,10 +481,11 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="mrab", choices=["mrab", "reference"])
-    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--sr", type=int, default=None)
     ap.add_argument("--no-srab", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

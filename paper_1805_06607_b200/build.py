@@ -10,8 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libmrab.so")
-SOURCES = ["mrab_api.cu", "kernels.cu", "kernels2d.cu", "kernels2d_tma.cu", "kernels2d_stream.cu", "kernels2d_march.cu",
-           "host_setup.cpp"]
+SOURCES = ["mrab_api.cu", "kernels.cu", "kernels2d.cu", "host_setup.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",

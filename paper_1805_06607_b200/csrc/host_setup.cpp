@@ -4,6 +4,7 @@
 // PAPER.md citations: P:343-394 (AB weights), P:205-208 + P:1526-1528 (SBP 2-4 operator),
 // P:628-637 (metric terms, reading R3), P:227-252 (overset phases, reading R17).
 #include <algorithm>
+#include <cstdlib>
 #include <array>
 #include <cmath>
 #include <cstring>
@@ -12,6 +13,33 @@
 #include "mrab_internal.h"
 
 namespace mrab {
+
+static Options g_opt;
+
+static long env_or(const char* name, long dflt) {
+    const char* e = getenv(name);
+    return e && e[0] ? atol(e) : dflt;
+}
+
+Options read_options() {
+    Options o;
+    o.overlap = (int)env_or("MRAB_OVERLAP", o.overlap);
+    o.bulk_ctas = (int)env_or("MRAB_BULK_CTAS", o.bulk_ctas);
+    o.lean = (int)env_or("MRAB_LEAN", o.lean);
+    o.tile_flags = (int)env_or("MRAB_TILE_FLAGS", o.tile_flags);
+    o.k2d = (int)env_or("MRAB_K2D", o.k2d);
+    if (o.k2d < -2 || o.k2d > 4 || o.k2d == -1) o.k2d = -2;
+    o.small_pts = env_or("MRAB_SMALL_PTS", o.small_pts);
+    o.curv_half = (int)env_or("MRAB_CURV_HALF", o.curv_half);
+    o.pf = (int)env_or("MRAB_PF", o.pf);
+    o.donor_staged = (int)env_or("MRAB_DONOR_STAGED", o.donor_staged);
+    o.interp_box = (int)env_or("MRAB_INTERP_BOX", o.interp_box);
+    o.interp_quad = (int)env_or("MRAB_INTERP_QUAD", o.interp_quad);
+    return o;
+}
+const Options& opts() { return g_opt; }
+void set_options(const Options& o) { g_opt = o; }
+
 
 // ------------------------------------------------------------------------------------
 // SBP 2-4 diagonal-norm first derivative (index space).  Rows by class code.
@@ -891,6 +919,7 @@ static bool build_overset(Plan& P, Error& err) {
 // ------------------------------------------------------------------------------------
 bool build_plan(const mrab_problem* pb, Plan& P, Error& err) {
     init_rows();
+    P.opt = read_options();
     if (!pb || pb->n_meshes < 1 || pb->n_meshes > kMaxMeshes || !pb->meshes || (pb->dim != 2 && pb->dim != 3)) {
         err = {MRAB_E_INVALID, "problem: need 1..8 meshes and dim 2 or 3"};
         return false;

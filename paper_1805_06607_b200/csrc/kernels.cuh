@@ -34,9 +34,6 @@ struct DevMesh {
     // 8^3-tile flag "write the Cartesian viscous fluxes here" (SAT points / donor stencils)
     const double* fh;
     const uint8_t* fvtile;
-    // 2-D viscous, large meshes: per-point SAT viscous-flux scratch [6][npts] of the
-    // row-marching kernel (kernels2d_march.cu); NULL = tile kernel
-    double* satv;
 };
 
 struct Gas {
@@ -85,8 +82,6 @@ bool rhs2d_interior_tile(const int* n, const int* periodic, const uint16_t* cls,
 // per-mesh tile shape (32 x 8 for small curvilinear meshes, else 32 x 16)
 void rhs2d_tile_shape_for(const int* n, int cart, int* tx, int* ty);
 int rhs2d_variant_for(const int* n, int cart);
-// host: whether a 2-D mesh takes the row-marching RHS kernel (kernels2d_march.cu)
-bool rhs2d_march_wanted(const int* n, int viscous);
 
 struct Box {
     int lo[3];

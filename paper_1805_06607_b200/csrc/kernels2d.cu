@@ -1164,12 +1164,7 @@ void launch_donor2d(const RecvTask& rt0, const SrcSets& ss, const MeshTable& mt,
     at[0].val.priority = greatest;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    static int staged = -1;
-    if (staged < 0) {
-        const char* e = getenv("MRAB_DONOR_STAGED");
-        staged = e ? atoi(e) : 1;
-    }
-    if (staged) {
+    if (opts().donor_staged) {
         static bool attr = false;
         if (!attr) {
             cudaFuncSetAttribute(k_donor2d_r<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
@@ -1191,19 +1186,9 @@ template <bool VISC, bool CART, int TY, int MINB, int NTH>
 static void launch_t(const DevMesh& m, const double* Q, const Gas& g, const Epilogue& ep0,
                      const DonorSet& ds, cudaStream_t st) {
     static bool init = false;
-    static int pf = -1;
-    if (pf < 0) {
-        const char* e = getenv("MRAB_PF");
-        pf = e ? atoi(e) : 1;
-    }
     Epilogue ep = ep0;
-    ep.pf = pf;
-    static int lean = -1;
-    if (lean < 0) {
-        const char* e = getenv("MRAB_LEAN");
-        lean = e ? atoi(e) : 1;
-    }
-    ep.lean = lean;
+    ep.pf = opts().pf;
+    ep.lean = opts().lean;
     const size_t bytes = std::max(Geo<VISC, TY, CART>::bytes, GeoL<VISC, TY>::bytes(CART));
     if (!init) {
         cudaFuncSetAttribute(k_rhs2d<VISC, CART, TY, MINB, NTH>,
@@ -1231,30 +1216,18 @@ static void launch_t(const DevMesh& m, const double* Q, const Gas& g, const Epil
     k_rhs2d<VISC, CART, TY, MINB, NTH><<<grid, NTH, bytes, st>>>(m, Q, g, ep, ds);
 }
 
-// tile-shape variant (set once per process from MRAB_K2D, for tuning): 0 = 32x16 tile, 256
-// threads, 2 CTAs/SM (default); 1 = 32x8 / 256 / 2; 2 = 32x8 / 256 / 3; 3 = 32x16 / 512 / 1;
-// 4 = 32x32 / 512 / 1
-static int k2d_variant() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("MRAB_K2D");
-        v = e ? atoi(e) : -2;   // -2: per mesh (rhs2d_variant_for)
-        if (v < -2 || v > 4 || v == -1) v = -2;
-    }
-    return v;
-}
+// tile-shape variant (Options::k2d, for tuning): 0 = 32x16 tile, 256 threads, 2 CTAs/SM
+// (default); 1 = 32x8 / 256 / 2; 2 = 32x8 / 256 / 3; 3 = 32x16 / 512 / 1; 4 = 32x32 / 512 / 1;
+// -2 = per mesh (rhs2d_variant_for)
+static int k2d_variant() { return opts().k2d; }
 
 // per-mesh tile shape: small curvilinear meshes (the config-3 O-grid, 65k points: one wave of
 // latency-bound tiles) take 32 x 8 tiles (twice as many CTAs, shorter per-CTA chains); the
-// rest 32 x 16.  MRAB_K2D=v forces variant v everywhere; MRAB_SMALL_PTS sets the threshold.
+// rest 32 x 16.  Options::k2d forces a variant everywhere; Options::small_pts sets the threshold.
 int rhs2d_variant_for(const int* n, int cart) {
     const int v = k2d_variant();
     if (v >= 0) return v;
-    static const long small = [] {
-        const char* e = getenv("MRAB_SMALL_PTS");
-        return e ? atol(e) : 100000L;
-    }();
-    return (!cart && (long)n[0] * n[1] <= small) ? 1 : 0;
+    return (!cart && (long)n[0] * n[1] <= opts().small_pts) ? 1 : 0;
 }
 
 void rhs2d_tile_shape_for(const int* n, int cart, int* tx, int* ty) {
@@ -1300,23 +1273,14 @@ static void launch_v(const DevMesh& m, const double* Q, const Gas& g, const Epil
         // curvilinear meshes stage their metrics too (one CTA per SM): no register cap
         default: {
             // curvilinear tiles capped at 128 registers so that one fits in half an SM beside a
-            // Cartesian bulk tile in the overlapped schedule (MRAB_CURV_HALF=0: no cap)
-            static const int half = [] {
-                const char* e = getenv("MRAB_CURV_HALF");
-                return e ? atoi(e) : 1;
-            }();
-            if (CART || half) launch_t<VISC, CART, 16, 2, 256>(m, Q, g, ep, ds, st);
+            // Cartesian bulk tile in the overlapped schedule (Options::curv_half = 0: no cap)
+            if (CART || opts().curv_half) launch_t<VISC, CART, 16, 2, 256>(m, Q, g, ep, ds, st);
             else launch_t<VISC, CART, 16, 1, 256>(m, Q, g, ep, ds, st);
             break;
         }
     }
 }
 
-bool launch_rhs2d_stream(const DevMesh& m, const double* Q, const Gas& g, const Epilogue& ep,
-                         cudaStream_t st);
-bool rhs2d_tma_possible(const DevMesh& m, const Epilogue& ep, const double* Q);
-bool launch_rhs2d_tma(const DevMesh& m, const double* Q, const Gas& g, const Epilogue& ep,
-                      cudaStream_t st);
 
 // Lean-only kernel over a list of interior tiles: with the general path compiled out it needs
 // 69.6 KB of shared memory (Cartesian) and 80 registers (three CTAs per SM).  Diagnostic only
@@ -1368,8 +1332,6 @@ static void launch_rhs2d_lean(const DevMesh& m, const double* Q, const Gas& g, c
 #undef MRAB_LEANL
 }
 
-bool launch_rhs2d_march(const DevMesh& m, const double* Q, const Gas& g, const Epilogue& ep,
-                        cudaStream_t st);
 
 void launch_rhs2d(const DevMesh& m, const double* Q, const Gas& g, const Epilogue& ep,
                   const DonorSet& ds, cudaStream_t st) {
@@ -1378,12 +1340,6 @@ void launch_rhs2d(const DevMesh& m, const double* Q, const Gas& g, const Epilogu
         launch_rhs2d_lean(m, Q, g, ep, st);
         return;
     }
-    // row-marching kernel for large viscous meshes (whole-mesh launches)
-    if (launch_rhs2d_march(m, Q, g, ep, st)) return;
-    // persistent TMA-pipelined kernel whenever its layout constraints hold (opt-in)
-    if (rhs2d_tma_possible(m, ep, Q) && launch_rhs2d_tma(m, Q, g, ep, st)) return;
-    // y-streaming tiles for meshes with more than one wave of tiles
-    if (launch_rhs2d_stream(m, Q, g, ep, st)) return;
     if (g.viscous) {
         if (m.cart) launch_v<true, true>(m, Q, g, ep, ds, st);
         else launch_v<true, false>(m, Q, g, ep, ds, st);

@@ -67,7 +67,6 @@ struct MeshDev {
     double* fvhat = nullptr;      // [S][d(d+1)][R]
     int32_t* tiles = nullptr;     // 2-D: critical tiles (cover the donor box) then the bulk
     int32_t* tlist = nullptr;     // 2-D: all tiles, non-interior first (bit 31 = interior)
-    double* satv = nullptr;       // [6][N] SAT viscous-flux scratch of the row-marching kernel
     int ncrit = 0, nbulk = 0;
     int ngen = 0;                 // non-interior tiles at the head of tlist
     DevMesh dm{};
@@ -218,10 +217,6 @@ static size_t plan_bytes(const Plan& P, bool dry, mrab_ctx* ctx, Bump* bump, boo
             if (D) {
                 D->tiles = (int32_t*)a;
                 D->tlist = (int32_t*)b;
-            }
-            if (rhs2d_march_wanted(m.n, P.viscous)) {
-                void* e = take((size_t)6 * N * sizeof(double));
-                if (D) D->satv = (double*)e;
             }
         }
     }
@@ -878,6 +873,7 @@ mrab_status mrab_plan_get_metrics(const mrab_plan* plan, int mesh, double* jinv,
 
 size_t mrab_workspace_bytes(const mrab_plan* plan) {
     if (!plan) return 0;
+    set_options(plan->P->opt);
     bool ok = true;
     return plan_bytes(*plan->P, true, nullptr, nullptr, &ok);
 }
@@ -890,6 +886,7 @@ mrab_status mrab_create(const mrab_plan* plan, const double* const* q0, void* d_
     if (!d_workspace || ((uintptr_t)d_workspace & 255)) return fail(MRAB_E_WORKSPACE, "workspace NULL or not 256-byte aligned");
     const Plan& P = *plan->P;
     if (ws_bytes < mrab_workspace_bytes(plan)) return fail(MRAB_E_WORKSPACE, "workspace too small");
+    set_options(P.opt);
     std::unique_ptr<mrab_ctx> c(new mrab_ctx());
     c->P = plan->P;
     c->user = (cudaStream_t)stream;
@@ -915,19 +912,11 @@ mrab_status mrab_create(const mrab_plan* plan, const double* const* q0, void* d_
         // bulk tiles of split meshes run on their own streams, concurrent with the critical tiles
         for (int g = 0; g < (int)P.meshes.size(); ++g)
             CK(cudaStreamCreateWithPriority(&c->side[P.meshes.size() + 1 + g], cudaStreamNonBlocking, least));
-        const char* ov = getenv("MRAB_OVERLAP");
         // critical/bulk split of slow meshes with per-node launch priorities (on by default;
-        // config 3: 0.1205 -> 0.110 ms per macro step; MRAB_OVERLAP=0 disables)
-        c->overlap = !(ov && ov[0] == '0');
-        // the bulk launch walks its tiles with one CTA per SM by default, so each SM keeps
-        // room for a CTA of the fast meshes' substeps
-        int dev = 0, nsm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        // bulk launches take one CTA per tile by default (MRAB_BULK_CTAS=k: k persistent CTAs)
-        const char* bc = getenv("MRAB_BULK_CTAS");
-        c->bulk_ctas = bc ? atoi(bc) : 0;
-        (void)nsm;
+        // config 3: 0.1205 -> 0.110 ms per macro step; Options::overlap = 0 disables)
+        c->overlap = P.opt.overlap != 0;
+        // bulk launches take one CTA per tile by default (Options::bulk_ctas = k: k persistent CTAs)
+        c->bulk_ctas = P.opt.bulk_ctas;
     }
     CK(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
@@ -999,11 +988,7 @@ mrab_status mrab_create(const mrab_plan* plan, const double* const* q0, void* d_
             CK(cudaMemcpy(D.rdonor, m.rdonor.data(), R * sizeof(int32_t), cudaMemcpyHostToDevice));
             CK(cudaMemcpy(D.rbase, m.rbase.data(), R * 3 * sizeof(int32_t), cudaMemcpyHostToDevice));
             CK(cudaMemcpy(D.rw, m.rw.data(), R * 12 * sizeof(double), cudaMemcpyHostToDevice));
-            static const int boxg = [] {
-                const char* e = getenv("MRAB_INTERP_BOX");
-                return e ? atoi(e) : 1;
-            }();
-            if (d == 3 && boxg) {
+            if (d == 3 && P.opt.interp_box) {
                 std::vector<int32_t> order;
                 const std::vector<int32_t> info = interp3_groups((int64_t)R, m.rdonor.data(), m.rbase.data(), order);
                 CK(cudaMemcpy(D.gorder, order.data(), R * sizeof(int32_t), cudaMemcpyHostToDevice));
@@ -1039,10 +1024,7 @@ mrab_status mrab_create(const mrab_plan* plan, const double* const* q0, void* d_
             rhs2d_tile_shape_for(m.n, m.cartesian ? 1 : 0, &tx, &ty);
             const int ntx = (m.n[0] + tx - 1) / tx, nty = (m.n[1] + ty - 1) / ty;
             std::vector<int32_t> crit, bulk, slow, fastl;
-            static const bool tag = [] {
-                const char* e = getenv("MRAB_TILE_FLAGS");
-                return !(e && e[0] == '0');
-            }();
+            const bool tag = P.opt.tile_flags != 0;
             for (int by = 0; by < nty; ++by)
                 for (int bx = 0; bx < ntx; ++bx) {
                     const bool interior = tag && rhs2d_interior_tile(m.n, m.periodic, m.cls.data(), P.viscous, bx, by, m.cartesian ? 1 : 0);
@@ -1063,10 +1045,6 @@ mrab_status mrab_create(const mrab_plan* plan, const double* const* q0, void* d_
             CK(cudaMemcpy(D.tlist, slow.data(), slow.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
             dm.tlist = D.tlist;
             dm.ntl = (int)slow.size();
-            if (D.satv) {
-                CK(cudaMemsetAsync(D.satv, 0, (size_t)6 * N * sizeof(double), c->st));
-                dm.satv = D.satv;
-            }
         }
         dm.nrecv = (int64_t)R;
         c->book.head[g] = P.history_m - 1;   // empty ring: the first push goes to slot 0
@@ -1105,9 +1083,47 @@ void mrab_destroy(mrab_ctx* c) {
     delete c;
 }
 
+// Capture every phase graph of the MRAB macro step (period = ring x double-buffer phases),
+// starting from the current bookkeeping; the bookkeeping is restored afterwards, so the graphs
+// are replayed in order by mrab_step.  Called once the bootstrap is done, so that no capture
+// or instantiation lands inside a later (timed) macro step.
+static mrab_status ensure_graphs(mrab_ctx* c) {
+    if (c->graphs[0]) return MRAB_OK;
+    const Book book0 = c->book;
+    const std::vector<int64_t> ev_start = c->evals;
+    for (int phase = 0; phase < c->period; ++phase) {
+        std::vector<int64_t> ev0 = c->evals;
+        c->launch_counter = 0;
+        CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+        issue_macro_step(c);
+        cudaGraph_t graph;
+        CK(cudaStreamEndCapture(c->st, &graph));
+        CK(cudaGraphInstantiate(&c->graphs[phase], graph, cudaGraphInstantiateFlagUseNodePriority));
+        CK(cudaGraphDestroy(graph));
+        if (phase == 0) c->launches_last = c->launch_counter;
+        c->book_after[phase] = c->book;
+        c->evals_per_phase[phase].resize(c->evals.size());
+        for (size_t g = 0; g < c->evals.size(); ++g) c->evals_per_phase[phase][g] = c->evals[g] - ev0[g];
+    }
+    c->book = book0;
+    c->evals = ev_start;
+    // upload the executable graphs now (the first launch would otherwise do it)
+    for (int phase = 0; phase < c->period; ++phase) CK(cudaGraphUpload(c->graphs[phase], c->st));
+    return MRAB_OK;
+}
+
+// the caller's stream is joined into the context stream (work queued on it before this call,
+// e.g. a torch kernel still writing a device source buffer, completes first)
+static mrab_status join_user(mrab_ctx* c) {
+    CK(cudaEventRecord(c->ev_in, c->user));
+    CK(cudaStreamWaitEvent(c->st, c->ev_in, 0));
+    return MRAB_OK;
+}
+
 mrab_status mrab_step(mrab_ctx* c, int n_macro) {
     if (!c || n_macro < 0) return fail(MRAB_E_INVALID, "bad ctx / n_macro");
     const Plan& P = *c->P;
+    set_options(P.opt);
     CK(cudaEventRecord(c->ev_in, c->user));
     CK(cudaStreamWaitEvent(c->st, c->ev_in, 0));
     const int64_t nboot_macro = P.history_m - 1;
@@ -1118,28 +1134,17 @@ mrab_status mrab_step(mrab_ctx* c, int n_macro) {
         } else {
             const int64_t k = c->macro - nboot_macro;
             const int phase = (int)(k % c->period);
-            if (!c->graphs[phase]) {
-                const Book before = c->book;
-                std::vector<int64_t> ev0 = c->evals;
-                c->launch_counter = 0;
-                CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
-                issue_macro_step(c);
-                cudaGraph_t graph;
-                CK(cudaStreamEndCapture(c->st, &graph));
-                CK(cudaGraphInstantiate(&c->graphs[phase], graph, cudaGraphInstantiateFlagUseNodePriority));
-                CK(cudaGraphDestroy(graph));
-                c->launches_last = c->launch_counter;
-                c->book_after[phase] = c->book;
-                c->evals_per_phase[phase].resize(c->evals.size());
-                for (size_t g = 0; g < c->evals.size(); ++g) c->evals_per_phase[phase][g] = c->evals[g] - ev0[g];
-                (void)before;
-            } else {
-                c->book = c->book_after[phase];
-                for (size_t g = 0; g < c->evals.size(); ++g) c->evals[g] += c->evals_per_phase[phase][g];
-            }
+            mrab_status st = ensure_graphs(c);
+            if (st != MRAB_OK) return st;
+            c->book = c->book_after[phase];
+            for (size_t g = 0; g < c->evals.size(); ++g) c->evals[g] += c->evals_per_phase[phase][g];
             CK(cudaGraphLaunch(c->graphs[phase], c->st));
         }
         c->macro++;
+        if (c->macro == nboot_macro) {
+            mrab_status st = ensure_graphs(c);
+            if (st != MRAB_OK) return st;
+        }
     }
     CK(cudaGetLastError());
     CK(cudaEventRecord(c->ev_out, c->st));
@@ -1156,6 +1161,7 @@ static const double* current_state(mrab_ctx* c, int g) {
 mrab_status mrab_get_state(mrab_ctx* c, int mesh, double* dst, double* t) {
     if (!c || mesh < 0 || mesh >= (int)c->md.size() || !dst) return fail(MRAB_E_INVALID, "bad arguments");
     const Plan& P = *c->P;
+    if (join_user(c) != MRAB_OK) return MRAB_E_CUDA;
     CK(cudaStreamSynchronize(c->st));
     const size_t n = (size_t)P.nc * P.meshes[mesh].npts;
     const double* src = current_state(c, mesh);
@@ -1175,6 +1181,7 @@ mrab_status mrab_get_state(mrab_ctx* c, int mesh, double* dst, double* t) {
 mrab_status mrab_set_state(mrab_ctx* c, int mesh, const double* src) {
     if (!c || mesh < 0 || mesh >= (int)c->md.size() || !src) return fail(MRAB_E_INVALID, "bad arguments");
     const Plan& P = *c->P;
+    if (join_user(c) != MRAB_OK) return MRAB_E_CUDA;
     CK(cudaStreamSynchronize(c->st));
     const size_t bytes = (size_t)P.nc * P.meshes[mesh].npts * sizeof(double);
     CK(cudaMemcpyAsync((double*)current_state(c, mesh), src, bytes, cudaMemcpyDefault, c->st));
@@ -1202,6 +1209,7 @@ mrab_status mrab_get_history(mrab_ctx* c, int mesh, int k, double* dst) {
     mrab_status st = history_slot(c, mesh, k, &src);
     if (st != MRAB_OK) return st;
     const size_t bytes = (size_t)c->P->nc * c->P->meshes[mesh].npts * sizeof(double);
+    if (join_user(c) != MRAB_OK) return MRAB_E_CUDA;
     CK(cudaStreamSynchronize(c->st));
     CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->st));
     CK(cudaStreamSynchronize(c->st));
@@ -1214,6 +1222,7 @@ mrab_status mrab_set_history(mrab_ctx* c, int mesh, int k, const double* src) {
     mrab_status st = history_slot(c, mesh, k, &dst);
     if (st != MRAB_OK) return st;
     const size_t bytes = (size_t)c->P->nc * c->P->meshes[mesh].npts * sizeof(double);
+    if (join_user(c) != MRAB_OK) return MRAB_E_CUDA;
     CK(cudaStreamSynchronize(c->st));
     CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->st));
     CK(cudaStreamSynchronize(c->st));
@@ -1224,6 +1233,8 @@ mrab_status mrab_rhs(mrab_ctx* c, const double* const* q, double* const* rhs_out
     if (!c || !q || !rhs_out) return fail(MRAB_E_INVALID, "bad arguments");
     const Plan& P = *c->P;
     const int G = (int)P.meshes.size();
+    set_options(P.opt);
+    if (join_user(c) != MRAB_OK) return MRAB_E_CUDA;
     CK(cudaStreamSynchronize(c->st));
     std::vector<const double*> state_of(G);
     for (int g = 0; g < G; ++g) {
@@ -1282,10 +1293,15 @@ mrab_status mrab_time_kernel(mrab_ctx* c, int kernel, int mesh, int reps, int fl
     if (!c || mesh < 0 || mesh >= (int)c->md.size() || reps < 1 || kernel < 0 || kernel > 5)
         return fail(MRAB_E_INVALID, "bad arguments");
     const Plan& P = *c->P;
+    set_options(P.opt);
     const MeshPlan& mp = P.meshes[mesh];
     MeshDev& D = c->md[mesh];
     const int m = P.history_m, nc = P.nc, d = P.dim;
     const double N = (double)mp.npts;
+    // the 2-D diagnostics (3-5) replay the interior-tile lists; the lean-only kernel (3) is
+    // compiled for 32 x 16 tiles only (variant 0)
+    if (kernel >= 3 && (d != 2 || (kernel == 3 && rhs2d_variant_for(mp.n, mp.cartesian ? 1 : 0) != 0)))
+        return fail(MRAB_E_INVALID, "kernel 3-5 are 2-D diagnostics; 3 needs the 32x16 tile variant");
     CK(cudaStreamSynchronize(c->st));
     void* flush = nullptr;
     const size_t fbytes = (size_t)256 << 20;

@@ -17,6 +17,27 @@ constexpr int kFar = 1 << 30;
 // stencil class codes, 4 bits per direction (reading R2: segment closures)
 enum : int { CLS_HOLE = 0, CLS_INT = 1, CLS_L0 = 2, CLS_R0 = 6 };
 
+// Tuning / diagnostic switches of the library.  Defaults are the
+// measured-best paths; the hot path reads no environment itself: the MRAB_* variables are read
+// in one place (read_options, at mrab_plan_create), stored in the plan, and installed as the
+// current options by every entry point that launches kernels (set_options).
+struct Options {
+    int overlap = 1;          // MRAB_OVERLAP: critical/bulk split of slow meshes on two streams
+    int bulk_ctas = 0;        // MRAB_BULK_CTAS: >0 = persistent CTAs for bulk launches
+    int lean = 1;             // MRAB_LEAN: 2-D interior tiles take the lean path
+    int tile_flags = 1;       // MRAB_TILE_FLAGS: 0 = no tile flagged interior
+    int k2d = -2;             // MRAB_K2D: force a 2-D tile variant (-2 = per mesh)
+    long small_pts = 100000;  // MRAB_SMALL_PTS: curvilinear meshes up to this size use 32x8 tiles
+    int curv_half = 1;        // MRAB_CURV_HALF: curvilinear 2-D tiles capped at 128 registers
+    int pf = 1;               // MRAB_PF: L2 prefetch of the general tile's epilogue rows
+    int donor_staged = 1;     // MRAB_DONOR_STAGED: region-staged 2-D donor gather
+    int interp_box = 1;       // MRAB_INTERP_BOX: 3-D gather staged per donor box
+    int interp_quad = 1;      // MRAB_INTERP_QUAD: four lanes per receiver (per-receiver 3-D gather)
+};
+Options read_options();
+const Options& opts();
+void set_options(const Options& o);
+
 struct Error {
     mrab_status st;
     std::string msg;
@@ -67,6 +88,7 @@ struct Plan {
     std::vector<std::vector<std::vector<double>>> coef;
     // donors[g][h] = 1 if mesh h has receivers whose donor is mesh g
     std::vector<std::vector<int>> donor_of;
+    Options opt;                            // switches read at plan creation
 };
 
 // host setup (host_setup.cpp)

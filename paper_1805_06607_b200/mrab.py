@@ -100,6 +100,22 @@ def _dptr(a: np.ndarray):
     return a.ctypes.data_as(C.POINTER(C.c_double))
 
 
+def _state_ptr(buf, nelem, what):
+    """Device or host address of a dense fp64 state buffer of exactly `nelem` elements (numpy
+    array or torch tensor, C-contiguous); anything else raises before the library copies."""
+    if isinstance(buf, np.ndarray):
+        ok = buf.dtype == np.float64 and buf.flags.c_contiguous and buf.size == nelem
+        ptr = buf.ctypes.data
+    else:
+        import torch
+        ok = (isinstance(buf, torch.Tensor) and buf.dtype == torch.float64
+              and buf.is_contiguous() and buf.numel() == nelem)
+        ptr = buf.data_ptr() if ok else 0
+    if not ok:
+        raise MrabError(1, f"{what}: need a C-contiguous float64 buffer of {nelem} elements")
+    return C.c_void_p(ptr)
+
+
 def ab_weights(nodes, n, a, b):
     nodes = np.ascontiguousarray(nodes, dtype=np.float64)
     out = np.zeros(len(nodes))
@@ -223,31 +239,29 @@ class Context:
         shp = (self.plan.nc,) + tuple(reversed(self.plan.shapes[g]))
         if out is None:
             out = np.zeros(shp)
-        ptr = out.ctypes.data if isinstance(out, np.ndarray) else out.data_ptr()
         t = C.c_double()
-        _check(lib().mrab_get_state(self.h, g, C.c_void_p(ptr), C.byref(t)))
+        _check(lib().mrab_get_state(self.h, g, _state_ptr(out, self._nelem(g), "get_state"),
+                                    C.byref(t)))
         return out, t.value
 
+    def _nelem(self, g):
+        return self.plan.nc * int(np.prod(self.plan.shapes[g]))
+
     def set_state(self, g, src):
-        ptr = src.ctypes.data if isinstance(src, np.ndarray) else src.data_ptr()
-        if isinstance(src, np.ndarray):
-            assert src.dtype == np.float64 and src.flags.c_contiguous
-        _check(lib().mrab_set_state(self.h, g, C.c_void_p(ptr)))
+        _check(lib().mrab_set_state(self.h, g, _state_ptr(src, self._nelem(g), "set_state")))
 
     def get_history(self, g, k, out=None):
         """Committed RHS history entry k (0 = oldest of m-1) of mesh g at the macro boundary."""
         shp = (self.plan.nc,) + tuple(reversed(self.plan.shapes[g]))
         if out is None:
             out = np.zeros(shp)
-        ptr = out.ctypes.data if isinstance(out, np.ndarray) else out.data_ptr()
-        _check(lib().mrab_get_history(self.h, g, int(k), C.c_void_p(ptr)))
+        _check(lib().mrab_get_history(self.h, g, int(k),
+                                      _state_ptr(out, self._nelem(g), "get_history")))
         return out
 
     def set_history(self, g, k, src):
-        if isinstance(src, np.ndarray):
-            assert src.dtype == np.float64 and src.flags.c_contiguous
-        ptr = src.ctypes.data if isinstance(src, np.ndarray) else src.data_ptr()
-        _check(lib().mrab_set_history(self.h, g, int(k), C.c_void_p(ptr)))
+        _check(lib().mrab_set_history(self.h, g, int(k),
+                                      _state_ptr(src, self._nelem(g), "set_history")))
 
     def rhs(self, states):
         qs = [np.ascontiguousarray(q, dtype=np.float64) for q in states]
