@@ -97,12 +97,37 @@ def test_ab_order_scalar(n, m):
     assert abs(eoc - n) < 0.3, eoc
 
 
+def _single_rate_vec(A, y0, h, nboot, nab):
+    """Hand-written coupled single-rate AB3 (vector y' = A y): nboot Heun RK3 steps at h
+    recording the stage-1 RHS of the last two of them, then AB3 at h."""
+    A = np.asarray(A, dtype=np.float64)
+    y = np.asarray(y0, dtype=np.float64)
+    hist = []
+    for k in range(nboot):
+        k1 = A @ y
+        k2 = A @ (y + h / 3 * k1)
+        k3 = A @ (y + 2 * h / 3 * k2)
+        if nboot - k <= 2:
+            hist.append(k1)
+        y = y + h * (k1 / 4 + 3 * k3 / 4)
+    hist.append(A @ y)
+    al = (5 / 12, -16 / 12, 23 / 12)
+    for _ in range(nab):
+        y = y + h * sum(a * f for a, f in zip(al, hist))
+        hist = hist[1:] + [A @ y]
+    return y
+
+
 def test_sr1_equals_srab_and_counts():
+    """MRAB with every step ratio 1 is single-rate AB: the oracle's MRAB on a coupled
+    2-component system against an independent hand-written coupled AB3 driver."""
     A = [[-1.0, 0.1], [0.1, -0.05]]
-    s = _Lin(A, [1.0, 0.5], 3, 3, 0.01)
-    a, _ = _run(s, [1, 1], 0.5)
-    b, _ = _run(s, [1, 1], 0.5)
-    assert a.base[0][0] == b.base[0][0] and a.base[1][0] == b.base[1][0]
+    h, nmac = 0.01, 40
+    s = _Lin(A, [1.0, 0.5], 3, 3, h)
+    mr = timeint.MRAB(s, steps=[1, 1], rhs_fn=s.rhs)
+    mr.run(nmac)
+    ref = _single_rate_vec(A, [1.0, 0.5], h, 2, nmac)
+    assert abs(mr.base[0][0] - ref[0]) <= 1e-14 and abs(mr.base[1][0] - ref[1]) <= 1e-14
     # counts: SR fast + 1 slow per macro step after the bootstrap (P:607-609)
     for SR in (2, 3, 4):
         s = _Lin(A, [1.0, 0.5], 3, 3, 0.01)
