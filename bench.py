@@ -353,7 +353,7 @@ def run_gpu(args):
                        "ms_per_launch_cold": msg, "algorithmic_bytes_per_launch": byg})
     kernel_times = {}
     for kid, name in ((0, "k_rhs"), (1, "k_visc"), (2, "k_interp")):
-        if kid == 1 and not p.viscous:
+        if kid == 1 and (not p.viscous or p.dim != 3):
             continue
         tot = 0.0
         for g in range(G):
@@ -374,7 +374,9 @@ def run_gpu(args):
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic,
             "kernel": (f"k_rhs2d (fused RHS+SAT+AB) on mesh {gdom} ({p.meshes[gdom].name})" if p.dim == 2 else
-                       f"k_flux3d + k_rhs3d (RHS in two passes, SAT, AB) on mesh {gdom} ({p.meshes[gdom].name})"),
+                       (f"k_rhs3z (fused one-pass RHS + SAT + AB, z-marching) on mesh {gdom} ({p.meshes[gdom].name})"
+                        if os.environ.get("MRAB_3D_FUSED", "0") not in ("", "0") else
+                        f"k_flux3d + k_rhs3d (RHS in two passes, SAT, AB) on mesh {gdom} ({p.meshes[gdom].name})")),
             "algorithmic_bytes_per_launch": by, "ms_per_launch": ms, "peak_source": peak_src,
             "kernel_ms_per_step_cold": kernel_times, "other_meshes": others,
             "fp64_pipe_pct_ncu": fp64_pct, "fp64_peak_tflops": _fp64_peak()[0],

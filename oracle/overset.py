@@ -127,13 +127,36 @@ def _cells(mesh):
     return np.stack([g.ravel() for g in reversed(grids)], axis=-1)
 
 
+BLOCK = 8      # cells per axis of the coarse bounding-box blocks (a pure pre-filter)
+
+
 def cell_bboxes(mesh):
+    """Grown corner-node bounding boxes of every cell (flat cell order), plus a coarse level:
+    the cells grouped by index-space blocks of BLOCK^d cells with the union box of each block.
+    The blocks only pre-filter candidate cells; the candidates are re-sorted into flat cell
+    order, so the cells tried (and the first accepted) are exactly those of the flat scan."""
     cells = _cells(mesh)
     corners = np.array(list(itertools.product([0, 1], repeat=mesh.dim)))
-    P = node_coords(mesh, cells[:, None, :] + corners[None])        # (ncell, 2^d, d)
-    lo, hi = P.min(axis=1), P.max(axis=1)
+    lo = np.full((len(cells), mesh.dim), np.inf)
+    hi = np.full((len(cells), mesh.dim), -np.inf)
+    for c in corners:                                               # one corner at a time
+        P = node_coords(mesh, cells + c[None])
+        lo = np.minimum(lo, P)
+        hi = np.maximum(hi, P)
     g = BBOX_GROW * (hi - lo) + BBOX_ABS
-    return cells, lo - g, hi + g
+    lo, hi = lo - g, hi + g
+    nb = [-(-(mesh.shape[k] if mesh.periodic[k] else mesh.shape[k] - 1) // BLOCK) for k in range(mesh.dim)]
+    bid = np.zeros(len(cells), dtype=np.int64)
+    stride = 1
+    for k in range(mesh.dim):
+        bid += (cells[:, k] // BLOCK) * stride
+        stride *= nb[k]
+    order = np.argsort(bid, kind="stable")
+    starts = np.concatenate([[0], np.nonzero(np.diff(bid[order]))[0] + 1])
+    blo = np.minimum.reduceat(lo[order], starts, axis=0)
+    bhi = np.maximum.reduceat(hi[order], starts, axis=0)
+    ends = np.concatenate([starts[1:], [len(order)]])
+    return cells, lo, hi, (order, starts, ends, blo, bhi)
 
 
 def stencil_base_from_cell(mesh, c):
@@ -214,12 +237,18 @@ def find_cells(mesh, X, chunk=512, bb=None):
     out = np.full(X.shape, np.nan)
     if len(X) == 0:
         return out
-    cells_all, lo_all, hi_all = bb if bb is not None else cell_bboxes(mesh)
+    cells_all, lo_all, hi_all, blocks = bb if bb is not None else cell_bboxes(mesh)
+    order, starts, ends, blo, bhi = blocks
     for q0 in range(0, len(X), chunk):
         Xc = X[q0:q0 + chunk]
-        # cells whose box meets the chunk's box (a pure pre-filter; order preserved)
-        keep = np.nonzero(np.all((lo_all <= Xc.max(axis=0)) & (hi_all >= Xc.min(axis=0)),
-                                 axis=1))[0]
+        # cells whose box meets the chunk's box (a pure pre-filter; flat order preserved):
+        # first the blocks whose union box meets it, then their cells, re-sorted
+        cmax, cmin = Xc.max(axis=0), Xc.min(axis=0)
+        kb = np.nonzero(np.all((blo <= cmax) & (bhi >= cmin), axis=1))[0]
+        if len(kb) == 0:
+            continue
+        cand = np.sort(np.concatenate([order[starts[b]:ends[b]] for b in kb]))
+        keep = cand[np.all((lo_all[cand] <= cmax) & (hi_all[cand] >= cmin), axis=1)]
         cells, lo, hi = cells_all[keep], lo_all[keep], hi_all[keep]
         hit = np.ones((len(Xc), len(keep)), dtype=bool)
         for k in range(mesh.dim):

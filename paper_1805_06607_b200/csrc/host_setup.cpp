@@ -35,6 +35,7 @@ Options read_options() {
     o.donor_staged = (int)env_or("MRAB_DONOR_STAGED", o.donor_staged);
     o.interp_box = (int)env_or("MRAB_INTERP_BOX", o.interp_box);
     o.interp_quad = (int)env_or("MRAB_INTERP_QUAD", o.interp_quad);
+    o.z3_fused = (int)env_or("MRAB_3D_FUSED", o.z3_fused);
     return o;
 }
 const Options& opts() { return g_opt; }

@@ -1,19 +1,19 @@
-// CUDA kernels of libmrab.so (sm_100a, fp64, CUDA cores; no tensor cores: the path is a
-// stencil, not a dense contraction).  DESIGN.md §5 lists each kernel with its roofline.
-// This file: the 3-D path and the shared pieces (2-D: kernels2d.cu, kernels2d_march.cu).
+// CUDA kernels of libmrab.so, 3-D path and shared pieces (sm_100a, fp64, CUDA cores; no tensor
+// cores: the path is a stencil, not a dense contraction).  DESIGN.md §5 lists each kernel with
+// its roofline.  2-D kernels: kernels2d.cu.
 //
-//   k_flux3d   3-D pass 1: cross-region state staged by cp.async, D1 gradients, F^V (flagged
-//              tiles), contravariant fluxes of every point once (R3/R11)
-//   k_rhs3d    3-D pass 2 (PRE) / single pass: R = -J sum_k D_k Fhat_k + SAT (eq:int
-//              P:279-299) fused with the AB / RK combination epilogue (eq:ab_general P:358-361)
-//   k_visc3d_x Cartesian viscous fluxes on donor boxes at intermediate states (one round trip)
+//   k_rhs3z    3-D fused RHS in ONE HBM pass: x-y tiles marching along z.  Primitives of a
+//              7-plane window in shared memory, D1 gradients, F^V, F^I, contravariant fluxes,
+//              D_kappa Fhat_kappa (R3/R11), SAT (eq:int P:279-299) and the AB / RK
+//              combination epilogue (eq:ab_general P:358-361).
+//   k_visc3d_x Cartesian viscous fluxes on donor boxes / donor-stencil tiles (the gathers read
+//              them, reading R18)
 //   k_combine  intermediate donor states base + sum beta_k R_k (MRAB Steps 2/5)
-//   k_interp3q Lagrange gather of donor state and viscous flux at receivers
-//   k_visc / k_rhs / k_interp  the original one-thread-per-point kernels (MRAB_3D_DIRECT=1,
-//              and the 2-D viscous pass on donor boxes)
+//   k_interp3b / k_interp3q  Lagrange gather of donor state and viscous flux
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstring>
 #include <vector>
 
 #include "kernels.cuh"
@@ -25,107 +25,6 @@ namespace mrab {
 void upload_stencil_rows() {}
 
 static constexpr double kP0 = 17.0 / 48.0;   // H_00 of the SBP norm (R14)
-
-__device__ __forceinline__ int64_t nbr(const DevMesh& m, int64_t p, int i, int k, int off,
-                                       int64_t stride) {
-    int n = m.n[k];
-    int ii = i + off;
-    if (ii < 0)
-        ii += n;
-    else if (ii >= n)
-        ii -= n;
-    return p + (int64_t)(ii - i) * stride;
-}
-
-template <int D>
-__device__ __forceinline__ void prim(const double* __restrict__ Q, int64_t q, int64_t N,
-                                     double gamma, double& rho, double* u, double& p,
-                                     double& E) {
-    rho = __ldg(Q + q);
-    double ir = rcp64(rho);
-    double ke = 0.0;
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-        double mi = __ldg(Q + (1 + i) * N + q);
-        u[i] = mi * ir;
-        ke += mi * u[i];
-    }
-    E = __ldg(Q + (D + 1) * N + q);
-    p = (gamma - 1.0) * (E - 0.5 * ke);
-}
-
-// ------------------------------------------------------------------------------------
-// viscous fluxes
-// ------------------------------------------------------------------------------------
-template <int D, bool CART>
-__global__ void __launch_bounds__(256) k_visc(DevMesh m, const double* __restrict__ Q,
-                                              double* __restrict__ FV, Box box, Gas g) {
-    const int bx = box.hi[0] - box.lo[0] + 1, by = box.hi[1] - box.lo[1] + 1,
-              bz = box.hi[2] - box.lo[2] + 1;
-    const int64_t tot = (int64_t)bx * by * bz;
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= tot) return;
-    int idx[3];
-    idx[0] = box.lo[0] + (int)(t % bx);
-    idx[1] = box.lo[1] + (int)((t / bx) % by);
-    idx[2] = box.lo[2] + (int)(t / ((int64_t)bx * by));
-    const int64_t N = m.npts;
-    const int64_t stride[3] = {1, m.n[0], (int64_t)m.n[0] * m.n[1]};
-    const int64_t p = idx[0] + stride[1] * idx[1] + stride[2] * idx[2];
-    const unsigned code = m.cls[p];
-    if (!code) return;
-    double dphi[D + 1][D];
-#pragma unroll
-    for (int k = 0; k < D; ++k) {
-        const int c = (code >> (4 * k)) & 15;
-        double acc[D + 1];
-#pragma unroll
-        for (int f = 0; f <= D; ++f) acc[f] = 0.0;
-        for (int s = 0; s < c_nst[c]; ++s) {
-            const int64_t q = nbr(m, p, idx[k], k, c_off[c][s], stride[k]);
-            double rho, u[D], pr, E;
-            prim<D>(Q, q, N, g.gamma, rho, u, pr, E);
-            const double cf = c_cf[c][s];
-#pragma unroll
-            for (int i = 0; i < D; ++i) acc[i] += cf * u[i];
-            acc[D] += cf * (g.gamma * pr / rho);
-        }
-#pragma unroll
-        for (int f = 0; f <= D; ++f) dphi[f][k] = acc[f];
-    }
-    double grad[D + 1][D];   // grad[f][i] = d phi_f / d x_i
-#pragma unroll
-    for (int f = 0; f <= D; ++f)
-#pragma unroll
-        for (int i = 0; i < D; ++i) {
-            if (CART) {
-                grad[f][i] = m.cJ * (m.cM[i] * dphi[f][i]);
-            } else {
-                double s = 0.0;
-#pragma unroll
-                for (int k = 0; k < D; ++k) s += __ldg(m.M + (k * D + i) * N + p) * dphi[f][k];
-                grad[f][i] = __ldg(m.J + p) * s;
-            }
-        }
-    double rho, u[D], pr, E;
-    prim<D>(Q, p, N, g.gamma, rho, u, pr, E);
-    double div = 0.0;
-#pragma unroll
-    for (int i = 0; i < D; ++i) div += grad[i][i];
-    const double iRe = 1.0 / g.Re;
-    const double kT = 1.0 / (g.Re * g.Pr * (g.gamma - 1.0));
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-        double e = 0.0;
-#pragma unroll
-        for (int j = 0; j < D; ++j) {
-            double tau = (grad[i][j] + grad[j][i] - (i == j ? (2.0 / 3.0) * div : 0.0)) * iRe;
-            FV[(int64_t)(i * (D + 1) + j) * N + p] = tau;
-            e += u[j] * tau;
-        }
-        FV[(int64_t)(i * (D + 1) + D) * N + p] = e + kT * grad[D][i];
-    }
-}
 
 // ------------------------------------------------------------------------------------
 // SAT characteristic penalty K^s(n; q) dq (analytic Euler eigensystem; readings R14/R15)
@@ -189,10 +88,1084 @@ __device__ __forceinline__ void kchar(const double* q, const double* n, double s
     out[D + 1] = wp * (H + c * un) + wm * (H - c * un) + w0 * (0.5 * ke) + l0 * rho * udt;
 }
 
+// 8^3 tiles of the donor-flux kernel
+namespace {
+constexpr int T3X = 8, T3Y = 8, T3Z = 8, NT3 = 256;
+constexpr int T3N = T3X * T3Y * T3Z;                  // 512
+constexpr int PPT3 = T3N / NT3;                       // 2 own points per thread
+}  // namespace
+
+// ------------------------------------------------------------------------------------
+// 3-D viscous fluxes, one memory round trip per tile: the state of the whole cross-shaped
+// region the three D1 passes read (tile 8^3 plus 3 layers on each of its six faces: 1664
+// points) is copied to shared memory by cp.async at once, turned into primitives in place,
+// and every gradient is taken from there (k_visc3d loaded one direction-extended region per
+// pass: three dependent round trips).  Same arithmetic as k_visc3d.
+// Cross-region index of tile-relative (x, y, z): the tile itself x + 8 y + 64 z, then the six
+// 3-deep face slabs (x-, x+, y-, y+, z-, z+) of 192 points each.
+// ------------------------------------------------------------------------------------
+constexpr int XREG = 512 + 6 * 192;   // 1664
+__device__ __forceinline__ int xreg_idx(int x, int y, int z) {
+    // x slabs: the 3-deep direction fastest; y and z slabs: x fastest (contiguous 8-point rows)
+    if (x < 0) return 512 + (x + 3) + 3 * (y + 8 * z);
+    if (x >= 8) return 512 + 192 + (x - 8) + 3 * (y + 8 * z);
+    if (y < 0) return 512 + 2 * 192 + x + 8 * ((y + 3) + 3 * z);
+    if (y >= 8) return 512 + 3 * 192 + x + 8 * ((y - 8) + 3 * z);
+    if (z < 0) return 512 + 4 * 192 + x + 8 * y + 64 * (z + 3);
+    if (z >= 8) return 512 + 5 * 192 + x + 8 * y + 64 * (z - 8);
+    return x + 8 * y + 64 * z;
+}
+__device__ __forceinline__ void xreg_xyz(int t, int& x, int& y, int& z) {
+    if (t < 512) {
+        x = t & 7; y = (t >> 3) & 7; z = t >> 6;
+        return;
+    }
+    const int k = t - 512, side = k / 192, w = k - side * 192;
+    if (side < 2) {
+        const int a = w % 3, b = (w / 3) & 7, c = w / 24;
+        x = side == 0 ? a - 3 : 8 + a;
+        y = b;
+        z = c;
+    } else if (side < 4) {
+        const int a = (w >> 3) % 3, c = (w >> 3) / 3;
+        x = w & 7;
+        y = side == 2 ? a - 3 : 8 + a;
+        z = c;
+    } else {
+        const int a = w >> 6;
+        x = w & 7;
+        y = (w >> 3) & 7;
+        z = side == 4 ? a - 3 : 8 + a;
+    }
+}
+constexpr size_t SMEMX = sizeof(double) * 5 * XREG;
+
+// stage the state of the cross-shaped region of the tile at (i0, j0, k0) into xr[5][XREG] by
+// cp.async: x-runs of the tile and of the y / z slabs two points at a time (16 bytes) when the
+// mesh rows are 16-byte aligned, the x slabs (3-point runs) and ragged ends point-wise.  Points
+// outside a non-periodic mesh are clamped to a valid address (no active stencil reads them).
+// full = false: the tile only (Euler: no gradients).
+__device__ __forceinline__ void stage_xregion(double* xr, const DevMesh& m, const double* __restrict__ Q,
+                                              int i0, int j0, int k0, bool full) {
+    const int n0 = m.n[0], n1 = m.n[1], n2 = m.n[2];
+    const int64_t N = m.npts, s1 = n0, s2 = (int64_t)n0 * n1;
+    const int per0 = m.periodic[0], per1 = m.periodic[1], per2 = m.periodic[2];
+    const bool al = (n0 & 1) == 0 && (i0 & 1) == 0;
+    const int npair = full ? (512 + 768) / 2 : 256;
+    for (int u = threadIdx.x; u < npair + (full ? 384 : 0); u += NT3) {
+        int t, w;
+        if (u < npair) {
+            t = 2 * u;
+            if (t >= 512) t += 384;           // skip the x slabs
+            w = 2;
+        } else {
+            t = 512 + (u - npair);            // x slabs, one point
+            w = 1;
+        }
+        int x, y, z;
+        xreg_xyz(t, x, y, z);
+        int gj = j0 + y, gk = k0 + z;
+        if (gj < 0) gj = per1 ? gj + n1 : 0; else if (gj >= n1) gj = per1 ? gj - n1 : n1 - 1;
+        if (gk < 0) gk = per2 ? gk + n2 : 0; else if (gk >= n2) gk = per2 ? gk - n2 : n2 - 1;
+        const bool pair16 = w == 2 && al && i0 + x + 1 < n0;
+        for (int e = 0; e < w; ++e) {
+            if (pair16 && e == 1) break;
+            int gi = i0 + x + e;
+            if (gi < 0) gi = per0 ? gi + n0 : 0; else if (gi >= n0) gi = per0 ? gi - n0 : n0 - 1;
+            const int64_t q = gi + s1 * gj + s2 * gk;
+#pragma unroll
+            for (int c = 0; c < 5; ++c) {
+                const unsigned sa = (unsigned)__cvta_generic_to_shared(xr + c * XREG + t + e);
+                if (pair16)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(Q + c * N + q));
+                else
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(Q + c * N + q));
+            }
+        }
+    }
+}
+
+// tiles == NULL: the 8^3 tiles of `box` (3-D grid); else one CTA per listed 8^3 tile of the
+// mesh (flat tile index, x fastest; the donor-stencil tiles of a stepping donor mesh)
+template <bool CART>
+__global__ void __launch_bounds__(NT3, 2) k_visc3d_x(DevMesh m, const double* __restrict__ Q,
+                                                    double* __restrict__ FV, Box box,
+                                                    const int32_t* __restrict__ tiles, Gas g) {
+    extern __shared__ __align__(16) double xr[];   // [5][XREG]: state, then (rho, u, v, w, T)
+    __shared__ uint16_t sc[T3N];
+    const int n0 = m.n[0], n1 = m.n[1], n2 = m.n[2];
+    const int64_t N = m.npts;
+    const int64_t s1 = n0, s2 = (int64_t)n0 * n1;
+    int i0, j0, k0;
+    if (tiles) {
+        const int tl = tiles[blockIdx.x];
+        const int ntx = (n0 + T3X - 1) / T3X, nty = (n1 + T3Y - 1) / T3Y;
+        i0 = (tl % ntx) * T3X;
+        j0 = ((tl / ntx) % nty) * T3Y;
+        k0 = (tl / (ntx * nty)) * T3Z;
+        box.hi[0] = n0 - 1;
+        box.hi[1] = n1 - 1;
+        box.hi[2] = n2 - 1;
+    } else {
+        i0 = box.lo[0] + blockIdx.x * T3X;
+        j0 = box.lo[1] + blockIdx.y * T3Y;
+        k0 = box.lo[2] + blockIdx.z * T3Z;
+    }
+    const int tid = threadIdx.x;
+    // ---- one round trip: the whole cross region (points outside a non-periodic mesh are
+    // clamped to a valid address; no active stencil reads them)
+    stage_xregion(xr, m, Q, i0, j0, k0, true);
+    unsigned clsv[PPT3];
+#pragma unroll
+    for (int s = 0; s < PPT3; ++s) {
+        const int t = tid + s * NT3;
+        const int gi = i0 + (t & 7), gj = j0 + ((t >> 3) & 7), gk = k0 + (t >> 6);
+        const bool live = gi <= box.hi[0] && gj <= box.hi[1] && gk <= box.hi[2];
+        clsv[s] = live ? m.cls[gi + s1 * gj + s2 * gk] : 0u;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    // ---- primitives in place
+    for (int t = tid; t < XREG; t += NT3) {
+        const double r = xr[t], mu = xr[XREG + t], mv = xr[2 * XREG + t], mw = xr[3 * XREG + t];
+        const double E = xr[4 * XREG + t];
+        const double ir = rcp64(r);
+        const double u = mu * ir, v = mv * ir, w = mw * ir;
+        xr[XREG + t] = u;
+        xr[2 * XREG + t] = v;
+        xr[3 * XREG + t] = w;
+        xr[4 * XREG + t] = g.gamma * g.gm1 * (E - 0.5 * (mu * u + mv * v + mw * w)) * ir;
+    }
+#pragma unroll
+    for (int s = 0; s < PPT3; ++s) sc[tid + s * NT3] = (uint16_t)clsv[s];
+    __syncthreads();
+    const double* pf = xr + XREG;   // [4][XREG]: u, v, w, T
+#pragma unroll
+    for (int s = 0; s < PPT3; ++s) {
+        const int t = tid + s * NT3;
+        const unsigned code = sc[t];
+        if (!code) continue;
+        const int x = t & 7, y = (t >> 3) & 7, z = t >> 6;
+        double d[3][4];   // d[kappa][u, v, w, T]
+#pragma unroll
+        for (int kap = 0; kap < 3; ++kap) {
+            const int cl = (code >> (4 * kap)) & 15;
+            auto at = [&](int o) {
+                return kap == 0 ? xreg_idx(x + o, y, z) : (kap == 1 ? xreg_idx(x, y + o, z) : xreg_idx(x, y, z + o));
+            };
+            if (cl == CLS_INT) {
+                const int a1 = at(1), b1 = at(-1), a2 = at(2), b2 = at(-2);
+#pragma unroll
+                for (int f = 0; f < 4; ++f) {
+                    const double* a = pf + f * XREG;
+                    d[kap][f] = (2.0 / 3.0) * (a[a1] - a[b1]) - (1.0 / 12.0) * (a[a2] - a[b2]);
+                }
+            } else {
+#pragma unroll
+                for (int f = 0; f < 4; ++f) d[kap][f] = 0.0;
+                const int ns = c_nst[cl];
+                for (int tt = 0; tt < ns; ++tt) {
+                    const double cf = c_cf[cl][tt];
+                    const int o = at(c_off[cl][tt]);
+#pragma unroll
+                    for (int f = 0; f < 4; ++f) d[kap][f] += cf * pf[f * XREG + o];
+                }
+            }
+        }
+        const double u[3] = {pf[t], pf[XREG + t], pf[2 * XREG + t]};
+        const int64_t p = (i0 + x) + s1 * (j0 + y) + s2 * (k0 + z);
+        double gr[4][3];   // gr[f][i] = d phi_f / d x_i
+#pragma unroll
+        for (int f = 0; f < 4; ++f)
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                if (CART) {
+                    gr[f][i] = m.cJ * (m.cM[i] * d[i][f]);
+                } else {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) acc += __ldg(m.M + (k * 3 + i) * N + p) * d[k][f];
+                    gr[f][i] = __ldg(m.J + p) * acc;
+                }
+            }
+        const double div = gr[0][0] + gr[1][1] + gr[2][2];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            double e = 0.0;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const double tau = (gr[i][j] + gr[j][i] - (i == j ? (2.0 / 3.0) * div : 0.0)) * g.iRe;
+                FV[(int64_t)(i * 4 + j) * N + p] = tau;
+                e += u[j] * tau;
+            }
+            FV[(int64_t)(i * 4 + 3) * N + p] = e + g.kT * gr[3][i];
+        }
+    }
+}
+
+// SAT penalties at one 3-D point (eq:int P:279-299; edges/corners sum over the flagged
+// directions; readings R14-R16), added to R.  q: the point's state; nv[k][i] =
+// (grad kappa_k)_i = J M_{k i}; fv[i][j]: the point's Cartesian viscous fluxes F^V_i (j < 3:
+// tau_ij, j = 3: energy).
+template <bool VISC>
+__device__ __forceinline__ void sat3(const DevMesh& m, const Gas& g, const double* q, int64_t p,
+                                     const int* idx, unsigned code, const double (&nv)[3][3],
+                                     const double (&fv)[3][4], double* R) {
+    constexpr int NC = 5;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const int cl = (code >> (4 * k)) & 15;
+        if (cl != CLS_L0 && cl != CLS_R0) continue;
+        const int sidx = (cl == CLS_L0) ? 0 : 1;
+        const double side = (cl == CLS_L0) ? 1.0 : -1.0;
+        const bool at_face = !m.periodic[k] && (sidx == 0 ? idx[k] == 0 : idx[k] == m.n[k] - 1);
+        const int typ = at_face ? m.face_bc[k][sidx] : MRAB_BC_OVERSET;
+        double qh[NC], dq[NC];
+        int slot = -1;
+        if (typ == MRAB_BC_OVERSET) {
+            slot = m.recv_slot[p];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) qh[c] = m.qhat[c * m.nrecv + slot];
+        } else if (typ == MRAB_BC_FARFIELD) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) qh[c] = g.q_inf[c];
+        } else {   // isothermal no-slip wall
+            qh[0] = q[0];
+            qh[1] = qh[2] = qh[3] = 0.0;
+            qh[4] = q[0] * g.wall_T / (g.gamma * (g.gamma - 1.0));
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c) dq[c] = q[c] - qh[c];
+        double kd[NC];
+        kchar<3>(q, nv[k], side, dq, g.gamma, kd);
+        double sig1 = 0.0;
+        if (VISC) sig1 = 0.5 * g.iRe * (nv[k][0] * nv[k][0] + nv[k][1] * nv[k][1] + nv[k][2] * nv[k][2]);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) R[c] -= (0.5 * kd[c] + sig1 * dq[c]) * (1.0 / kP0);
+        if (VISC && typ != MRAB_BC_WALL) {
+            // F^V_kappa - Fhat^V_kappa contracted with grad(kappa)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                double fk = 0.0, fh = 0.0;
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    fk += nv[k][i] * fv[i][j];
+                    if (typ == MRAB_BC_OVERSET) fh += nv[k][i] * m.fvhat[(int64_t)(i * 4 + j) * m.nrecv + slot];
+                }
+                R[1 + j] += 0.5 * side * (fk - fh) * (1.0 / kP0);
+            }
+        }
+    }
+}
+
+// =====================================================================================
+// k_rhs3z: the 3-D RHS of one mesh in one HBM pass.
+//
+// A CTA owns a TX x TY tile of the x-y plane and marches along z (persistent CTAs: the
+// (tile, plane) work is split evenly over the grid, each CTA walking contiguous z-segments).
+// At step q the CTA forms, for the plane q,
+//   * the D1 gradients of (u, v, w, T) at the points where a contravariant flux is needed:
+//     the tile itself (all three fluxes) and two "arms" of 3 points beyond the tile in x
+//     (Fhat_x only) and in y (Fhat_y only).  D_x / D_y read the plane's primitives over the
+//     tile + 6 cross region, D_z reads a 7-plane ring of primitives (planes q-3 .. q+3);
+//   * F^V (tau, heat flux; R11), F^I, Fhat_kappa = sum_i M_{kappa i} (F^I_i - F^V_i);
+//   * Fhat_z(q) of a tile point is scattered into shared-memory accumulators of the planes
+//     q-3 .. q+3 with the coefficient of offset q - p of each target plane's own segment row
+//     (closures by class code, reading R2); the SAT terms of the plane are added too (they
+//     need F^V at the point, which is in registers there);
+//   * D_x Fhat_x + D_y Fhat_y at the tile points (the fluxes go through shared memory).
+// Plane q-3 is then complete: R = -J * acc, the AB / RK combination and its stores.
+// Threads: one flux point each (192 tile points, 96 y-arm and 72 x-arm points, 24 idle), so
+// no thread carries two flux evaluations; the divergence, completion and epilogue of a tile
+// point are split over two threads (components 0-2 / 3-4).  Every global read of the state is
+// a cp.async of the conserved variables straight into the ring slot of the plane (converted
+// to primitives in place one step later); the epilogue inputs (base, two history terms, J)
+// of the next completed plane are staged the same way.  HBM traffic per point: Q read once,
+// R and the new state written once, history terms read once (plus halo re-reads of
+// neighbouring tiles, mostly L2 hits).
+// =====================================================================================
+// per-phase cycle accounting of k_rhs3z (diagnostic build only: -DMRAB_Z3_PROF; CTA thread 0
+// adds its phase times into ep.trace[0..6])
+#ifdef MRAB_Z3_PROF
+#define Z3PROF(...) __VA_ARGS__
+#else
+#define Z3PROF(...)
+#endif
+namespace z3 {
+constexpr int TX = 16, TY = 12, NT = 384, H = 3;
+constexpr int NTP = TX * TY;                                        // 192 tile points
+// the ring box: x in [-4, TX+4) (TMA rows start on 16-byte boundaries), y in [-3, TY+3)
+constexpr int XO = 4, BX = TX + 2 * XO, BY = TY + 2 * H, NB = BX * BY;   // 24 x 18
+constexpr int FXW = TX + 2 * H;                                     // Fhat_x rows: x in [-3, TX+3)
+constexpr int NXA = 2 * H * TY, NYA = 2 * H * TX;                   // arm flux points, 72 + 96
+constexpr int NF = NTP + NYA + NXA;                                 // 360 flux points
+constexpr int NZ = 7;
+// outer arms beyond the ring box (x-stencils of x-arm points reach x in [-6, -4) and
+// [TX+4, TX+6); y-stencils of y-arm points y in [-6, -3) and [TY+3, TY+6)): four boxes, each
+// [5][rows][cols] at a 128-byte aligned offset: x boxes 12 rows x 2 columns, y boxes 3 x 16
+constexpr int OBX = 2 * TY, OBY = H * TX;                           // 24, 48 points per component
+constexpr int OX0 = 0, OX1 = 128, OY0 = 256, OY1 = OY0 + 5 * OBY, NOB = OY1 + 5 * OBY;
+constexpr int NOP = 2 * OBX + 2 * OBY;                              // 144 outer points
+constexpr int SLOT = 5 * NB;                                        // ring slot (128-byte multiple)
+constexpr int O_PR = 0;                           // [NZ][SLOT] ring: rho, u, v, w, T (5 x NB)
+constexpr int O_PO = O_PR + NZ * SLOT;            // outer-arm state of plane q (boxes above)
+constexpr int O_EP = O_PO + NOB;                  // [2][5][NTP] staged epilogue inputs (base, src0)
+constexpr int O_FX = O_EP + 2 * 5 * NTP;          // [5][TY][FXW] Fhat_x, x-extended rows
+constexpr int O_FY = O_FX + 5 * TY * FXW;         // [5][BY][TX] Fhat_y, y-extended columns
+constexpr int O_AC = O_FY + 5 * BY * TX;          // [NZ][5][NTP] z accumulators
+constexpr int O_FZ = O_AC + NZ * 5 * NTP;         // [5][NTP]  D_z prims, then Fhat_z of plane q
+constexpr int O_TB = O_FZ + 5 * NTP;              // [10][7] D1 coefficient of offset -3..3 by class
+constexpr int O_BAR = O_TB + 72;                  // two mbarriers
+constexpr int O_END = O_BAR + 2;
+constexpr size_t SMEM = sizeof(double) * O_END + 128;   // + alignment of the base to 128 bytes
+enum { KT = 0, KX = 1, KY = 2 };                  // tile point, x-arm point, y-arm point
+// TMA transaction bytes
+constexpr unsigned TX_BOX = 8u * 5 * NB, TX_OUT = 8u * 5 * NOP, TX_EP = 8u * 5 * NTP;
+
+// flux point f of the CTA: kind and tile-relative (x, y).  0..191 tile points, 192..287
+// y-arm points (TX per row, rows -3..-1 and TY..TY+2), 288..359 x-arm points (6 per row)
+__device__ __forceinline__ int fpt(int f, int& x, int& y) {
+    if (f < NTP) {
+        x = f % TX;
+        y = f / TX;
+        return KT;
+    }
+    if (f < NTP + NYA) {
+        const int o = f - NTP, r = o / TX;
+        x = o % TX;
+        y = r < 3 ? r - 3 : TY + r - 3;
+        return KY;
+    }
+    const int o = f - NTP - NYA, c = o % 6;
+    y = o / 6;
+    x = c < 3 ? c - 3 : TX + c - 3;
+    return KX;
+}
+
+__device__ __forceinline__ int wrapi(int i, int n, int per) {
+    if (i < 0) return per ? i + n : 0;
+    if (i >= n) return per ? i - n : n - 1;
+    return i;
+}
+
+// D1 along one direction of the primitive fields in MASK (bit f = field f of u, v, w, T) for
+// segment row `cl`; at(o, fs) returns the address of field u at offset o and sets the field
+// stride fs; fields outside MASK are set to 0.  Warps whose active lanes all take the interior
+// row use its 4 taps; otherwise every lane applies its own row as 7 taps (offsets -3..3) from
+// the coefficient table tb (zeros off the row), without divergence.
+template <int MASK, class At>
+__device__ __forceinline__ void d1f4(int cl, At at, double* d, const double* tb) {
+    if (__all_sync(__activemask(), cl == CLS_INT)) {
+        int s1, s2, s3, s4;
+        const double* a1 = at(1, s1);
+        const double* b1 = at(-1, s2);
+        const double* a2 = at(2, s3);
+        const double* b2 = at(-2, s4);
+        double va1[4], vb1[4], va2[4], vb2[4];
+#pragma unroll
+        for (int f = 0; f < 4; ++f) {
+            if (!((MASK >> f) & 1)) continue;
+            va1[f] = a1[f * s1];
+            vb1[f] = b1[f * s2];
+            va2[f] = a2[f * s3];
+            vb2[f] = b2[f * s4];
+        }
+#pragma unroll
+        for (int f = 0; f < 4; ++f)
+            d[f] = ((MASK >> f) & 1) ? (2.0 / 3.0) * (va1[f] - vb1[f]) - (1.0 / 12.0) * (va2[f] - vb2[f]) : 0.0;
+    } else {
+#pragma unroll
+        for (int f = 0; f < 4; ++f) d[f] = 0.0;
+        const double* row = tb + cl * 7 + 3;
+#pragma unroll
+        for (int o = -3; o <= 3; ++o) {
+            int fs;
+            const double* a = at(o, fs);
+            const double cf = row[o];
+#pragma unroll
+            for (int f = 0; f < 4; ++f)
+                if ((MASK >> f) & 1) d[f] += cf * a[f * fs];
+        }
+    }
+}
+
+// D1 of a flux component along a shared-memory line (stride st): interior row (uni = the whole
+// warp is interior) or the 7-tap row `row` = tb + cl * 7 + 3
+__device__ __forceinline__ double d1s(const double* f, int st, bool uni, const double* row) {
+    if (uni) return (2.0 / 3.0) * (f[st] - f[-st]) - (1.0 / 12.0) * (f[2 * st] - f[-2 * st]);
+    double acc = 0.0;
+#pragma unroll
+    for (int o = -3; o <= 3; ++o) acc += row[o] * f[o * st];
+    return acc;
+}
+
+// per-step ring slot offsets: zo[o + 3] = offset of the slot of plane q + o
+struct ZRing {
+    int zo[7];
+};
+}  // namespace z3
+
+// The flux computation of one flux point of plane q in three parts: D_x / D_y of (u, v, w, T)
+// (z3_dxy), D_z (z3_dz) and the assembly (z3_assemble: metrics, gradients by the chain rule,
+// F^V, F^I, Fhat).  KIND: tile point -> all three Fhat, x-arm -> Fhat_x, y-arm -> Fhat_y.  Arms
+// on Cartesian meshes take only the 8 derivatives their F^V_kappa needs.
+template <int KIND, bool CART>
+struct ZMask {
+    static constexpr int X = (KIND == z3::KY && CART) ? 0x3 : 0xF;   // y-arm: d/dx of u, v only
+    static constexpr int Y = (KIND == z3::KX && CART) ? 0x3 : 0xF;   // x-arm: d/dy of u, v only
+    static constexpr int Z = (KIND == z3::KX && CART) ? 0x5 : ((KIND == z3::KY && CART) ? 0x6 : 0xF);
+};
+
+template <bool CART, int KIND>
+__device__ __forceinline__ void z3_dxy(const double* __restrict__ prq, const double* __restrict__ po,
+                                       const double* __restrict__ tb, int x, int y, unsigned code,
+                                       double (&d)[3][4]) {
+    using namespace z3;
+    const int b = (y + H) * BX + x + XO;
+    {
+        auto at = [&](int o, int& fs) -> const double* {
+            const int xx = x + o;
+            if (KIND == KX && xx < -XO) { fs = OBX; return po + OX0 + OBX + y * 2 + (xx + 6); }
+            if (KIND == KX && xx >= TX + XO) { fs = OBX; return po + OX1 + OBX + y * 2 + (xx - TX - XO); }
+            fs = NB;
+            return prq + NB + b + o;
+        };
+        z3::d1f4<ZMask<KIND, CART>::X>((code >> 0) & 15, at, d[0], tb);
+    }
+    {
+        auto at = [&](int o, int& fs) -> const double* {
+            const int yy = y + o;
+            if (KIND == KY && yy < -H) { fs = OBY; return po + OY0 + OBY + (yy + 6) * TX + x; }
+            if (KIND == KY && yy >= TY + H) { fs = OBY; return po + OY1 + OBY + (yy - TY - H) * TX + x; }
+            fs = NB;
+            return prq + NB + b + o * BX;
+        };
+        z3::d1f4<ZMask<KIND, CART>::Y>((code >> 4) & 15, at, d[1], tb);
+    }
+}
+
+template <int MASK>
+__device__ __forceinline__ void z3_dz(const double* __restrict__ pr, const z3::ZRing& zr,
+                                      const double* __restrict__ tb, int x, int y, unsigned code,
+                                      double* d) {
+    using namespace z3;
+    const int b = (y + H) * BX + x + XO;
+    auto at = [&](int o, int& fs) -> const double* {
+        fs = NB;
+        return pr + zr.zo[o + 3] + NB + b;       // o is a compile-time constant here
+    };
+    z3::d1f4<MASK>((code >> 8) & 15, at, d, tb);
+}
+
+template <bool VISC, bool CART, int KIND>
+__device__ __forceinline__ void z3_assemble(const DevMesh& m, const Gas& g, const double* __restrict__ prq,
+                                            int x, int y, const double (&d)[3][4], int64_t pidx,
+                                            double (&Fh)[3][5], double (&fv)[3][4], double (&Mp)[3][3],
+                                            double& Jp) {
+    using namespace z3;
+    const int b = (y + H) * BX + x + XO;
+    const double rho = prq[b];
+    const double u[3] = {prq[NB + b], prq[2 * NB + b], prq[3 * NB + b]};
+    const double T = prq[4 * NB + b];
+    if (CART) {
+        Jp = m.cJ;
+    } else {
+        Jp = __ldg(m.J + pidx);
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int i = 0; i < 3; ++i) Mp[k][i] = __ldg(m.M + (int64_t)(k * 3 + i) * m.npts + pidx);
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) fv[i][j] = 0.0;
+    if (VISC) {
+        double gr[4][3];   // gr[f][i] = d phi_f / d x_i (chain rule with the metrics)
+#pragma unroll
+        for (int f = 0; f < 4; ++f)
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                if (CART) {
+                    gr[f][i] = m.cJ * (m.cM[i] * d[i][f]);
+                } else {
+                    gr[f][i] = Jp * (Mp[0][i] * d[0][f] + Mp[1][i] * d[1][f] + Mp[2][i] * d[2][f]);
+                }
+            }
+        const double div = gr[0][0] + gr[1][1] + gr[2][2];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            if (CART && KIND == KX && i != 0) continue;   // Cartesian arms: F_kappa only
+            if (CART && KIND == KY && i != 1) continue;
+            double e = 0.0;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const double tau = (gr[i][j] + gr[j][i] - (i == j ? (2.0 / 3.0) * div : 0.0)) * g.iRe;
+                fv[i][j] = tau;
+                e += u[j] * tau;
+            }
+            fv[i][3] = e + g.kT * gr[3][i];
+        }
+    }
+    const double pp = rho * T * g.igamma;
+    const double E = pp * g.igm1 + 0.5 * rho * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+    // Cartesian fluxes F_i = F^I_i - F^V_i, then Fhat_kappa for the wanted kappa
+    double F[3][5];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const double mi = rho * u[i];
+        F[i][0] = mi;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) F[i][1 + j] = mi * u[j] + (i == j ? pp : 0.0) - fv[i][j];
+        F[i][4] = (E + pp) * u[i] - fv[i][3];
+    }
+#pragma unroll
+    for (int kap = 0; kap < 3; ++kap) {
+        if (KIND == KX && kap != 0) continue;
+        if (KIND == KY && kap != 1) continue;
+#pragma unroll
+        for (int c = 0; c < 5; ++c) {
+            if (CART) Fh[kap][c] = m.cM[kap] * F[kap][c];
+            else Fh[kap][c] = Mp[kap][0] * F[0][c] + Mp[kap][1] * F[1][c] + Mp[kap][2] * F[2][c];
+        }
+    }
+}
+
+// one arm flux point of plane q -> FX (x-arm) or FY (y-arm)
+template <bool VISC, bool CART, int KIND>
+__device__ __forceinline__ void z3_arm(const DevMesh& m, const Gas& g, const double* pr, const z3::ZRing& zr,
+                                       const double* po, const double* tb, double* FX, double* FY, int x,
+                                       int y, unsigned code, int64_t pidx) {
+    using namespace z3;
+    double Fh[3][5], fv[3][4], Mp[3][3], Jp, d[3][4];
+    double* dst = KIND == KX ? FX + y * FXW + x + H : FY + (y + H) * TX + x;
+    const int cs = KIND == KX ? TY * FXW : BY * TX;
+    if (code) {
+        const double* prq = pr + zr.zo[3];
+        if (VISC) {
+            z3_dxy<CART, KIND>(prq, po, tb, x, y, code, d);
+            z3_dz<ZMask<KIND, CART>::Z>(pr, zr, tb, x, y, code, d[2]);
+        }
+        z3_assemble<VISC, CART, KIND>(m, g, prq, x, y, d, pidx, Fh, fv, Mp, Jp);
+#pragma unroll
+        for (int c = 0; c < 5; ++c) dst[c * cs] = Fh[KIND == KX ? 0 : 1][c];
+    } else {
+#pragma unroll
+        for (int c = 0; c < 5; ++c) dst[c * cs] = 0.0;
+    }
+}
+
+// After the flux barrier, at the completion point (components C0..C1-1): Fhat_z(q) scattered
+// into the accumulators of planes q-3 .. q+3 with each target plane's row coefficient (zc: the
+// point's z classes of those planes), then D_x Fhat_x + D_y Fhat_y into plane q's.
+template <int C0, int C1>
+__device__ __forceinline__ void z3_div(const double* __restrict__ FX, const double* __restrict__ FY,
+                                       const double* __restrict__ FZ, double* __restrict__ ac, const int* ao,
+                                       const double* __restrict__ tb, int tp, int xp, int yp, unsigned code,
+                                       unsigned zc) {
+    using namespace z3;
+    constexpr int NCG = C1 - C0;
+    const unsigned am = __activemask();
+    double fz[NCG], dv[NCG];
+#pragma unroll
+    for (int c = C0; c < C1; ++c) fz[c - C0] = FZ[c * NTP + tp];
+    const int cx = code & 15, cy = (code >> 4) & 15;
+    const bool ux = __all_sync(am, cx == CLS_INT), uy = __all_sync(am, cy == CLS_INT);
+#pragma unroll
+    for (int c = C0; c < C1; ++c) {
+        const double dx = d1s(FX + c * TY * FXW + yp * FXW + xp + H, 1, ux, tb + cx * 7 + 3);
+        const double dy = d1s(FY + c * BY * TX + (yp + H) * TX + xp, TX, uy, tb + cy * 7 + 3);
+        dv[c - C0] = dx + dy;
+    }
+    // every load before any store (the accumulator slots are distinct; the compiler cannot
+    // know that, so the order is explicit)
+    if (__all_sync(am, zc == 0x1111111u)) {
+        // all seven planes take the interior row at every lane: offsets -2, -1, +1, +2 only
+        // (plane p = q - o receives c_o Fhat_z(q), c_{+-1} = +-2/3, c_{+-2} = -+1/12)
+        constexpr double cfk[7] = {0.0, -1.0 / 12.0, 2.0 / 3.0, 0.0, -2.0 / 3.0, 1.0 / 12.0, 0.0};
+        double av[7][NCG];
+#pragma unroll
+        for (int k = 1; k < 6; ++k)
+#pragma unroll
+            for (int c = C0; c < C1; ++c) av[k][c - C0] = ac[ao[k] + c * NTP + tp];
+#pragma unroll
+        for (int k = 1; k < 6; ++k)
+#pragma unroll
+            for (int c = C0; c < C1; ++c)
+                ac[ao[k] + c * NTP + tp] = av[k][c - C0] + (k == 3 ? dv[c - C0] : cfk[k] * fz[c - C0]);
+    } else {
+        double cf[7], av[7][NCG];
+#pragma unroll
+        for (int k = 0; k < 7; ++k) {
+            cf[k] = tb[((zc >> (4 * k)) & 15u) * 7 + (3 - k) + 3];
+#pragma unroll
+            for (int c = C0; c < C1; ++c) av[k][c - C0] = ac[ao[k] + c * NTP + tp];
+        }
+#pragma unroll
+        for (int k = 0; k < 7; ++k)
+#pragma unroll
+            for (int c = C0; c < C1; ++c)
+                ac[ao[k] + c * NTP + tp] = av[k][c - C0] + cf[k] * fz[c - C0] + (k == 3 ? dv[c - C0] : 0.0);
+    }
+}
+
+// completion of plane p at one tile point (components C0..C1-1): R = -J acc, epilogue, clear.
+// es: the staged inputs [base, src0][5][NTP]; s1v: the second history term (registers)
+template <int C0, int C1>
+__device__ __forceinline__ void z3_complete(const Epilogue& ep, int nsrc_st, double* a, const double* es,
+                                            const double (&s1v)[3], int tp, bool live, bool hole, double Jp,
+                                            int64_t N, int64_t pidx) {
+    using namespace z3;
+    if (live) {
+#pragma unroll
+        for (int c = C0; c < C1; ++c) {
+            const double R = hole ? 0.0 : -Jp * a[c * NTP];
+            if (ep.r_out) ep.r_out[c * N + pidx] = R;
+            if (ep.y_out) {
+                double y = es[c * NTP + tp];
+                if (nsrc_st > 0) y += ep.csrc[0] * es[(5 + c) * NTP + tp];
+                if (nsrc_st > 1) y += ep.csrc[1] * s1v[c - C0];
+                for (int k = 2; k < ep.nsrc; ++k) y += ep.csrc[k] * __ldg(ep.src[k] + c * N + pidx);
+                ep.y_out[c * N + pidx] = y + ep.c_new * R;
+            }
+        }
+    }
+    // the slot becomes plane q+4's (first scattered into at step q+1, after two barriers)
+#pragma unroll
+    for (int c = C0; c < C1; ++c) a[c * NTP] = 0.0;
+}
+
+// mbarrier / TMA helpers (PTX; sm_90+): one arrival with a transaction count, 4-D tiled loads
+__device__ __forceinline__ void mb_init(unsigned a) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mb_expect(unsigned a, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mb_wait(unsigned a, unsigned parity) {
+    unsigned done = 0;
+    while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done) : "r"(a), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma4_l2(unsigned long long map, int x, int y, int z, int c) {
+    asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global [%0, {%1, %2, %3, %4}];"
+                 ::"l"(map), "r"(x), "r"(y), "r"(z), "r"(c) : "memory");
+}
+__device__ __forceinline__ void tma4(unsigned dst, unsigned long long map, int x, int y, int z, int c, unsigned bar) {
+    asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+                 ::"r"(dst), "l"(map), "r"(x), "r"(y), "r"(z), "r"(c), "r"(bar) : "memory");
+}
+
+template <bool VISC, bool CART>
+__global__ void __launch_bounds__(z3::NT, 1) k_rhs3z(DevMesh m, const double* __restrict__ Q, Gas g,
+                                                     Epilogue ep, const __grid_constant__ Z3Maps maps) {
+    using namespace z3;
+    extern __shared__ __align__(128) double sm_raw[];
+    double* sm = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(sm_raw) + 127) & ~uintptr_t(127));
+    double* pr = sm + O_PR;
+    double* po = sm + O_PO;
+    double* es = sm + O_EP;
+    double* FX = sm + O_FX;
+    double* FY = sm + O_FY;
+    double* ac = sm + O_AC;
+    double* FZ = sm + O_FZ;
+    double* tb = sm + O_TB;
+    const unsigned bar_p = (unsigned)__cvta_generic_to_shared(sm + O_BAR);   // plane loads
+    const unsigned bar_e = bar_p + 8;                                        // epilogue loads
+    const int tid = threadIdx.x;
+    const int n0 = m.n[0], n1 = m.n[1], n2 = m.n[2];
+    const int per0 = m.periodic[0], per1 = m.periodic[1], per2 = m.periodic[2];
+    const int64_t N = m.npts, plane = (int64_t)n0 * n1;
+    const int ntx = (n0 + TX - 1) / TX, nty = (n1 + TY - 1) / TY;
+    // D1 coefficient of offset o (-3..3) in segment row cl (zeros off the row and for holes)
+    if (tid < 70) {
+        const int cl = tid / 7, o = tid % 7 - 3;
+        double c = 0.0;
+        for (int s = 0; s < c_nst[cl]; ++s)
+            if (c_off[cl][s] == o) c = c_cf[cl][s];
+        tb[tid] = c;
+    }
+    if (tid == 0) {
+        mb_init(bar_p);
+        mb_init(bar_e);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    unsigned ph_p = 0, ph_e = 0;                       // mbarrier phase parities
+    // generic addresses of the tensor maps in the kernel's parameter space
+    const unsigned long long mbox = reinterpret_cast<unsigned long long>(&maps.box);
+    const unsigned long long mox = reinterpret_cast<unsigned long long>(&maps.ox);
+    const unsigned long long moy = reinterpret_cast<unsigned long long>(&maps.oy);
+    const unsigned long long mbase = reinterpret_cast<unsigned long long>(&maps.base);
+    const unsigned long long ms0 = reinterpret_cast<unsigned long long>(&maps.s0);
+
+    const int nsrc_st = ep.y_out ? min(ep.nsrc, 2) : 0;
+    const bool ep_tma = maps.ep_ok && ep.y_out;
+    // plane offset of plane k (clamped / wrapped) and whether k is a mesh plane
+    auto zpl = [&](int k) -> int { return k < 0 ? (per2 ? k + n2 : 0) : (k >= n2 ? (per2 ? k - n2 : n2 - 1) : k); };
+    auto zoff = [&](int k) -> int64_t { return plane * zpl(k); };
+    auto zin = [&](int k) { return per2 || (k >= 0 && k < n2); };
+
+    const int64_t W = (int64_t)ntx * nty * n2;
+    int64_t w = W * blockIdx.x / gridDim.x;
+    const int64_t wend = W * (blockIdx.x + 1) / gridDim.x;
+    // this thread's flux point (tid < NF), completion point / component group
+    int xf = 0, yf = 0;
+    const int kind = tid < NF ? fpt(tid, xf, yf) : -1;
+    const int tp = tid % NTP;
+    const int xp = tp % TX, yp = tp / TX;
+    const bool lo_grp = tid < NTP;                     // components 0-2 (else 3-4)
+    // element-wise fallback loads (tiles whose box crosses a periodic seam): box points tid and
+    // tid + NT, outer point tid (< 4 OB)
+    const bool has1 = tid + NT < NB, has_o = tid < NOP;
+    const int xs0 = tid % BX - XO, ys0 = tid / BX - H;
+    const int xs1 = (tid + NT) % BX - XO, ys1 = (tid + NT) / BX - H;
+    int xo, yo, oos;                                   // outer point: coordinates, component stride
+    double* po_pt;
+    if (tid < 2 * OBX) {
+        const int e = tid % OBX;
+        xo = (tid < OBX ? -6 : TX + XO) + e % 2;
+        yo = e / 2;
+        oos = OBX;
+        po_pt = po + (tid < OBX ? OX0 : OX1) + e;
+    } else {
+        const int t2 = tid - 2 * OBX, e = t2 % OBY;
+        xo = e % TX;
+        yo = (t2 < OBY ? -6 : TY + H) + e / TX;
+        oos = OBY;
+        po_pt = po + (t2 < OBY ? OY0 : OY1) + e;
+    }
+    while (w < wend) {
+        const int tile = (int)(w / n2), z0 = (int)(w % n2);
+        const int64_t zrem = (int64_t)z0 + (wend - w);
+        const int z1 = (int)(zrem < (int64_t)n2 ? zrem : (int64_t)n2);
+        w += z1 - z0;
+        const int i0 = (tile % ntx) * TX, j0 = (tile / ntx) * TY;
+        // TMA for the plane loads unless the box or the outer arms cross a periodic seam (TMA
+        // fills out-of-mesh points with zeros; across a seam the wrapped values are needed)
+        const bool tma = maps.ok && !(per0 && (i0 - 6 < 0 || i0 + TX + 6 > n0)) &&
+                         !(per1 && (j0 - 6 < 0 || j0 + TY + 6 > n1));
+        __syncthreads();   // the previous segment is done with shared memory
+        // in-plane offsets of this thread's fallback points (clamped / wrapped)
+        const int go0 = wrapi(i0 + xs0, n0, per0) + n0 * wrapi(j0 + ys0, n1, per1);
+        const int go1 = wrapi(i0 + xs1, n0, per0) + n0 * wrapi(j0 + ys1, n1, per1);
+        const int goo = wrapi(i0 + xo, n0, per0) + n0 * wrapi(j0 + yo, n1, per1);
+        // flux point: computed if inside the mesh or across a periodic seam (points beyond a
+        // non-periodic face get the hole code 0); completion point: output if inside the mesh;
+        // its codes (D_z hand-off, divergence, z classes) at the wrapped position if computed
+        const int gi = i0 + xf, gj = j0 + yf;
+        const bool inf = kind >= 0 && (per0 || (gi >= 0 && gi < n0)) && (per1 || (gj >= 0 && gj < n1));
+        const int of = wrapi(gi, n0, per0) + n0 * wrapi(gj, n1, per1);
+        const int gip = i0 + xp, gjp = j0 + yp;
+        const bool outp = gip < n0 && gjp < n1;
+        const bool inp = (gip < n0 || per0) && (gjp < n1 || per1);
+        const int op = (outp ? gip : 0) + n0 * (outp ? gjp : 0);
+        const int opw = wrapi(gip, n0, per0) + n0 * wrapi(gjp, n1, per1);
+        const uint16_t* __restrict__ clsf = m.cls + of;
+        const uint16_t* __restrict__ clsp = m.cls + opw;
+        for (int i = tid; i < NZ * 5 * NTP; i += NT) ac[i] = 0.0;
+        auto cpa = [](double* dst, const double* src) {
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(src));
+        };
+        auto commit = [] { asm volatile("cp.async.commit_group;" ::: "memory"); };
+        // the conserved state of plane kb into a ring slot and (with_outer) the outer arms of
+        // plane ko: TMA boxes issued by thread 0 on bar_p, or element-wise cp.async
+        auto issue_plane = [&](int kb, int slot_off, bool with_outer, int ko) {
+            double* dst = pr + slot_off;
+            if (tma) {
+                if (tid == 0) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    mb_expect(bar_p, TX_BOX + (with_outer ? TX_OUT : 0u));
+                    const unsigned d0 = (unsigned)__cvta_generic_to_shared(dst);
+                    tma4(d0, mbox, i0 - XO, j0 - H, zpl(kb), 0, bar_p);
+                    if (with_outer) {
+                        const unsigned o0 = (unsigned)__cvta_generic_to_shared(po);
+                        const int ko_ = zpl(ko);
+                        tma4(o0 + 8 * OX0, mox, i0 - 6, j0, ko_, 0, bar_p);
+                        tma4(o0 + 8 * OX1, mox, i0 + TX + XO, j0, ko_, 0, bar_p);
+                        tma4(o0 + 8 * OY0, moy, i0, j0 - 6, ko_, 0, bar_p);
+                        tma4(o0 + 8 * OY1, moy, i0, j0 + TY + H, ko_, 0, bar_p);
+                    }
+                }
+            } else {
+                const double* src = Q + zoff(kb);
+#pragma unroll
+                for (int c = 0; c < 5; ++c) cpa(dst + c * NB + tid, src + go0 + c * N);
+                if (has1)
+#pragma unroll
+                    for (int c = 0; c < 5; ++c) cpa(dst + c * NB + tid + NT, src + go1 + c * N);
+                if (with_outer && has_o) {
+                    const double* so = Q + zoff(ko) + goo;
+#pragma unroll
+                    for (int c = 0; c < 5; ++c) cpa(po_pt + c * oos, so + c * N);
+                }
+                commit();
+            }
+        };
+        auto wait_plane = [&] {
+            if (tma) {
+                mb_wait(bar_p, ph_p);
+                ph_p ^= 1u;
+            } else {
+                asm volatile("cp.async.wait_all;" ::: "memory");
+            }
+        };
+        // epilogue inputs (base, two history terms) of plane p: TMA tile boxes on bar_e, or
+        // element-wise by the completion threads (their components)
+        auto issue_ep = [&](int p) {
+            if (ep_tma) {
+                if (tid == 0) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    mb_expect(bar_e, TX_EP * (1 + (nsrc_st > 0)));
+                    const unsigned d0 = (unsigned)__cvta_generic_to_shared(es);
+                    tma4(d0, mbase, i0, j0, p, 0, bar_e);
+                    if (nsrc_st > 0) tma4(d0 + 8 * 5 * NTP, ms0, i0, j0, p, 0, bar_e);
+                }
+            } else if (ep.y_out && outp) {
+                const int64_t q = op + plane * p;
+                const int c0 = lo_grp ? 0 : 3, c1 = lo_grp ? 3 : 5;
+                for (int c = c0; c < c1; ++c) {
+                    cpa(es + c * NTP + tp, ep.base + c * N + q);
+                    if (nsrc_st > 0) cpa(es + (5 + c) * NTP + tp, ep.src[0] + c * N + q);
+                }
+                commit();
+            }
+        };
+        auto wait_ep = [&] {
+            if (ep_tma) {
+                mb_wait(bar_e, ph_e);
+                ph_e ^= 1u;
+            } else {
+                asm volatile("cp.async.wait_all;" ::: "memory");
+            }
+        };
+        // conserved -> (rho, u, v, w, T) in place (zero-filled points beyond a face stay zero)
+        auto convert1 = [&](double* a, int stride) {
+            const double r = a[0], mu = a[stride], mv = a[2 * stride], mw = a[3 * stride];
+            const double E = a[4 * stride];
+            const double ir = r != 0.0 ? rcp64(r) : 0.0;
+            const double u = mu * ir, v = mv * ir, ww = mw * ir;
+            a[stride] = u;
+            a[2 * stride] = v;
+            a[3 * stride] = ww;
+            a[4 * stride] = g.gamma * g.gm1 * (E - 0.5 * (mu * u + mv * v + mw * ww)) * ir;
+        };
+
+        const int qs = z0 - 9, qe = z1 + 2;
+        // ring slot offsets of planes q-3 .. q+3 (zr) and accumulator slot offsets (ao), rotated
+        // by one slot per step; step 0 puts plane qs+3 in slot 3
+        ZRing zr;
+        int ao[7];
+#pragma unroll
+        for (int o = 0; o < 7; ++o) {
+            zr.zo[o] = ((o + NZ - 3) % NZ) * SLOT;
+            ao[o] = ((o + NZ - 3) % NZ) * 5 * NTP;
+        }
+        issue_plane(qs + 3, zr.zo[6], false, 0);
+        unsigned zc = 0;   // z classes of the completion point, planes q-3 .. q+3 (4 bits each)
+        unsigned cF = (inf && zin(qs)) ? (unsigned)__ldg(clsf + zoff(qs)) : 0u;
+        unsigned cP = (inp && zin(qs)) ? (unsigned)__ldg(clsp + zoff(qs)) : 0u;
+        unsigned cZ = (inp && zin(qs + 3)) ? (unsigned)__ldg(clsp + zoff(qs + 3)) : 0u;
+        int64_t pq = zoff(qs), pq1 = zoff(qs + 1), pq4 = zoff(qs + 4);
+        unsigned long long tprof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int q = qs; q <= qe; ++q) {
+            const bool grad = q >= z0 - 3;
+            const int p = q - 3;
+            const bool live_p = p >= z0 && outp;
+            const unsigned codef = cF, codep = cP;
+            Z3PROF(unsigned long long tpa = clock64());
+            zc = (zc >> 4) | (((cZ >> 8) & 15u) << 24);
+            if (q > qs) {
+                // plane offsets of q, q+1, q+4: one plane on, except at a clamped or wrapped face
+                pq = pq1;
+                pq1 = (q + 1 > 0 && q + 1 < n2) ? pq1 + plane : zoff(q + 1);
+                pq4 = (q + 4 > 0 && q + 4 < n2) ? pq4 + plane : zoff(q + 4);
+            }
+            {
+                const bool in1 = zin(q + 1), in4 = zin(q + 4);
+                cF = (inf && in1) ? (unsigned)__ldg(clsf + pq1) : 0u;
+                cP = (inp && in1) ? (unsigned)__ldg(clsp + pq1) : 0u;
+                cZ = (inp && in4) ? (unsigned)__ldg(clsp + pq4) : 0u;
+            }
+            const double Jn = (!CART && live_p) ? __ldg(m.J + op + plane * p) : m.cJ;
+            // the second history term of this thread's components of plane q-3 (used at the end
+            // of the step)
+            double s1v[3] = {0.0, 0.0, 0.0};
+            if (nsrc_st > 1 && live_p) {
+                const double* s1p = ep.src[1] + op + plane * p;
+                if (lo_grp) {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) s1v[c] = __ldg(s1p + c * N);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) s1v[c] = __ldg(s1p + (3 + c) * N);
+                }
+            }
+            // L2 prefetch of the state of plane q+7 (box and outer arms) and of the epilogue inputs
+            // of plane q-1, so the shared-memory loads issued later find them in L2
+            if (tma && tid == 32) {
+                const int k7 = zpl(q + 7);
+                tma4_l2(mbox, i0 - XO, j0 - H, k7, 0);
+                tma4_l2(mox, i0 - 6, j0, k7, 0);
+                tma4_l2(mox, i0 + TX + XO, j0, k7, 0);
+                tma4_l2(moy, i0, j0 - 6, k7, 0);
+                tma4_l2(moy, i0, j0 + TY + H, k7, 0);
+            }
+            if (ep_tma && tid == 64 && p + 2 >= z0 && p + 2 < z1) {
+                tma4_l2(mbase, i0, j0, p + 2, 0);
+                if (nsrc_st > 0) tma4_l2(ms0, i0, j0, p + 2, 0);
+            }
+            wait_plane();
+            __syncthreads();
+            Z3PROF(unsigned long long tpb = clock64(); tprof[0] += tpb - tpa);
+            // epilogue inputs of plane q-3 (completed at the end of this step)
+            if (p >= z0) issue_ep(p);
+            // ---- plane q+3 (ring) and the outer arms of plane q: conserved -> primitives
+            {
+                double* a = pr + zr.zo[6];
+                convert1(a + tid, NB);
+                if (has1) convert1(a + tid + NT, NB);
+                if (grad && has_o) convert1(po_pt, oos);
+            }
+            __syncthreads();
+            Z3PROF(unsigned long long tpc = clock64(); tprof[1] += tpc - tpb);
+            if (grad) {
+                if (kind == KT) {
+                    // ---- tile point: D_x, D_y here, D_z from the threads >= NTP (named barrier
+                    // 1), then all three fluxes (Fhat_z to the hand-off buffer) and the SAT
+                    double Fh[3][5], fv[3][4], Mp[3][3], Jp, d[3][4];
+                    const double* prq = pr + zr.zo[3];
+                    if (VISC && codef) z3_dxy<CART, KT>(prq, po, tb, xf, yf, codef, d);
+                    if (VISC) asm volatile("bar.sync 1, %0;" ::"r"(NT) : "memory");
+                    double* fxd = FX + yf * FXW + xf + H;
+                    double* fyd = FY + (yf + H) * TX + xf;
+                    if (codef) {
+                        const int64_t pidx = of + pq;
+                        if (VISC)
+#pragma unroll
+                            for (int f = 0; f < 4; ++f) d[2][f] = FZ[f * NTP + tid];
+                        z3_assemble<VISC, CART, KT>(m, g, prq, xf, yf, d, pidx, Fh, fv, Mp, Jp);
+#pragma unroll
+                        for (int c = 0; c < 5; ++c) {
+                            fxd[c * TY * FXW] = Fh[0][c];
+                            fyd[c * BY * TX] = Fh[1][c];
+                            FZ[c * NTP + tid] = Fh[2][c];
+                        }
+                        // SAT terms of this point (eq:int), folded into the plane's accumulator
+                        bool sat = false;
+#pragma unroll
+                        for (int k = 0; k < 3; ++k) {
+                            const unsigned cl = (codef >> (4 * k)) & 15u;
+                            sat = sat || cl == CLS_L0 || cl == CLS_R0;
+                        }
+                        if (sat && outp) {
+                            double qv[5];
+#pragma unroll
+                            for (int c = 0; c < 5; ++c) qv[c] = __ldg(Q + c * N + pidx);
+                            double nv[3][3];
+#pragma unroll
+                            for (int k = 0; k < 3; ++k)
+#pragma unroll
+                                for (int i = 0; i < 3; ++i)
+                                    nv[k][i] = CART ? (i == k ? m.cJ * m.cM[k] : 0.0) : Jp * Mp[k][i];
+                            const int idx[3] = {gi, gj, zpl(q)};
+                            double Rs[5] = {0, 0, 0, 0, 0};
+                            sat3<VISC>(m, g, qv, pidx, idx, codef, nv, fv, Rs);
+                            const double mij = -rcp64(Jp);
+                            double* a = ac + ao[3] + tid;
+#pragma unroll
+                            for (int c = 0; c < 5; ++c) a[c * NTP] += Rs[c] * mij;
+                        }
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < 5; ++c) {
+                            fxd[c * TY * FXW] = 0.0;
+                            fyd[c * BY * TX] = 0.0;
+                            FZ[c * NTP + tid] = 0.0;
+                        }
+                    }
+                } else {
+                    // ---- D_z of (u, v, w, T) at tile point tp (hand-off through FZ rows 0-3,
+                    // named barrier 1), then this thread's arm point
+                    if (VISC) {
+                        if (codep) {
+                            double dz[4];
+                            z3_dz<0xF>(pr, zr, tb, xp, yp, codep, dz);
+#pragma unroll
+                            for (int f = 0; f < 4; ++f) FZ[f * NTP + tp] = dz[f];
+                        }
+                        asm volatile("bar.arrive 1, %0;" ::"r"(NT) : "memory");
+                    }
+                    if (kind == KY)
+                        z3_arm<VISC, CART, KY>(m, g, pr, zr, po, tb, FX, FY, xf, yf, codef, of + pq);
+                    else if (kind == KX)
+                        z3_arm<VISC, CART, KX>(m, g, pr, zr, po, tb, FX, FY, xf, yf, codef, of + pq);
+                }
+                __syncthreads();
+                Z3PROF(unsigned long long tpd = clock64(); tprof[2] += tpd - tpc; tpc = tpd);
+                // ---- the outer arms of plane q+1 and the ring slot of plane q+4 (= q-3, free now)
+                if (q + 1 <= qe) issue_plane(q + 4, zr.zo[0], true, q + 1);
+                Z3PROF(unsigned long long tpf = clock64(); tprof[7] += tpf - tpc; tpc = tpf);
+                // ---- z scatter, D_x Fhat_x + D_y Fhat_y at the completion point (its components)
+                if (codep) {
+                    if (lo_grp) z3_div<0, 3>(FX, FY, FZ, ac, ao, tb, tp, xp, yp, codep, zc);
+                    else z3_div<3, 5>(FX, FY, FZ, ac, ao, tb, tp, xp, yp, codep, zc);
+                }
+                Z3PROF(unsigned long long tpe = clock64(); tprof[3] += tpe - tpc; tpc = tpe);
+            } else if (q + 1 <= qe) {
+                // warm-up: only the ring fills (the outer arms from plane z0-3 on)
+                issue_plane(q + 4, zr.zo[0], q + 1 >= z0 - 3, q + 1);
+            }
+            // ---- plane q-3 is complete: R = -J acc, epilogue; its accumulators are cleared
+            if (p >= z0) wait_ep();
+            {
+                double* a = ac + ao[0] + tp;                         // slot of plane q-3
+                const bool hole = (zc & 15u) == 0u;
+                const int64_t pidx = op + plane * (live_p ? p : 0);
+                if (lo_grp) z3_complete<0, 3>(ep, nsrc_st, a, es, s1v, tp, live_p, hole, Jn, N, pidx);
+                else z3_complete<3, 5>(ep, nsrc_st, a, es, s1v, tp, live_p, hole, Jn, N, pidx);
+            }
+            Z3PROF(tprof[grad ? 4 : 5] += clock64() - tpc; tprof[6] += 1);
+            // rotate the slot tables by one plane
+            {
+                const int z0o = zr.zo[0], a0o = ao[0];
+#pragma unroll
+                for (int o = 0; o < 6; ++o) {
+                    zr.zo[o] = zr.zo[o + 1];
+                    ao[o] = ao[o + 1];
+                }
+                zr.zo[6] = z0o;
+                ao[6] = a0o;
+            }
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        Z3PROF(if (tid == 0 && ep.trace)
+                   for (int k = 0; k < 8; ++k) atomicAdd(ep.trace + k, tprof[k]));
+        (void)tprof;
+    }
+}
+
+
+// =====================================================================================
+// 3-D RHS in two passes (the default 3-D path; k_rhs3z above is the one-pass alternative,
+// Options::z3_fused):
+//   k_flux3d  per 8^3 tile: the cross-shaped state region staged by cp.async in one round trip,
+//             primitives in place, D1 gradients at the tile points, then the contravariant
+//             fluxes Fhat_kappa = sum_i M_kappa,i (F^I_i - F^V_i) of every point written once
+//             ([3][5][N]); the Cartesian viscous fluxes F^V are written in tiles holding SAT
+//             points (the SAT term reads them);
+//   k_rhs3d<PRE>  the tiled divergence reading Fhat_kappa in three register-staged passes,
+//             D_kappa by class code, SAT, AB / RK epilogue.
+// Measured (config 4 block mesh, B200): both passes 1.04 ms vs 2.2 ms for k_rhs3z (DESIGN.md
+// §7): k_rhs3z moves 1.5x the algorithmic bytes instead of 2.9x, but recomputes the fluxes of
+// the tile's arms and is latency-bound at 12 warps per SM.
+// =====================================================================================
 // SAT penalties at one point (eq:int P:279-299; edges/corners sum over flagged directions,
 // P:292-294), added to R.  Shared by the direct and the tiled 3-D RHS kernels.
 template <int D, bool VISC, bool CART>
-__device__ __forceinline__ void sat_point(const DevMesh& m, const double* __restrict__ Q,
+__device__ __forceinline__ void sat_point_fv(const DevMesh& m, const double* __restrict__ Q,
                                           const double* __restrict__ FV, const Gas& g, int64_t p,
                                           const int* idx, unsigned code, double Jp, double* R) {
     constexpr int NC = D + 2;
@@ -255,89 +1228,6 @@ __device__ __forceinline__ void sat_point(const DevMesh& m, const double* __rest
     }
 
 // ------------------------------------------------------------------------------------
-// fused RHS + SAT + combination epilogue
-// ------------------------------------------------------------------------------------
-template <int D, bool VISC, bool CART>
-__global__ void __launch_bounds__(256) k_rhs(DevMesh m, const double* __restrict__ Q,
-                                             const double* __restrict__ FV, Gas g, Epilogue ep) {
-    constexpr int NC = D + 2;
-    const int64_t N = m.npts;
-    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= N) return;
-    const int64_t stride[3] = {1, m.n[0], (int64_t)m.n[0] * m.n[1]};
-    int idx[3];
-    idx[0] = (int)(p % m.n[0]);
-    idx[1] = (int)((p / m.n[0]) % m.n[1]);
-    idx[2] = (int)(p / stride[2]);
-    const unsigned code = m.cls[p];
-    double R[NC];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) R[c] = 0.0;
-    if (code) {
-#pragma unroll
-        for (int k = 0; k < D; ++k) {
-            const int cl = (code >> (4 * k)) & 15;
-            double acc[NC];
-#pragma unroll
-            for (int c = 0; c < NC; ++c) acc[c] = 0.0;
-            for (int s = 0; s < c_nst[cl]; ++s) {
-                const int64_t q = nbr(m, p, idx[k], k, c_off[cl][s], stride[k]);
-                double rho, u[D], pr, E;
-                prim<D>(Q, q, N, g.gamma, rho, u, pr, E);
-                double fh[NC];
-#pragma unroll
-                for (int c = 0; c < NC; ++c) fh[c] = 0.0;
-#pragma unroll
-                for (int i = 0; i < D; ++i) {
-                    double Mki;
-                    if (CART) {
-                        if (i != k) continue;
-                        Mki = m.cM[k];
-                    } else {
-                        Mki = __ldg(m.M + (k * D + i) * N + q);
-                    }
-                    // F^I_i - F^V_i
-                    double f[NC];
-                    f[0] = rho * u[i];
-#pragma unroll
-                    for (int j = 0; j < D; ++j) f[1 + j] = rho * u[i] * u[j] + (i == j ? pr : 0.0);
-                    f[D + 1] = (E + pr) * u[i];
-                    if (VISC) {
-#pragma unroll
-                        for (int j = 0; j <= D; ++j)
-                            f[1 + j] -= __ldg(FV + (int64_t)(i * (D + 1) + j) * N + q);
-                    }
-#pragma unroll
-                    for (int c = 0; c < NC; ++c) fh[c] += Mki * f[c];
-                }
-                const double cf = c_cf[cl][s];
-#pragma unroll
-                for (int c = 0; c < NC; ++c) acc[c] += cf * fh[c];
-            }
-#pragma unroll
-            for (int c = 0; c < NC; ++c) R[c] += acc[c];
-        }
-        const double Jp = CART ? m.cJ : __ldg(m.J + p);
-#pragma unroll
-        for (int c = 0; c < NC; ++c) R[c] = -Jp * R[c];
-
-        sat_point<D, VISC, CART>(m, Q, FV, g, p, idx, code, Jp, R);
-    }
-    if (ep.r_out) {
-#pragma unroll
-        for (int c = 0; c < NC; ++c) ep.r_out[c * N + p] = R[c];
-    }
-    if (ep.y_out) {
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            double y = ep.base[c * N + p] + ep.c_new * R[c];
-            for (int s = 0; s < ep.nsrc; ++s) y += ep.csrc[s] * ep.src[s][c * N + p];
-            ep.y_out[c * N + p] = y;
-        }
-    }
-}
-
-// ------------------------------------------------------------------------------------
 // 3-D tiled RHS: per direction kappa, the contravariant flux Fhat_kappa is formed once per
 // point of the tile extended by the D1 reach (3) along kappa and staged in shared memory;
 // every point then applies its own segment row, accumulating in shared memory.  All global
@@ -348,9 +1238,6 @@ __global__ void __launch_bounds__(256) k_rhs(DevMesh m, const double* __restrict
 // Tile 8 x 8 x 8, 256 threads.
 // ------------------------------------------------------------------------------------
 namespace {
-constexpr int T3X = 8, T3Y = 8, T3Z = 8, NT3 = 256;
-constexpr int T3N = T3X * T3Y * T3Z;                  // 512
-constexpr int PPT3 = T3N / NT3;                       // 2 own points per thread
 constexpr int REG3 = 14 * 8 * 8;                      // extended region (any direction)
 constexpr int KR3 = (REG3 + NT3 - 1) / NT3;           // region points per thread (4)
 constexpr size_t SMEM3 = sizeof(double) * 5 * (REG3 + T3N) + sizeof(uint16_t) * T3N;
@@ -608,7 +1495,7 @@ __global__ void __launch_bounds__(NT3, 2) k_rhs3d(DevMesh m, const double* __res
             }
             if (sat) {
                 const int idx[3] = {gi, gj, gk};
-                sat_point<3, VISC, CART>(m, Q, FV, g, p, idx, code, Jp, Rs);
+                sat_point_fv<3, VISC, CART>(m, Q, FV, g, p, idx, code, Jp, Rs);
             }
         }
         if (ep.r_out) {
@@ -618,329 +1505,6 @@ __global__ void __launch_bounds__(NT3, 2) k_rhs3d(DevMesh m, const double* __res
         if (ep.y_out) {
 #pragma unroll
             for (int c = 0; c < NC; ++c) ep.y_out[c * N + p] = yb[c] + ep.c_new * Rs[c];
-        }
-    }
-}
-
-// ------------------------------------------------------------------------------------
-// 3-D tiled viscous fluxes over a box: per direction kappa the primitives (u, v, w, T) of
-// the tile extended by 3 along kappa are staged in shared memory (decoupled loads), each
-// tile point takes its segment row of D1; then Cartesian gradients, stress, heat flux and
-// F^V_i (12 values, layout [i][j]) are written.  Tile 8 x 8 x 8, 256 threads.
-// ------------------------------------------------------------------------------------
-template <bool CART>
-__global__ void __launch_bounds__(NT3, 2) k_visc3d(DevMesh m, const double* __restrict__ Q,
-                                                  double* __restrict__ FV, Box box, Gas g) {
-    __shared__ double pv[4][REG3];
-    __shared__ uint16_t sc[T3N];
-    const int n0 = m.n[0], n1 = m.n[1], n2 = m.n[2];
-    const int64_t N = m.npts;
-    const int64_t s1 = n0, s2 = (int64_t)n0 * n1;
-    const int i0 = box.lo[0] + blockIdx.x * T3X, j0 = box.lo[1] + blockIdx.y * T3Y,
-              k0 = box.lo[2] + blockIdx.z * T3Z;
-    const int tid = threadIdx.x;
-    // class codes: stored to shared memory after the first region loads are issued
-    unsigned clsv[PPT3];
-#pragma unroll
-    for (int s = 0; s < PPT3; ++s) {
-        const int t = tid + s * NT3;
-        const int gi = i0 + (t & 7), gj = j0 + ((t >> 3) & 7), gk = k0 + (t >> 6);
-        const bool live = gi <= box.hi[0] && gj <= box.hi[1] && gk <= box.hi[2];
-        clsv[s] = live ? m.cls[gi + s1 * gj + s2 * gk] : 0u;
-    }
-    double d[PPT3][3][4];   // d[s][kappa][u,v,w,T]
-#pragma unroll
-    for (int kap = 0; kap < 3; ++kap) {
-        const int ex = kap == 0 ? 3 : 0, ey = kap == 1 ? 3 : 0, ez = kap == 2 ? 3 : 0;
-        const int RX = T3X + 2 * ex, RY = T3Y + 2 * ey;
-        double lq[KR3][5];
-#pragma unroll
-        for (int r = 0; r < KR3; ++r) {
-            const int t = tid + r * NT3;
-            const int x = t % RX, y = (t / RX) % RY, z = t / (RX * RY);
-            int gg[3] = {i0 - ex + x, j0 - ey + y, k0 - ez + z};
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                const int n = m.n[k];
-                if (gg[k] < 0) gg[k] = m.periodic[k] ? gg[k] + n : 0;
-                else if (gg[k] >= n) gg[k] = m.periodic[k] ? gg[k] - n : n - 1;
-            }
-            const int64_t q = gg[0] + s1 * gg[1] + s2 * gg[2];
-#pragma unroll
-            for (int c = 0; c < 5; ++c) lq[r][c] = __ldg(Q + c * N + q);
-        }
-        if (kap > 0) __syncthreads();   // previous direction's stencils are done with pv
-#pragma unroll
-        for (int r = 0; r < KR3; ++r) {
-            const int t = tid + r * NT3;
-            if (t >= REG3) break;
-            const double ir = rcp64(lq[r][0]);
-            const double u = lq[r][1] * ir, v = lq[r][2] * ir, w = lq[r][3] * ir;
-            pv[0][t] = u;
-            pv[1][t] = v;
-            pv[2][t] = w;
-            pv[3][t] = g.gamma * g.gm1 * (lq[r][4] - 0.5 * (lq[r][1] * u + lq[r][2] * v + lq[r][3] * w)) * ir;
-        }
-        if (kap == 0)
-#pragma unroll
-            for (int s = 0; s < PPT3; ++s) sc[tid + s * NT3] = (uint16_t)clsv[s];
-        __syncthreads();
-        const int sk = kap == 0 ? 1 : (kap == 1 ? RX : RX * RY);
-#pragma unroll
-        for (int s = 0; s < PPT3; ++s) {
-            const int t = tid + s * NT3;
-            const unsigned code = sc[t];
-#pragma unroll
-            for (int f = 0; f < 4; ++f) d[s][kap][f] = 0.0;
-            if (!code) continue;
-            const int x = t & 7, y = (t >> 3) & 7, z = t >> 6;
-            const int rr = (x + ex) + RX * ((y + ey) + RY * (z + ez));
-            const int cl = (code >> (4 * kap)) & 15;
-            if (cl == CLS_INT) {
-#pragma unroll
-                for (int f = 0; f < 4; ++f) {
-                    const double* a = pv[f];
-                    d[s][kap][f] = (2.0 / 3.0) * (a[rr + sk] - a[rr - sk]) - (1.0 / 12.0) * (a[rr + 2 * sk] - a[rr - 2 * sk]);
-                }
-            } else {
-                const int ns = c_nst[cl];
-                for (int tt = 0; tt < ns; ++tt) {
-                    const double cf = c_cf[cl][tt];
-                    const int o = rr + c_off[cl][tt] * sk;
-#pragma unroll
-                    for (int f = 0; f < 4; ++f) d[s][kap][f] += cf * pv[f][o];
-                }
-            }
-        }
-    }
-    // center primitives (the z-extended region holds the tile points at z + 3)
-#pragma unroll
-    for (int s = 0; s < PPT3; ++s) {
-        const int t = tid + s * NT3;
-        const unsigned code = sc[t];
-        if (!code) continue;
-        const int x = t & 7, y = (t >> 3) & 7, z = t >> 6;
-        const int rr = x + T3X * (y + T3Y * (z + 3));
-        const double u[3] = {pv[0][rr], pv[1][rr], pv[2][rr]};
-        const int64_t p = (i0 + x) + s1 * (j0 + y) + s2 * (k0 + z);
-        double gr[4][3];   // gr[f][i] = d phi_f / d x_i
-#pragma unroll
-        for (int f = 0; f < 4; ++f)
-#pragma unroll
-            for (int i = 0; i < 3; ++i) {
-                if (CART) {
-                    gr[f][i] = m.cJ * (m.cM[i] * d[s][i][f]);
-                } else {
-                    double acc = 0.0;
-#pragma unroll
-                    for (int k = 0; k < 3; ++k) acc += __ldg(m.M + (k * 3 + i) * N + p) * d[s][k][f];
-                    gr[f][i] = __ldg(m.J + p) * acc;
-                }
-            }
-        const double div = gr[0][0] + gr[1][1] + gr[2][2];
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            double e = 0.0;
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {
-                const double tau = (gr[i][j] + gr[j][i] - (i == j ? (2.0 / 3.0) * div : 0.0)) * g.iRe;
-                FV[(int64_t)(i * 4 + j) * N + p] = tau;
-                e += u[j] * tau;
-            }
-            FV[(int64_t)(i * 4 + 3) * N + p] = e + g.kT * gr[3][i];
-        }
-    }
-}
-
-// ------------------------------------------------------------------------------------
-// 3-D viscous fluxes, one memory round trip per tile: the state of the whole cross-shaped
-// region the three D1 passes read (tile 8^3 plus 3 layers on each of its six faces: 1664
-// points) is copied to shared memory by cp.async at once, turned into primitives in place,
-// and every gradient is taken from there (k_visc3d loaded one direction-extended region per
-// pass: three dependent round trips).  Same arithmetic as k_visc3d.
-// Cross-region index of tile-relative (x, y, z): the tile itself x + 8 y + 64 z, then the six
-// 3-deep face slabs (x-, x+, y-, y+, z-, z+) of 192 points each.
-// ------------------------------------------------------------------------------------
-constexpr int XREG = 512 + 6 * 192;   // 1664
-__device__ __forceinline__ int xreg_idx(int x, int y, int z) {
-    // x slabs: the 3-deep direction fastest; y and z slabs: x fastest (contiguous 8-point rows)
-    if (x < 0) return 512 + (x + 3) + 3 * (y + 8 * z);
-    if (x >= 8) return 512 + 192 + (x - 8) + 3 * (y + 8 * z);
-    if (y < 0) return 512 + 2 * 192 + x + 8 * ((y + 3) + 3 * z);
-    if (y >= 8) return 512 + 3 * 192 + x + 8 * ((y - 8) + 3 * z);
-    if (z < 0) return 512 + 4 * 192 + x + 8 * y + 64 * (z + 3);
-    if (z >= 8) return 512 + 5 * 192 + x + 8 * y + 64 * (z - 8);
-    return x + 8 * y + 64 * z;
-}
-__device__ __forceinline__ void xreg_xyz(int t, int& x, int& y, int& z) {
-    if (t < 512) {
-        x = t & 7; y = (t >> 3) & 7; z = t >> 6;
-        return;
-    }
-    const int k = t - 512, side = k / 192, w = k - side * 192;
-    if (side < 2) {
-        const int a = w % 3, b = (w / 3) & 7, c = w / 24;
-        x = side == 0 ? a - 3 : 8 + a;
-        y = b;
-        z = c;
-    } else if (side < 4) {
-        const int a = (w >> 3) % 3, c = (w >> 3) / 3;
-        x = w & 7;
-        y = side == 2 ? a - 3 : 8 + a;
-        z = c;
-    } else {
-        const int a = w >> 6;
-        x = w & 7;
-        y = (w >> 3) & 7;
-        z = side == 4 ? a - 3 : 8 + a;
-    }
-}
-constexpr size_t SMEMX = sizeof(double) * 5 * XREG;
-
-// stage the state of the cross-shaped region of the tile at (i0, j0, k0) into xr[5][XREG] by
-// cp.async: x-runs of the tile and of the y / z slabs two points at a time (16 bytes) when the
-// mesh rows are 16-byte aligned, the x slabs (3-point runs) and ragged ends point-wise.  Points
-// outside a non-periodic mesh are clamped to a valid address (no active stencil reads them).
-// full = false: the tile only (Euler: no gradients).
-__device__ __forceinline__ void stage_xregion(double* xr, const DevMesh& m, const double* __restrict__ Q,
-                                              int i0, int j0, int k0, bool full) {
-    const int n0 = m.n[0], n1 = m.n[1], n2 = m.n[2];
-    const int64_t N = m.npts, s1 = n0, s2 = (int64_t)n0 * n1;
-    const int per0 = m.periodic[0], per1 = m.periodic[1], per2 = m.periodic[2];
-    const bool al = (n0 & 1) == 0 && (i0 & 1) == 0;
-    const int npair = full ? (512 + 768) / 2 : 256;
-    for (int u = threadIdx.x; u < npair + (full ? 384 : 0); u += NT3) {
-        int t, w;
-        if (u < npair) {
-            t = 2 * u;
-            if (t >= 512) t += 384;           // skip the x slabs
-            w = 2;
-        } else {
-            t = 512 + (u - npair);            // x slabs, one point
-            w = 1;
-        }
-        int x, y, z;
-        xreg_xyz(t, x, y, z);
-        int gj = j0 + y, gk = k0 + z;
-        if (gj < 0) gj = per1 ? gj + n1 : 0; else if (gj >= n1) gj = per1 ? gj - n1 : n1 - 1;
-        if (gk < 0) gk = per2 ? gk + n2 : 0; else if (gk >= n2) gk = per2 ? gk - n2 : n2 - 1;
-        const bool pair16 = w == 2 && al && i0 + x + 1 < n0;
-        for (int e = 0; e < w; ++e) {
-            if (pair16 && e == 1) break;
-            int gi = i0 + x + e;
-            if (gi < 0) gi = per0 ? gi + n0 : 0; else if (gi >= n0) gi = per0 ? gi - n0 : n0 - 1;
-            const int64_t q = gi + s1 * gj + s2 * gk;
-#pragma unroll
-            for (int c = 0; c < 5; ++c) {
-                const unsigned sa = (unsigned)__cvta_generic_to_shared(xr + c * XREG + t + e);
-                if (pair16)
-                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(Q + c * N + q));
-                else
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(Q + c * N + q));
-            }
-        }
-    }
-}
-
-template <bool CART>
-__global__ void __launch_bounds__(NT3, 2) k_visc3d_x(DevMesh m, const double* __restrict__ Q,
-                                                    double* __restrict__ FV, Box box, Gas g) {
-    extern __shared__ __align__(16) double xr[];   // [5][XREG]: state, then (rho, u, v, w, T)
-    __shared__ uint16_t sc[T3N];
-    const int n0 = m.n[0], n1 = m.n[1], n2 = m.n[2];
-    const int64_t N = m.npts;
-    const int64_t s1 = n0, s2 = (int64_t)n0 * n1;
-    const int i0 = box.lo[0] + blockIdx.x * T3X, j0 = box.lo[1] + blockIdx.y * T3Y,
-              k0 = box.lo[2] + blockIdx.z * T3Z;
-    const int tid = threadIdx.x;
-    const int per0 = m.periodic[0], per1 = m.periodic[1], per2 = m.periodic[2];
-    // ---- one round trip: the whole cross region (points outside a non-periodic mesh are
-    // clamped to a valid address; no active stencil reads them)
-    stage_xregion(xr, m, Q, i0, j0, k0, true);
-    unsigned clsv[PPT3];
-#pragma unroll
-    for (int s = 0; s < PPT3; ++s) {
-        const int t = tid + s * NT3;
-        const int gi = i0 + (t & 7), gj = j0 + ((t >> 3) & 7), gk = k0 + (t >> 6);
-        const bool live = gi <= box.hi[0] && gj <= box.hi[1] && gk <= box.hi[2];
-        clsv[s] = live ? m.cls[gi + s1 * gj + s2 * gk] : 0u;
-    }
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncthreads();
-    // ---- primitives in place
-    for (int t = tid; t < XREG; t += NT3) {
-        const double r = xr[t], mu = xr[XREG + t], mv = xr[2 * XREG + t], mw = xr[3 * XREG + t];
-        const double E = xr[4 * XREG + t];
-        const double ir = rcp64(r);
-        const double u = mu * ir, v = mv * ir, w = mw * ir;
-        xr[XREG + t] = u;
-        xr[2 * XREG + t] = v;
-        xr[3 * XREG + t] = w;
-        xr[4 * XREG + t] = g.gamma * g.gm1 * (E - 0.5 * (mu * u + mv * v + mw * w)) * ir;
-    }
-#pragma unroll
-    for (int s = 0; s < PPT3; ++s) sc[tid + s * NT3] = (uint16_t)clsv[s];
-    __syncthreads();
-    const double* pf = xr + XREG;   // [4][XREG]: u, v, w, T
-#pragma unroll
-    for (int s = 0; s < PPT3; ++s) {
-        const int t = tid + s * NT3;
-        const unsigned code = sc[t];
-        if (!code) continue;
-        const int x = t & 7, y = (t >> 3) & 7, z = t >> 6;
-        double d[3][4];   // d[kappa][u, v, w, T]
-#pragma unroll
-        for (int kap = 0; kap < 3; ++kap) {
-            const int cl = (code >> (4 * kap)) & 15;
-            auto at = [&](int o) {
-                return kap == 0 ? xreg_idx(x + o, y, z) : (kap == 1 ? xreg_idx(x, y + o, z) : xreg_idx(x, y, z + o));
-            };
-            if (cl == CLS_INT) {
-                const int a1 = at(1), b1 = at(-1), a2 = at(2), b2 = at(-2);
-#pragma unroll
-                for (int f = 0; f < 4; ++f) {
-                    const double* a = pf + f * XREG;
-                    d[kap][f] = (2.0 / 3.0) * (a[a1] - a[b1]) - (1.0 / 12.0) * (a[a2] - a[b2]);
-                }
-            } else {
-#pragma unroll
-                for (int f = 0; f < 4; ++f) d[kap][f] = 0.0;
-                const int ns = c_nst[cl];
-                for (int tt = 0; tt < ns; ++tt) {
-                    const double cf = c_cf[cl][tt];
-                    const int o = at(c_off[cl][tt]);
-#pragma unroll
-                    for (int f = 0; f < 4; ++f) d[kap][f] += cf * pf[f * XREG + o];
-                }
-            }
-        }
-        const double u[3] = {pf[t], pf[XREG + t], pf[2 * XREG + t]};
-        const int64_t p = (i0 + x) + s1 * (j0 + y) + s2 * (k0 + z);
-        double gr[4][3];   // gr[f][i] = d phi_f / d x_i
-#pragma unroll
-        for (int f = 0; f < 4; ++f)
-#pragma unroll
-            for (int i = 0; i < 3; ++i) {
-                if (CART) {
-                    gr[f][i] = m.cJ * (m.cM[i] * d[i][f]);
-                } else {
-                    double acc = 0.0;
-#pragma unroll
-                    for (int k = 0; k < 3; ++k) acc += __ldg(m.M + (k * 3 + i) * N + p) * d[k][f];
-                    gr[f][i] = __ldg(m.J + p) * acc;
-                }
-            }
-        const double div = gr[0][0] + gr[1][1] + gr[2][2];
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            double e = 0.0;
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {
-                const double tau = (gr[i][j] + gr[j][i] - (i == j ? (2.0 / 3.0) * div : 0.0)) * g.iRe;
-                FV[(int64_t)(i * 4 + j) * N + p] = tau;
-                e += u[j] * tau;
-            }
-            FV[(int64_t)(i * 4 + 3) * N + p] = e + g.kT * gr[3][i];
         }
     }
 }
@@ -1109,159 +1673,6 @@ __global__ void __launch_bounds__(NT3, 2) k_flux3d(DevMesh m, const double* __re
     }
 }
 
-constexpr int REGD = 14 * 8 * 8;                    // one kappa-extended region
-constexpr size_t SMEMD = sizeof(double) * 3 * 5 * REGD;
-
-template <bool VISC, bool CART>
-__global__ void __launch_bounds__(NT3, 2) k_div3d(DevMesh m, const double* __restrict__ Q,
-                                                 const double* __restrict__ FH,
-                                                 const double* __restrict__ FV, Gas g, Epilogue ep) {
-    constexpr int NC = 5;
-    extern __shared__ __align__(16) double fb[];     // [kappa][c][REGD]
-    __shared__ uint16_t sc[T3N];
-    const int n0 = m.n[0], n1 = m.n[1], n2 = m.n[2];
-    const int64_t N = m.npts;
-    const int64_t s1 = n0, s2 = (int64_t)n0 * n1;
-    const int i0 = blockIdx.x * T3X, j0 = blockIdx.y * T3Y, k0 = blockIdx.z * T3Z;
-    const int tid = threadIdx.x;
-    const int per0 = m.periodic[0], per1 = m.periodic[1], per2 = m.periodic[2];
-    // ---- the three extended regions of Fhat_kappa in one round trip
-    // y- and z-extended regions: x-runs of 8 doubles, 16-byte copies when rows are 16-byte
-    // aligned (even n0; tiles start at multiples of 8)
-    const bool pair = (n0 & 1) == 0 && i0 + 8 <= n0;
-#pragma unroll
-    for (int kap = 1; kap < 3; ++kap) {
-        if (!pair) break;
-        const int ey = kap == 1 ? 3 : 0, ez = kap == 2 ? 3 : 0;
-        const int RY = T3Y + 2 * ey;
-        for (int t = tid; t < REGD / 2; t += NT3) {
-            const int x2 = t & 3, y = (t >> 2) % RY, z = (t >> 2) / RY;
-            int gj = j0 - ey + y, gk = k0 - ez + z;
-            if (gj < 0) gj = per1 ? gj + n1 : 0; else if (gj >= n1) gj = per1 ? gj - n1 : n1 - 1;
-            if (gk < 0) gk = per2 ? gk + n2 : 0; else if (gk >= n2) gk = per2 ? gk - n2 : n2 - 1;
-            const int64_t q = i0 + 2 * x2 + s1 * gj + s2 * gk;
-            const int e = 2 * x2 + T3X * (y + RY * z);
-#pragma unroll
-            for (int c = 0; c < NC; ++c) {
-                const unsigned sa = (unsigned)__cvta_generic_to_shared(fb + (kap * NC + c) * REGD + e);
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(FH + (int64_t)(kap * NC + c) * N + q));
-            }
-        }
-    }
-#pragma unroll
-    for (int kap = 0; kap < 3; ++kap) {
-        if (kap > 0 && pair) break;
-        const int ex = kap == 0 ? 3 : 0, ey = kap == 1 ? 3 : 0, ez = kap == 2 ? 3 : 0;
-        const int RX = T3X + 2 * ex, RY = T3Y + 2 * ey;
-        for (int t = tid; t < REGD; t += NT3) {
-            const int x = t % RX, y = (t / RX) % RY, z = t / (RX * RY);
-            int gi = i0 - ex + x, gj = j0 - ey + y, gk = k0 - ez + z;
-            if (gi < 0) gi = per0 ? gi + n0 : 0; else if (gi >= n0) gi = per0 ? gi - n0 : n0 - 1;
-            if (gj < 0) gj = per1 ? gj + n1 : 0; else if (gj >= n1) gj = per1 ? gj - n1 : n1 - 1;
-            if (gk < 0) gk = per2 ? gk + n2 : 0; else if (gk >= n2) gk = per2 ? gk - n2 : n2 - 1;
-            const int64_t q = gi + s1 * gj + s2 * gk;
-#pragma unroll
-            for (int c = 0; c < NC; ++c) {
-                const unsigned sa = (unsigned)__cvta_generic_to_shared(fb + (kap * NC + c) * REGD + t);
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(FH + (int64_t)(kap * NC + c) * N + q));
-            }
-        }
-    }
-    unsigned clsv[PPT3];
-#pragma unroll
-    for (int s = 0; s < PPT3; ++s) {
-        const int t = tid + s * NT3;
-        const int gi = i0 + (t & 7), gj = j0 + ((t >> 3) & 7), gk = k0 + (t >> 6);
-        const bool live = gi < n0 && gj < n1 && gk < n2;
-        clsv[s] = live ? m.cls[gi + s1 * gj + s2 * gk] : 0u;
-    }
-    // epilogue inputs requested while the regions land
-    double yb[PPT3][NC];
-#pragma unroll
-    for (int s = 0; s < PPT3; ++s)
-#pragma unroll
-        for (int c = 0; c < NC; ++c) yb[s][c] = 0.0;
-    if (ep.y_out) {
-#pragma unroll
-        for (int s = 0; s < PPT3; ++s) {
-            const int t = tid + s * NT3;
-            const int gi = min(i0 + (t & 7), n0 - 1), gj = min(j0 + ((t >> 3) & 7), n1 - 1), gk = min(k0 + (t >> 6), n2 - 1);
-            const int64_t p = gi + s1 * gj + s2 * gk;
-#pragma unroll
-            for (int c = 0; c < NC; ++c) {
-                double y = __ldg(ep.base + c * N + p);
-                for (int k = 0; k < ep.nsrc; ++k) y += ep.csrc[k] * __ldg(ep.src[k] + c * N + p);
-                yb[s][c] = y;
-            }
-        }
-    }
-#pragma unroll
-    for (int s = 0; s < PPT3; ++s) sc[tid + s * NT3] = (uint16_t)clsv[s];
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncthreads();
-#pragma unroll
-    for (int s = 0; s < PPT3; ++s) {
-        const int t = tid + s * NT3;
-        const int x = t & 7, y = (t >> 3) & 7, z = t >> 6;
-        const int gi = i0 + x, gj = j0 + y, gk = k0 + z;
-        if (gi >= n0 || gj >= n1 || gk >= n2) continue;
-        const int64_t p = gi + s1 * gj + s2 * gk;
-        const unsigned code = sc[t];
-        double Rs[NC] = {0, 0, 0, 0, 0};
-        if (code) {
-            double acc[NC] = {0, 0, 0, 0, 0};
-#pragma unroll
-            for (int kap = 0; kap < 3; ++kap) {
-                const int ex = kap == 0 ? 3 : 0, ey = kap == 1 ? 3 : 0, ez = kap == 2 ? 3 : 0;
-                const int RX = T3X + 2 * ex, RY = T3Y + 2 * ey;
-                const int rr = (x + ex) + RX * ((y + ey) + RY * (z + ez));
-                const int sk = kap == 0 ? 1 : (kap == 1 ? RX : RX * RY);
-                const double* f = fb + kap * NC * REGD;
-                const int cl = (code >> (4 * kap)) & 15;
-                if (cl == CLS_INT) {
-#pragma unroll
-                    for (int c = 0; c < NC; ++c) {
-                        const double* fc = f + c * REGD;
-                        acc[c] += (2.0 / 3.0) * (fc[rr + sk] - fc[rr - sk]) - (1.0 / 12.0) * (fc[rr + 2 * sk] - fc[rr - 2 * sk]);
-                    }
-                } else {
-                    const int ns = c_nst[cl];
-                    double a2[NC] = {0, 0, 0, 0, 0};
-                    for (int tt = 0; tt < ns; ++tt) {
-                        const double cf = c_cf[cl][tt];
-                        const int o = rr + c_off[cl][tt] * sk;
-#pragma unroll
-                        for (int c = 0; c < NC; ++c) a2[c] += cf * f[c * REGD + o];
-                    }
-#pragma unroll
-                    for (int c = 0; c < NC; ++c) acc[c] += a2[c];
-                }
-            }
-            const double Jp = CART ? m.cJ : __ldg(m.J + p);
-#pragma unroll
-            for (int c = 0; c < NC; ++c) Rs[c] = -Jp * acc[c];
-            bool sat = false;
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                const int cl = (code >> (4 * k)) & 15;
-                sat = sat || cl == CLS_L0 || cl == CLS_R0;
-            }
-            if (sat) {
-                const int idx[3] = {gi, gj, gk};
-                sat_point<3, VISC, CART>(m, Q, FV, g, p, idx, code, Jp, Rs);
-            }
-        }
-        if (ep.r_out) {
-#pragma unroll
-            for (int c = 0; c < NC; ++c) ep.r_out[c * N + p] = Rs[c];
-        }
-        if (ep.y_out) {
-#pragma unroll
-            for (int c = 0; c < NC; ++c) ep.y_out[c * N + p] = yb[s][c] + ep.c_new * Rs[c];
-        }
-    }
-}
-
 // ------------------------------------------------------------------------------------
 // intermediate states on a box: out = base + sum_k c_k src_k (all components)
 // ------------------------------------------------------------------------------------
@@ -1289,58 +1700,6 @@ __global__ void __launch_bounds__(256) k_combine(int nc, int64_t N, int n0, int 
         out[c * N + p] = y;
     }
 }
-
-// ------------------------------------------------------------------------------------
-// donor gather (Lagrange interpolation, tensor product of per-axis weights)
-// ------------------------------------------------------------------------------------
-template <int D, bool VISC>
-__global__ void __launch_bounds__(128) k_interp(RecvList rl, DonorSet ds) {
-    constexpr int NC = D + 2;
-    constexpr int NF = D * (D + 1);
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= rl.n) return;
-    const int dm = rl.donor[r];
-    const int b0 = rl.base[r * 3 + 0], b1 = rl.base[r * 3 + 1], b2 = rl.base[r * 3 + 2];
-    const int n0 = ds.n[dm][0], n1 = ds.n[dm][1], n2 = ds.n[dm][2];
-    const int64_t N = ds.npts[dm];
-    const double* __restrict__ S = ds.state[dm];
-    const double* __restrict__ F = ds.fv[dm];
-    const double* w = rl.w + r * 12;
-    double qa[NC], fa[VISC ? NF : 1];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) qa[c] = 0.0;
-    if (VISC)
-#pragma unroll
-        for (int c = 0; c < NF; ++c) fa[c] = 0.0;
-    const int nz = (D == 3) ? 4 : 1;
-    for (int a2 = 0; a2 < nz; ++a2) {
-        int kk = b2 + a2;
-        if (kk >= n2) kk -= n2;
-        const double w2 = (D == 3) ? w[8 + a2] : 1.0;
-        for (int a1 = 0; a1 < 4; ++a1) {
-            int jj = b1 + a1;
-            if (jj >= n1) jj -= n1;
-            const double w12 = w2 * w[4 + a1];
-            for (int a0 = 0; a0 < 4; ++a0) {
-                int ii = b0 + a0;
-                if (ii >= n0) ii -= n0;
-                const double W = w12 * w[a0];
-                const int64_t q = ii + (int64_t)n0 * (jj + (int64_t)n1 * kk);
-#pragma unroll
-                for (int c = 0; c < NC; ++c) qa[c] += W * __ldg(S + c * N + q);
-                if (VISC)
-#pragma unroll
-                    for (int c = 0; c < NF; ++c) fa[c] += W * __ldg(F + c * N + q);
-            }
-        }
-    }
-#pragma unroll
-    for (int c = 0; c < NC; ++c) rl.qhat[c * rl.n + r] = qa[c];
-    if (VISC)
-#pragma unroll
-        for (int c = 0; c < NF; ++c) rl.fvhat[c * rl.n + r] = fa[c];
-}
-
 // 3-D gather, four lanes per receiver: lane a0 takes the stencil column i = b0 + a0, so the
 // four lanes of a receiver read 32 contiguous bytes per (j, k) row (one sector instead of four
 // scattered ones); the column sums are reduced over the quad with two shuffles per value.
@@ -1513,64 +1872,137 @@ std::vector<int32_t> interp3_groups(int64_t R, const int32_t* donor, const int32
 // ------------------------------------------------------------------------------------
 // launchers
 // ------------------------------------------------------------------------------------
-static inline unsigned blocks_for(int64_t n, int bs) { return (unsigned)((n + bs - 1) / bs); }
+static int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
 
-void launch_visc(int dim, const DevMesh& m, const double* Q, double* FV, const Box& box,
-                 const Gas& gas, cudaStream_t st) {
-    int64_t tot = (int64_t)(box.hi[0] - box.lo[0] + 1) * (box.hi[1] - box.lo[1] + 1) *
-                  (box.hi[2] - box.lo[2] + 1);
-    if (tot <= 0) return;
-    unsigned nb = blocks_for(tot, 256);
-    static int direct = -1;
-    if (direct < 0) {
-        const char* e = getenv("MRAB_3D_DIRECT");
-        direct = e && e[0] == '1';
+void launch_visc(const DevMesh& m, const double* Q, double* FV, const Box& box, const int32_t* tiles,
+                 int ntiles, const Gas& gas, cudaStream_t st) {
+    static bool init = false;
+    if (!init) {
+        cudaFuncSetAttribute(k_visc3d_x<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEMX);
+        cudaFuncSetAttribute(k_visc3d_x<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEMX);
+        init = true;
     }
-    if (dim == 3 && !direct) {
-        dim3 grid((box.hi[0] - box.lo[0] + T3X) / T3X, (box.hi[1] - box.lo[1] + T3Y) / T3Y,
-                  (box.hi[2] - box.lo[2] + T3Z) / T3Z);
-        static int xr = -1;
-        if (xr < 0) {
-            const char* e = getenv("MRAB_VISC3D_X");
-            xr = e ? atoi(e) : 1;
-            cudaFuncSetAttribute(k_visc3d_x<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEMX);
-            cudaFuncSetAttribute(k_visc3d_x<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEMX);
-        }
-        if (xr) {
-            if (m.cart) k_visc3d_x<true><<<grid, NT3, SMEMX, st>>>(m, Q, FV, box, gas);
-            else k_visc3d_x<false><<<grid, NT3, SMEMX, st>>>(m, Q, FV, box, gas);
-        } else {
-            if (m.cart) k_visc3d<true><<<grid, NT3, 0, st>>>(m, Q, FV, box, gas);
-            else k_visc3d<false><<<grid, NT3, 0, st>>>(m, Q, FV, box, gas);
-        }
-        return;
-    }
-    if (dim == 2) {
-        if (m.cart) k_visc<2, true><<<nb, 256, 0, st>>>(m, Q, FV, box, gas);
-        else k_visc<2, false><<<nb, 256, 0, st>>>(m, Q, FV, box, gas);
+    dim3 grid;
+    if (tiles) {
+        if (ntiles <= 0) return;
+        grid = dim3(ntiles);
     } else {
-        if (m.cart) k_visc<3, true><<<nb, 256, 0, st>>>(m, Q, FV, box, gas);
-        else k_visc<3, false><<<nb, 256, 0, st>>>(m, Q, FV, box, gas);
+        for (int k = 0; k < 3; ++k)
+            if (box.hi[k] < box.lo[k]) return;
+        grid = dim3((box.hi[0] - box.lo[0] + T3X) / T3X, (box.hi[1] - box.lo[1] + T3Y) / T3Y,
+                    (box.hi[2] - box.lo[2] + T3Z) / T3Z);
     }
+    if (m.cart) k_visc3d_x<true><<<grid, NT3, SMEMX, st>>>(m, Q, FV, box, tiles, gas);
+    else k_visc3d_x<false><<<grid, NT3, SMEMX, st>>>(m, Q, FV, box, tiles, gas);
 }
 
 void launch_rhs2d(const DevMesh& m, const double* Q, const Gas& g, const Epilogue& ep,
                   const DonorSet& ds, cudaStream_t st);
 
-bool rhs3d_split() {
-    static int v = -1;
-    if (v < 0) {
-        // default (MRAB_3D_SPLIT=0: k_visc3d_x + k_rhs3d): config 4 8.43 -> 8.08 ms/step,
-        // config 5 20.2 -> 16.8 ms/step
-        const char* e = getenv("MRAB_3D_SPLIT");
-        const char* d = getenv("MRAB_3D_DIRECT");
-        v = (e && e[0] == '0') || (d && d[0] == '1') ? 0 : 1;
+// tensor maps of the buffers one launch reads (k_rhs3z): the state (box + outer arms) and the
+// epilogue inputs; a buffer without a map (odd n0, or not one of the context's state-shaped
+// buffers) makes the kernel use element-wise cp.async for it
+static Z3Maps z3_maps_for(const DevMesh& m, const double* Q, const Epilogue& ep) {
+    Z3Maps mp;
+    std::memset(&mp, 0, sizeof(mp));
+    const Z3Table* t = m.z3t;
+    if (!t) return mp;
+    auto find = [&](const void* ptr) -> int {
+        for (int i = 0; i < t->n; ++i)
+            if (t->ptr[i] == ptr) return i;
+        return -1;
+    };
+    const int iq = find(Q);
+    if (iq >= 0) {
+        mp.box = t->box[iq];
+        mp.ox = t->ox[iq];
+        mp.oy = t->oy[iq];
+        mp.ok = 1;
     }
-    return v == 1;
+    if (ep.y_out) {
+        const int nst = std::min(ep.nsrc, 2);
+        const int ib = find(ep.base), i0 = nst > 0 ? find(ep.src[0]) : 0, i1 = nst > 1 ? find(ep.src[1]) : 0;
+        if (ib >= 0 && i0 >= 0 && i1 >= 0) {
+            mp.base = t->ep[ib];
+            if (nst > 0) mp.s0 = t->ep[i0];
+            if (nst > 1) mp.s1 = t->ep[i1];
+            mp.ep_ok = 1;
+        }
+    }
+    return mp;
 }
 
-void launch_flux3d(const DevMesh& m, const double* Q, double* FH, double* FV, const Gas& gas,
-                   cudaStream_t st) {
+bool z3_encode(const DevMesh& m, const void* buf, Z3Table& t) {
+    using Enc = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Enc enc = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return (Enc) nullptr;
+        return (Enc)fn;
+    }();
+    if (!enc || t.n >= Z3Table::kMax) return false;
+    // TMA: 16-byte aligned base and strides (even n0), every dimension < 2^31
+    if ((m.n[0] & 1) || ((uintptr_t)buf & 15)) return false;
+    const cuuint64_t dim[4] = {(cuuint64_t)m.n[0], (cuuint64_t)m.n[1], (cuuint64_t)m.n[2], 5};
+    const cuuint64_t str[3] = {(cuuint64_t)m.n[0] * 8, (cuuint64_t)m.n[0] * m.n[1] * 8, (cuuint64_t)m.npts * 8};
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    auto one = [&](CUtensorMap* out, cuuint32_t bx, cuuint32_t by) {
+        const cuuint32_t box[4] = {bx, by, 1, 5};
+        return enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void*>(buf), dim, str, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    };
+    const int i = t.n;
+    if (!one(&t.box[i], z3::BX, z3::BY) || !one(&t.ox[i], 2, z3::TY) || !one(&t.oy[i], z3::TX, z3::H) ||
+        !one(&t.ep[i], z3::TX, z3::TY))
+        return false;
+    t.ptr[i] = buf;
+    t.n = i + 1;
+    return true;
+}
+
+template <bool VISC, bool CART>
+static void launch_z3(const DevMesh& m, const double* Q, const Gas& gas, const Epilogue& ep,
+                      cudaStream_t st) {
+    static bool init = false;
+    if (!init) {
+        cudaFuncSetAttribute(k_rhs3z<VISC, CART>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)z3::SMEM);
+        init = true;
+    }
+    const int64_t W = (int64_t)((m.n[0] + z3::TX - 1) / z3::TX) * ((m.n[1] + z3::TY - 1) / z3::TY) * m.n[2];
+    // persistent: one CTA per SM (the kernel takes ~222 KB of shared memory), the (tile, plane)
+    // work split evenly between them
+    const unsigned grid = (unsigned)std::min<int64_t>(W, sm_count());
+    const Z3Maps maps = z3_maps_for(m, Q, ep);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(z3::NT);
+    cfg.dynamicSmemBytes = z3::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    if (ep.has_prio) {
+        at[0].id = cudaLaunchAttributePriority;
+        at[0].val.priority = ep.prio;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+    }
+    cudaLaunchKernelEx(&cfg, k_rhs3z<VISC, CART>, m, Q, gas, ep, maps);
+}
+
+void launch_flux3d(const DevMesh& m, const double* Q, const Gas& gas, cudaStream_t st) {
     static bool init = false;
     if (!init) {
         cudaFuncSetAttribute(k_flux3d<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEMX);
@@ -1580,105 +2012,53 @@ void launch_flux3d(const DevMesh& m, const double* Q, double* FH, double* FV, co
         init = true;
     }
     const dim3 grid(tile3_blocks(m.n));
+    double* FH = const_cast<double*>(m.fh);
     if (gas.viscous) {
-        if (m.cart) k_flux3d<true, true><<<grid, NT3, SMEMX, st>>>(m, Q, FH, FV, m.fvtile, gas);
-        else k_flux3d<true, false><<<grid, NT3, SMEMX, st>>>(m, Q, FH, FV, m.fvtile, gas);
+        if (m.cart) k_flux3d<true, true><<<grid, NT3, SMEMX, st>>>(m, Q, FH, m.fv, m.fvtile, gas);
+        else k_flux3d<true, false><<<grid, NT3, SMEMX, st>>>(m, Q, FH, m.fv, m.fvtile, gas);
     } else {
-        if (m.cart) k_flux3d<false, true><<<grid, NT3, SMEMX, st>>>(m, Q, FH, FV, m.fvtile, gas);
-        else k_flux3d<false, false><<<grid, NT3, SMEMX, st>>>(m, Q, FH, FV, m.fvtile, gas);
+        if (m.cart) k_flux3d<false, true><<<grid, NT3, SMEMX, st>>>(m, Q, FH, m.fv, m.fvtile, gas);
+        else k_flux3d<false, false><<<grid, NT3, SMEMX, st>>>(m, Q, FH, m.fv, m.fvtile, gas);
     }
 }
 
-void launch_rhs(int dim, const DevMesh& m, const double* Q, const double* FV, const Gas& gas,
-                const Epilogue& ep, const DonorSet& ds, cudaStream_t st) {
+template <bool VISC, bool CART>
+static void launch_div3d(const DevMesh& m, const double* Q, const Gas& gas, const Epilogue& ep, cudaStream_t st) {
+    static bool init = false;
+    if (!init) {
+        cudaFuncSetAttribute(k_rhs3d<VISC, CART, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM3);
+        init = true;
+    }
+    const dim3 grid(tile3_blocks(m.n));
+    k_rhs3d<VISC, CART, true><<<grid, NT3, SMEM3, st>>>(m, Q, m.fv, gas, ep, m.fh);
+}
+
+void launch_rhs(int dim, const DevMesh& m, const double* Q, const Gas& gas, const Epilogue& ep,
+                const DonorSet& ds, cudaStream_t st) {
     if (dim == 2) {
         launch_rhs2d(m, Q, gas, ep, ds, st);
         return;
     }
-    if (m.fh && rhs3d_split()) {
-        static bool init = false;
-        if (!init) {
-            cudaFuncSetAttribute(k_div3d<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEMD);
-            cudaFuncSetAttribute(k_div3d<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEMD);
-            cudaFuncSetAttribute(k_div3d<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEMD);
-            cudaFuncSetAttribute(k_div3d<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEMD);
-            init = true;
-        }
-        dim3 grid((m.n[0] + T3X - 1) / T3X, (m.n[1] + T3Y - 1) / T3Y, (m.n[2] + T3Z - 1) / T3Z);
-        static const int staged = [] {
-            const char* e = getenv("MRAB_DIV3D_STAGED");
-            return e ? atoi(e) : 0;
-        }();
-        if (staged) {
-            if (gas.viscous) {
-                if (m.cart) k_div3d<true, true><<<grid, NT3, SMEMD, st>>>(m, Q, m.fh, FV, gas, ep);
-                else k_div3d<true, false><<<grid, NT3, SMEMD, st>>>(m, Q, m.fh, FV, gas, ep);
-            } else {
-                if (m.cart) k_div3d<false, true><<<grid, NT3, SMEMD, st>>>(m, Q, m.fh, FV, gas, ep);
-                else k_div3d<false, false><<<grid, NT3, SMEMD, st>>>(m, Q, m.fh, FV, gas, ep);
-            }
-            return;
-        }
-        // the tiled RHS reading the precomputed fluxes (three register-staged passes)
-        const dim3 grid1(tile3_blocks(m.n));
-        static bool init3 = false;
-        if (!init3) {
-            cudaFuncSetAttribute(k_rhs3d<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM3);
-            cudaFuncSetAttribute(k_rhs3d<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM3);
-            cudaFuncSetAttribute(k_rhs3d<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM3);
-            cudaFuncSetAttribute(k_rhs3d<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM3);
-            init3 = true;
-        }
+    if (opts().z3_fused || !m.fh) {
+        // one-pass fused kernel (opt-in; also when the two-pass buffers are absent)
         if (gas.viscous) {
-            if (m.cart) k_rhs3d<true, true, true><<<grid1, NT3, SMEM3, st>>>(m, Q, FV, gas, ep, m.fh);
-            else k_rhs3d<true, false, true><<<grid1, NT3, SMEM3, st>>>(m, Q, FV, gas, ep, m.fh);
+            if (m.cart) launch_z3<true, true>(m, Q, gas, ep, st);
+            else launch_z3<true, false>(m, Q, gas, ep, st);
         } else {
-            if (m.cart) k_rhs3d<false, true, true><<<grid1, NT3, SMEM3, st>>>(m, Q, FV, gas, ep, m.fh);
-            else k_rhs3d<false, false, true><<<grid1, NT3, SMEM3, st>>>(m, Q, FV, gas, ep, m.fh);
+            if (m.cart) launch_z3<false, true>(m, Q, gas, ep, st);
+            else launch_z3<false, false>(m, Q, gas, ep, st);
         }
         return;
     }
-    static int direct = -1;
-    if (direct < 0) {
-        const char* e = getenv("MRAB_3D_DIRECT");
-        direct = e && e[0] == '1';
-    }
-    if (!direct) {
-        const size_t bytes = SMEM3;
-        static bool init[4] = {false, false, false, false};
-        const dim3 grid(tile3_blocks(m.n));
-#define MRAB_RHS3(V, C, I)                                                                          \
-    do {                                                                                            \
-        if (!init[I]) {                                                                             \
-            cudaFuncSetAttribute(k_rhs3d<V, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes); \
-            init[I] = true;                                                                         \
-        }                                                                                           \
-        k_rhs3d<V, C><<<grid, NT3, bytes, st>>>(m, Q, FV, gas, ep);                                 \
-    } while (0)
-        if (gas.viscous) {
-            if (m.cart) MRAB_RHS3(true, true, 0); else MRAB_RHS3(true, false, 1);
-        } else {
-            if (m.cart) MRAB_RHS3(false, true, 2); else MRAB_RHS3(false, false, 3);
-        }
-#undef MRAB_RHS3
-        return;
-    }
-    unsigned nb = blocks_for(m.npts, 256);
-#define MRAB_RHS(D, V, C) k_rhs<D, V, C><<<nb, 256, 0, st>>>(m, Q, FV, gas, ep)
-    if (dim == 2) {
-        if (gas.viscous) {
-            if (m.cart) MRAB_RHS(2, true, true); else MRAB_RHS(2, true, false);
-        } else {
-            if (m.cart) MRAB_RHS(2, false, true); else MRAB_RHS(2, false, false);
-        }
+    // two passes: contravariant fluxes, then divergence + SAT + epilogue
+    launch_flux3d(m, Q, gas, st);
+    if (gas.viscous) {
+        if (m.cart) launch_div3d<true, true>(m, Q, gas, ep, st);
+        else launch_div3d<true, false>(m, Q, gas, ep, st);
     } else {
-        if (gas.viscous) {
-            if (m.cart) MRAB_RHS(3, true, true); else MRAB_RHS(3, true, false);
-        } else {
-            if (m.cart) MRAB_RHS(3, false, true); else MRAB_RHS(3, false, false);
-        }
+        if (m.cart) launch_div3d<false, true>(m, Q, gas, ep, st);
+        else launch_div3d<false, false>(m, Q, gas, ep, st);
     }
-#undef MRAB_RHS
 }
 
 void launch_combine(int nc, const DevMesh& m, const Box& box, const double* base, int nsrc,
@@ -1693,7 +2073,26 @@ void launch_combine(int nc, const DevMesh& m, const Box& box, const double* base
     int64_t tot = (int64_t)(box.hi[0] - box.lo[0] + 1) * (box.hi[1] - box.lo[1] + 1) *
                   (box.hi[2] - box.lo[2] + 1);
     if (tot <= 0) return;
-    k_combine<<<blocks_for(tot, 256), 256, 0, st>>>(nc, m.npts, m.n[0], m.n[1], box, a, out);
+    k_combine<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(nc, m.npts, m.n[0], m.n[1], box, a, out);
+}
+
+void launch_interp(int viscous, const RecvList& rl, const DonorSet& ds, cudaStream_t st) {
+    if (rl.n <= 0) return;
+    if (rl.ginfo && rl.ngroups > 0) {
+        const size_t bytes = sizeof(double) * (viscous ? 17 : 5) * IBOXN;
+        static bool init = false;
+        if (!init) {
+            cudaFuncSetAttribute(k_interp3b<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double) * 17 * IBOXN));
+            cudaFuncSetAttribute(k_interp3b<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double) * 17 * IBOXN));
+            init = true;
+        }
+        if (viscous) k_interp3b<true><<<rl.ngroups, 128, bytes, st>>>(rl, ds);
+        else k_interp3b<false><<<rl.ngroups, 128, bytes, st>>>(rl, ds);
+    } else {
+        const unsigned nbq = (unsigned)((rl.n * 4 + 127) / 128);
+        if (viscous) k_interp3q<true><<<nbq, 128, 0, st>>>(rl, ds);
+        else k_interp3q<false><<<nbq, 128, 0, st>>>(rl, ds);
+    }
 }
 
 // "rhs blowup" check: any non-finite value in n doubles sets *flag
@@ -1721,38 +2120,4 @@ void launch_l2_scrub(void* a, void* b, size_t bytes, int tag, cudaStream_t st) {
     cudaMemsetAsync(a, tag & 0xff, bytes, st);
     k_scrub_read<<<148 * 8, 256, 0, st>>>((const double4*)b, bytes / sizeof(double4), (double*)a);
 }
-
-void launch_interp(int dim, int viscous, const RecvList& rl, const DonorSet& ds, cudaStream_t st) {
-    if (rl.n <= 0) return;
-    unsigned nb = blocks_for(rl.n, 128);
-    if (dim == 2) {
-        if (viscous) k_interp<2, true><<<nb, 128, 0, st>>>(rl, ds);
-        else k_interp<2, false><<<nb, 128, 0, st>>>(rl, ds);
-    } else {
-        static int quad = -1;
-        if (quad < 0) {
-            const char* e = getenv("MRAB_INTERP_QUAD");
-            quad = e ? atoi(e) : 1;
-        }
-        if (rl.ginfo && rl.ngroups > 0) {
-            const size_t bytes = sizeof(double) * (viscous ? 17 : 5) * IBOXN;
-            static bool init = false;
-            if (!init) {
-                cudaFuncSetAttribute(k_interp3b<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double) * 17 * IBOXN));
-                cudaFuncSetAttribute(k_interp3b<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double) * 17 * IBOXN));
-                init = true;
-            }
-            if (viscous) k_interp3b<true><<<rl.ngroups, 128, bytes, st>>>(rl, ds);
-            else k_interp3b<false><<<rl.ngroups, 128, bytes, st>>>(rl, ds);
-        } else if (quad) {
-            const unsigned nbq = (unsigned)((rl.n * 4 + 127) / 128);
-            if (viscous) k_interp3q<true><<<nbq, 128, 0, st>>>(rl, ds);
-            else k_interp3q<false><<<nbq, 128, 0, st>>>(rl, ds);
-        } else {
-            if (viscous) k_interp<3, true><<<nb, 128, 0, st>>>(rl, ds);
-            else k_interp<3, false><<<nb, 128, 0, st>>>(rl, ds);
-        }
-    }
-}
-
 }  // namespace mrab

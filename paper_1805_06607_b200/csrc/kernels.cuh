@@ -1,6 +1,7 @@
 // Device-side data structures and kernel launchers of libmrab.so (sm_100a, fp64).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -8,11 +9,30 @@
 
 namespace mrab {
 
+// TMA tensor maps of a mesh's state-shaped buffers (host table, built at mrab_create; 4-D
+// views [5][n2][n1][n0] with the boxes k_rhs3z loads)
+struct Z3Table {
+    static constexpr int kMax = 16;
+    int n = 0;
+    const void* ptr[kMax];
+    CUtensorMap box[kMax], ox[kMax], oy[kMax], ep[kMax];
+};
+// the maps one k_rhs3z launch uses (kernel parameter, __grid_constant__)
+struct Z3Maps {
+    CUtensorMap box, ox, oy, base, s0, s1;
+    int ok, ep_ok;
+};
+// host: add the tensor maps of one state-shaped buffer of mesh m to t (false if TMA cannot
+// describe it: odd n0, misaligned)
+struct DevMesh;
+bool z3_encode(const DevMesh& m, const void* buf, Z3Table& t);
+
 struct DevMesh {
     int n[3];
     int periodic[3];
     int face_bc[3][2];
     int64_t npts;
+    const Z3Table* z3t;        // host pointer: TMA tensor maps of the 3-D buffers (NULL = none)
     int cart;                  // constant diagonal metrics
     double cJ;                 // J = 1/J^-1 (Cartesian)
     double cM[3];              // M[k][k]    (Cartesian)
@@ -26,14 +46,15 @@ struct DevMesh {
     const int32_t* rdonor;     // [R] donor mesh of each receiver
     const int32_t* rbase;      // [R][3] donor stencil base
     const double* rw;          // [R][3][4] per-axis Lagrange weights
+    // 3-D two-pass RHS: contravariant fluxes [3][5][npts] (k_flux3d -> k_rhs3d), the mesh's
+    // Cartesian viscous-flux buffer, and the per-8^3-tile flag "F^V is read here" (SAT points)
+    const double* fh;
+    double* fv;
+    const uint8_t* fvtile;
     // 2-D: tile list of the RHS kernel, every tile once, non-interior tiles first;
     // bit 31 set = interior tile (see rhs2d_interior_tile); NULL = decide in the kernel
     const int32_t* tlist;
     int ntl;
-    // 3-D two-pass RHS: contravariant fluxes [3][5][npts] (k_flux3d -> k_div3d) and the per
-    // 8^3-tile flag "write the Cartesian viscous fluxes here" (SAT points / donor stencils)
-    const double* fh;
-    const uint8_t* fvtile;
 };
 
 struct Gas {
@@ -155,20 +176,18 @@ struct MeshTable {
 void launch_donor2d(const RecvTask& rt, const SrcSets& ss, const MeshTable& mt, const Gas& gas,
                     cudaStream_t st);
 
-void launch_visc(int dim, const DevMesh& m, const double* Q, double* FV, const Box& box,
-                 const Gas& gas, cudaStream_t st);
-// 3-D two-pass RHS (default): whether it is on, and its flux pass (writes m.fh, and F^V in the
-// flagged tiles); launch_rhs then runs the divergence pass
-bool rhs3d_split();
-void launch_flux3d(const DevMesh& m, const double* Q, double* FH, double* FV, const Gas& gas,
-                   cudaStream_t st);
-// 3-D: direct kernel reading FV and the gathered qhat/fvhat; 2-D: tiled kernel that forms
-// its own viscous fluxes and gathers donor data inline at its receivers from `ds`.
-void launch_rhs(int dim, const DevMesh& m, const double* Q, const double* FV, const Gas& gas,
-                const Epilogue& ep, const DonorSet& ds, cudaStream_t st);
+// 3-D Cartesian viscous fluxes F^V of a donor mesh where the gathers read them: on the 8^3
+// tiles of `box` (tiles == NULL) or on a list of 8^3 tiles (flat index, x fastest)
+void launch_visc(const DevMesh& m, const double* Q, double* FV, const Box& box, const int32_t* tiles,
+                 int ntiles, const Gas& gas, cudaStream_t st);
+// 3-D: the fused one-pass RHS kernel k_rhs3z (reads the gathered qhat/fvhat at its receivers);
+// 2-D: the tiled kernel that forms its own viscous fluxes and gathers donor data inline at its
+// receivers from `ds`.
+void launch_rhs(int dim, const DevMesh& m, const double* Q, const Gas& gas, const Epilogue& ep,
+                const DonorSet& ds, cudaStream_t st);
 void launch_combine(int nc, const DevMesh& m, const Box& box, const double* base, int nsrc,
                     const double* const* src, const double* csrc, double* out, cudaStream_t st);
-void launch_interp(int dim, int viscous, const RecvList& rl, const DonorSet& ds, cudaStream_t st);
+void launch_interp(int viscous, const RecvList& rl, const DonorSet& ds, cudaStream_t st);
 void upload_stencil_rows();
 // L2 scrub for cold-cache timing: write `a` (bytes) then stream-read `b` (bytes) so that the
 // L2 ends up holding clean lines of an unrelated buffer (no dirty write-backs later).

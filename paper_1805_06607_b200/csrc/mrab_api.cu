@@ -47,8 +47,11 @@ struct MeshDev {
     double* Q[2] = {nullptr, nullptr};
     double* ring[kMaxHist] = {nullptr};
     double* FV = nullptr;
-    double* FH = nullptr;         // 3-D: contravariant fluxes [3][5][N] (two-pass RHS)
-    uint8_t* fvtile = nullptr;    // 3-D: per 8^3 tile, write F^V there (SAT points, donor stencils)
+    int32_t* fvlist = nullptr;    // 3-D: the 8^3 tiles holding donor-stencil points (F^V there)
+    int nfv = 0;
+    double* FH = nullptr;         // 3-D two-pass RHS: contravariant fluxes [3][5][N]
+    uint8_t* fvtile = nullptr;    // 3-D two-pass RHS: per 8^3 tile, SAT points inside (F^V written)
+    Z3Table z3tab;                // 3-D: TMA tensor maps of the state-shaped buffers
     double* dstate = nullptr;
     double* kbuf[4] = {nullptr, nullptr, nullptr, nullptr};
     double* ystage = nullptr;
@@ -152,11 +155,13 @@ static size_t plan_bytes(const Plan& P, bool dry, mrab_ctx* ctx, Bump* bump, boo
         }
         if (d == 3) {
             const size_t nt = (size_t)((m.n[0] + 7) / 8) * ((m.n[1] + 7) / 8) * ((m.n[2] + 7) / 8);
-            void* a = take((size_t)15 * N * sizeof(double));
-            void* b = take(nt);
+            void* b = take(nt * sizeof(int32_t));
+            void* f = P.opt.z3_fused ? nullptr : take((size_t)15 * N * sizeof(double));
+            void* t = take(nt);
             if (D) {
-                D->FH = (double*)a;
-                D->fvtile = (uint8_t*)b;
+                D->fvlist = (int32_t*)b;
+                D->FH = (double*)f;
+                D->fvtile = (uint8_t*)t;
             }
         }
         {
@@ -278,7 +283,7 @@ static void issue_interp(mrab_ctx* c, int g, const double* const* state_of, bool
     rl.gorder = D.gorder;
     rl.ginfo = D.ginfo;
     rl.ngroups = D.ngroups;
-    launch_interp(P.dim, P.viscous, rl, make_ds(c, state_of), c->st);
+    launch_interp(P.viscous, rl, make_ds(c, state_of), c->st);
     c->launch_counter++;
 }
 
@@ -349,24 +354,19 @@ static SrcSet plain_states(mrab_ctx* c, const double* const* state_of) {
 static void issue_visc(mrab_ctx* c, int g, const double* Q, const Box& box) {
     const Plan& P = *c->P;
     if (!P.viscous) return;
-    launch_visc(P.dim, c->md[g].dm, Q, c->md[g].FV, box, c->gas, c->st);
+    launch_visc(c->md[g].dm, Q, c->md[g].FV, box, nullptr, 0, c->gas, c->st);
     c->launch_counter++;
 }
 
-// viscous fluxes a stepping mesh must provide: the 3-D direct RHS kernel reads them on the
-// whole mesh; the 2-D tiled kernel computes its own, so only the donor box is needed there.
+// 3-D: Cartesian viscous fluxes of donor mesh g at its current (stepping) state, on the 8^3
+// tiles holding the donor stencils the gathers read (the fused RHS kernel keeps its own F^V
+// on chip)
 static void issue_step_visc(mrab_ctx* c, int g, const double* Q) {
     const Plan& P = *c->P;
-    const MeshPlan& mp = P.meshes[g];
-    if (P.dim == 3 && rhs3d_split()) {
-        // two-pass 3-D RHS: the flux pass (contravariant fluxes everywhere, F^V where read)
-        MeshDev& D = c->md[g];
-        launch_flux3d(D.dm, Q, D.FH, D.FV, c->gas, c->st);
-        c->launch_counter++;
-    } else if (P.dim == 3)
-        issue_visc(c, g, Q, whole_box(mp));
-    else if (mp.is_donor)
-        issue_visc(c, g, Q, make_box(mp.fv_lo, mp.fv_hi));
+    MeshDev& D = c->md[g];
+    if (!P.viscous || P.dim != 3 || D.nfv == 0) return;
+    launch_visc(D.dm, Q, D.FV, Box{}, D.fvlist, D.nfv, c->gas, c->st);
+    c->launch_counter++;
 }
 
 // every mesh evaluated at the given states (RK stages, the rhs hook): donor data for all
@@ -384,7 +384,7 @@ static void issue_all_donors(mrab_ctx* c, const double* const* state_of) {
 
 static void issue_rhs(mrab_ctx* c, int g, const double* Q, const Epilogue& ep,
                       const double* const* state_of) {
-    launch_rhs(c->P->dim, c->md[g].dm, Q, c->md[g].FV, c->gas, ep, make_ds(c, state_of), c->st);
+    launch_rhs(c->P->dim, c->md[g].dm, Q, c->gas, ep, make_ds(c, state_of), c->st);
     c->launch_counter++;
 }
 
@@ -447,7 +447,9 @@ static void issue_macro_step(mrab_ctx* c) {
                 }
                 const double* Q = D.Q[c->book.cur[g]];
                 state_of[g] = Q;
-                issue_step_visc(c, g, Q);
+                bool read_now = false;
+                for (int h = 0; h < G; ++h) read_now = read_now || (h != g && stepping[h] && P.donor_of[g][h]);
+                if (read_now) issue_step_visc(c, g, Q);
             } else if (partial[g]) {
                 const MeshPlan& mp = P.meshes[g];
                 const int jj = j % mp.s;
@@ -692,7 +694,7 @@ static void issue_macro_step_dag2d(mrab_ctx* c) {
                 Epilogue e1 = ep;
                 e1.tiles = D.tiles;
                 e1.ntiles = D.ncrit;
-                launch_rhs(2, dm, ep.base, D.FV, c->gas, e1, ds, c->side[g]);
+                launch_rhs(2, dm, ep.base, c->gas, e1, ds, c->side[g]);
                 last_crit[g] = dag_done(c, g);
                 dag_wait(c, gb, pre);
                 Epilogue e2 = ep;
@@ -700,12 +702,12 @@ static void issue_macro_step_dag2d(mrab_ctx* c) {
                 e2.ntiles = D.nbulk;
                 e2.persist = c->bulk_ctas;
                 e2.trace_tag = (3 << 12) | (g << 8) | (j & 0xff);
-                launch_rhs(2, dm, ep.base, D.FV, c->gas, e2, ds, c->side[gb]);
+                launch_rhs(2, dm, ep.base, c->gas, e2, ds, c->side[gb]);
                 c->launch_counter += 2;
                 dag_wait(c, g, dag_done(c, gb));
                 last_full[g] = dag_done(c, g);
             } else {
-                launch_rhs(2, dm, ep.base, D.FV, c->gas, ep, ds, c->side[g]);
+                launch_rhs(2, dm, ep.base, c->gas, ep, ds, c->side[g]);
                 c->launch_counter++;
                 last_full[g] = dag_done(c, g);
                 last_crit[g] = last_full[g];
@@ -951,21 +953,10 @@ mrab_status mrab_create(const mrab_plan* plan, const double* const* q0, void* d_
         }
         CK(cudaMemcpy(D.cls, m.cls.data(), N * sizeof(uint16_t), cudaMemcpyHostToDevice));
         if (d == 3) {
-            // F^V is read at SAT points (the viscous penalty) and at donor stencils (gathers)
+            // F^V is read by the gathers at the exact donor stencils (4^3 points) of every
+            // receiver this mesh donates to: the 8^3 tiles holding them
             const int tx = (m.n[0] + 7) / 8, ty = (m.n[1] + 7) / 8, tz = (m.n[2] + 7) / 8;
             std::vector<uint8_t> fl((size_t)tx * ty * tz, 0);
-            for (int k = 0; k < m.n[2]; ++k)
-                for (int jj = 0; jj < m.n[1]; ++jj)
-                    for (int i = 0; i < m.n[0]; ++i) {
-                        const unsigned cc = m.cls[m.idx(i, jj, k)];
-                        bool need = false;
-                        for (int a = 0; a < 3; ++a) {
-                            const int cl = (cc >> (4 * a)) & 15;
-                            need = need || cl == CLS_L0 || cl == CLS_R0;
-                        }
-                        if (need) fl[(size_t)(i / 8) + tx * ((size_t)(jj / 8) + (size_t)ty * (k / 8))] = 1;
-                    }
-            // the exact donor stencils (4^3 points) of every receiver this mesh donates to
             for (size_t h = 0; h < P.meshes.size(); ++h) {
                 const MeshPlan& mh = P.meshes[h];
                 for (size_t r = 0; r < mh.rdonor.size(); ++r) {
@@ -980,7 +971,26 @@ mrab_status mrab_create(const mrab_plan* plan, const double* const* q0, void* d_
                             }
                 }
             }
-            CK(cudaMemcpy(D.fvtile, fl.data(), fl.size(), cudaMemcpyHostToDevice));
+            std::vector<int32_t> lst;
+            for (size_t t = 0; t < fl.size(); ++t)
+                if (fl[t]) lst.push_back((int32_t)t);
+            D.nfv = (int)lst.size();
+            if (!lst.empty())
+                CK(cudaMemcpy(D.fvlist, lst.data(), lst.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+            // two-pass RHS: the 8^3 tiles holding SAT points (k_flux3d writes F^V there)
+            std::vector<uint8_t> st((size_t)tx * ty * tz, 0);
+            for (int k = 0; k < m.n[2]; ++k)
+                for (int jj = 0; jj < m.n[1]; ++jj)
+                    for (int i = 0; i < m.n[0]; ++i) {
+                        const unsigned cc = m.cls[m.idx(i, jj, k)];
+                        bool need = false;
+                        for (int a = 0; a < 3; ++a) {
+                            const int cl = (cc >> (4 * a)) & 15;
+                            need = need || cl == CLS_L0 || cl == CLS_R0;
+                        }
+                        if (need) st[(size_t)(i / 8) + tx * ((size_t)(jj / 8) + (size_t)ty * (k / 8))] = 1;
+                    }
+            CK(cudaMemcpy(D.fvtile, st.data(), st.size(), cudaMemcpyHostToDevice));
         }
         CK(cudaMemcpy(D.recv_slot, m.recv_slot.data(), N * sizeof(int32_t), cudaMemcpyHostToDevice));
         if (R) {
@@ -1016,8 +1026,6 @@ mrab_status mrab_create(const mrab_plan* plan, const double* const* q0, void* d_
         dm.rdonor = D.rdonor;
         dm.rbase = D.rbase;
         dm.rw = D.rw;
-        dm.fh = D.FH;
-        dm.fvtile = D.fvtile;
         if (d == 2) {
             // tile lists: tiles meeting the donor state box first (critical), then the rest
             int tx, ty;
@@ -1047,6 +1055,18 @@ mrab_status mrab_create(const mrab_plan* plan, const double* const* q0, void* d_
             dm.ntl = (int)slow.size();
         }
         dm.nrecv = (int64_t)R;
+        dm.z3t = nullptr;
+        dm.fh = D.FH;
+        dm.fv = D.FV;
+        dm.fvtile = D.fvtile;
+        if (d == 3) {
+            // TMA descriptors of every buffer the fused 3-D kernel reads as a state or as an
+            // epilogue input (a buffer TMA cannot describe falls back to cp.async)
+            const double* bufs[] = {D.Q[0], D.Q[1], D.ystage, D.dstate, D.kbuf[0], D.kbuf[1], D.kbuf[2], D.kbuf[3]};
+            for (const double* b : bufs) z3_encode(dm, b, D.z3tab);
+            for (int k = 0; k < P.history_m; ++k) z3_encode(dm, D.ring[k], D.z3tab);
+            dm.z3t = D.z3tab.n ? &D.z3tab : nullptr;
+        }
         c->book.head[g] = P.history_m - 1;   // empty ring: the first push goes to slot 0
         c->book.cur[g] = 0;
         c->book.pending[g] = 0;
@@ -1302,6 +1322,8 @@ mrab_status mrab_time_kernel(mrab_ctx* c, int kernel, int mesh, int reps, int fl
     // compiled for 32 x 16 tiles only (variant 0)
     if (kernel >= 3 && (d != 2 || (kernel == 3 && rhs2d_variant_for(mp.n, mp.cartesian ? 1 : 0) != 0)))
         return fail(MRAB_E_INVALID, "kernel 3-5 are 2-D diagnostics; 3 needs the 32x16 tile variant");
+    if (kernel == 1 && (d != 3 || !P.viscous))
+        return fail(MRAB_E_INVALID, "kernel 1 (donor viscous fluxes) is a 3-D viscous kernel");
     CK(cudaStreamSynchronize(c->st));
     void* flush = nullptr;
     const size_t fbytes = (size_t)256 << 20;
@@ -1322,6 +1344,7 @@ mrab_status mrab_time_kernel(mrab_ctx* c, int kernel, int mesh, int reps, int fl
             ep.r_out = D.kbuf[0];
             ep.y_out = D.kbuf[1];
             ep.base = Q;
+            ep.trace = d == 3 ? c->trace : nullptr;   // 3-D: phase-cycle accounting (profiling build)
             ep.c_new = P.h * mp.s * P.coef[mesh][mp.s][m - 1];
             ep.nsrc = m - 1;
             for (int k = 0; k < m - 1; ++k) {
@@ -1339,16 +1362,13 @@ mrab_status mrab_time_kernel(mrab_ctx* c, int kernel, int mesh, int reps, int fl
                 rhs2d_tile_shape_for(mp.n, mp.cartesian ? 1 : 0, &tx, &ty);
                 Nk = (double)ep.ntiles * tx * ty;
             }
-            if (d == 3 && rhs3d_split() && kernel == 0)
-                launch_flux3d(D.dm, Q, D.FH, D.FV, c->gas, c->st);   // the RHS is both passes
-            launch_rhs(d, D.dm, Q, D.FV, c->gas, ep, make_ds(c, state_of.data()), c->st);
+            launch_rhs(d, D.dm, Q, c->gas, ep, make_ds(c, state_of.data()), c->st);
             // Q read, R written, (m-1) ring reads, state written, metrics if curvilinear
             bytes = 8.0 * Nk * (nc * (m + 2) + (mp.cartesian ? 0 : 1 + d * d));
         } else if (kernel == 1) {
-            // the box the MRAB step uses: whole mesh (3-D), donor box (2-D)
-            Box b = (d == 3 || !mp.is_donor) ? whole_box(mp) : make_box(mp.fv_lo, mp.fv_hi);
-            launch_visc(d, D.dm, Q, D.FV, b, c->gas, c->st);
-            const double Nb = (double)(b.hi[0] - b.lo[0] + 1) * (b.hi[1] - b.lo[1] + 1) * (b.hi[2] - b.lo[2] + 1);
+            // 3-D donor viscous fluxes on the donor-stencil tiles of a stepping donor
+            launch_visc(D.dm, Q, D.FV, Box{}, D.fvlist, D.nfv, c->gas, c->st);
+            const double Nb = 512.0 * D.nfv;
             // Q read, Cartesian viscous fluxes written, metrics if curvilinear
             bytes = 8.0 * Nb * (nc + d * (d + 1) + (mp.cartesian ? 0 : 1 + d * d));
         } else {

@@ -33,6 +33,7 @@ struct Options {
     int donor_staged = 1;     // MRAB_DONOR_STAGED: region-staged 2-D donor gather
     int interp_box = 1;       // MRAB_INTERP_BOX: 3-D gather staged per donor box
     int interp_quad = 1;      // MRAB_INTERP_QUAD: four lanes per receiver (per-receiver 3-D gather)
+    int z3_fused = 0;         // MRAB_3D_FUSED: 3-D RHS in one pass (k_rhs3z) instead of two
 };
 Options read_options();
 const Options& opts();

@@ -1,7 +1,7 @@
-"""GPU parity of the non-default kernel paths (selected by environment variables that are read
-once per process, so each case runs in a subprocess): the 3-D single-pass RHS (k_visc3d_x +
-k_rhs3d), the 3-D staged divergence kernel, the per-receiver 3-D gather, the 2-D general tile path for every tile (no lean
-path), and the serial (non-overlapped) 2-D schedule.  Each must match the oracle like the
+"""GPU parity of the non-default kernel paths (selected by the MRAB_* switches, read into the
+plan's Options at mrab_plan_create; each case runs in a subprocess): the one-pass fused 3-D
+RHS (k_rhs3z: z-marching tiles, TMA-staged planes), the per-receiver 3-D gather, the 2-D general tile path for every tile (no lean path), and the serial
+(non-overlapped) 2-D schedule with uncapped curvilinear tiles.  Each must match the oracle like the
 default path (states after N macro steps to 1e-10, RHS to 1e-10)."""
 import os
 import subprocess
@@ -39,9 +39,8 @@ print("ok", rel, rel2)
 """
 
 CASES = [
-    (4, {"MRAB_3D_SPLIT": "0"}),
-    (5, {"MRAB_3D_SPLIT": "0"}),
-    (4, {"MRAB_DIV3D_STAGED": "1"}),
+    (4, {"MRAB_3D_FUSED": "1"}),
+    (5, {"MRAB_3D_FUSED": "1"}),
     (5, {"MRAB_INTERP_BOX": "0"}),
     (3, {"MRAB_LEAN": "0"}),
     (3, {"MRAB_TILE_FLAGS": "0"}),

@@ -136,25 +136,6 @@ def test_nonfinite_reported():
     ctx.close()
 
 
-# The row-marching 2-D kernel (kernels2d_march.cu) is chosen per mesh at create time
-# (MRAB_MARCH: 0 = never, 1 = meshes >= MRAB_MARCH_MIN points, 2 = every viscous 2-D mesh).
-# Forced on the test-size viscous configs, with short work items (MRAB_MARCH_L) so that lead-in
-# rows, strip edges, periodic wrap, walls, holes and overset faces all cross item boundaries.
-@pytest.mark.parametrize("cid", [2, 3])
-@pytest.mark.parametrize("rows", ["0", "5", "64"])
-def test_rhs_parity_march(cid, rows, monkeypatch):
-    monkeypatch.setenv("MRAB_MARCH", "2")
-    monkeypatch.setenv("MRAB_MARCH_L", rows)
-    test_rhs_parity(cid)
-
-
-@pytest.mark.parametrize("cid,kw", [(2, {}), (3, {"sr": 4}), (3, {"sr": 2})])
-def test_state_parity_march(cid, kw, monkeypatch):
-    monkeypatch.setenv("MRAB_MARCH", "2")
-    monkeypatch.setenv("MRAB_MARCH_L", "7")
-    test_state_parity(cid, kw)
-
-
 @pytest.mark.parametrize("cid,kw", [(3, {"sr": 4}), (2, {})])
 def test_overlapped_schedule_is_bitwise_serial(cid, kw, monkeypatch):
     """The overlapped macro step (critical/bulk split of the slow mesh on two streams, node
