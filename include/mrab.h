@@ -57,7 +57,33 @@ typedef struct {
     const double* xyz;       /* host [dim][n2][n1][n0] node coordinates                       */
     int priority;            /* hole-cutting priority: higher cuts lower (R17)                */
     int step_multiple;       /* s_g: finest micro steps per step of this mesh (R8)           */
+    /* Optional caller-supplied setup (NULL = the library builds it):
+     *   metrics  host [1 + dim*dim][n2][n1][n0]: [0] = J^-1, [1 + kappa*dim + i] = M[kappa][i]
+     *            = J^-1 d kappa / d x_i; J^-1 must be > 0 at every active point
+     *            (else MRAB_E_INVALID).  Used verbatim (a mesh whose terms are constant and
+     *            diagonal to 1e-10 relative is still run with the Cartesian kernels).
+     *   iblank   host [n2][n1][n0], 0 = hole, nonzero = active (P:232-236 hole cutting).
+     *            Used verbatim; segments (R2) and receivers (segment ends facing a hole or an
+     *            overset face) are derived from it (MRAB_E_SEGMENT if a segment is
+     *            shorter than 8 points). */
+    const double* metrics;
+    const int8_t* iblank;
 } mrab_mesh_desc;
+
+/* One overset receiver and its donor stencil ("donor cells", reading R17):
+ * receiver point recv_index (flat, i fastest) of mesh recv_mesh takes its interpolated state
+ * from the 4^dim stencil of mesh donor_mesh with lowest corner base[] (index order; wrapped
+ * into [0, n) in periodic directions; base[2] = 0 in 2-D) and per-axis Lagrange weights
+ * w[axis][a] (qhat = sum_abc w[0][a] w[1][b] w[2][c] q[base + (a, b, c)];
+ * w[2] = (1, 0, 0, 0) in 2-D). */
+typedef struct {
+    int32_t recv_mesh;
+    int32_t donor_mesh;
+    int64_t recv_index;
+    int32_t base[3];
+    int32_t reserved;        /* 0 */
+    double w[3][4];
+} mrab_donor;
 
 typedef struct {
     int dim;
@@ -70,6 +96,14 @@ typedef struct {
     int order_n;             /* AB order n                                      */
     int history_m;           /* history length m >= n; m > n = min-norm extended AB */
     double h;                /* finest micro step; mesh g steps h_g = s_g h                 */
+    /* Optional caller-supplied donor table (n_donors = 0 / donors = NULL: the library
+     * searches the donors, R17).  When given it must hold exactly one entry per receiver
+     * of every mesh (the receivers follow from the blanking): a missing receiver is
+     * MRAB_E_ORPHAN; a point that is not a receiver, a duplicate, a donor stencil that
+     * leaves the donor mesh or touches a hole, or donor_mesh == recv_mesh is MRAB_E_INVALID.
+     * Weights are used verbatim. */
+    int64_t n_donors;
+    const mrab_donor* donors;
 } mrab_problem;
 
 typedef struct mrab_plan mrab_plan;   /* host setup: tables, metrics, coefficients         */
@@ -89,6 +123,21 @@ mrab_status mrab_ab_weights(const double* nodes, int m, int n, double a, double 
 mrab_status mrab_plan_create(const mrab_problem* problem, mrab_plan** out);
 void        mrab_plan_destroy(mrab_plan* plan);
 
+/* The overset setup alone (P:227-252 phases: hole cutting, receiver identification, donor
+ * search, interpolation weights; reading R17), honouring any caller-supplied iblank / donors
+ * in `problem` exactly as mrab_plan_create does.  Outputs are allocated by the library and
+ * released with mrab_free:
+ *   *iblank_out  int8 [sum_g n_points(g)], the meshes' blanking concatenated in mesh order
+ *                (1 active / 0 hole);
+ *   *donors_out  mrab_donor [*n_out], receivers of mesh 0 (ascending point), then mesh 1, ...
+ * Feeding both back through mrab_mesh_desc.iblank / mrab_problem.donors reproduces the plan
+ * bit for bit.  Errors: those of mrab_plan_create; outputs untouched on failure. */
+mrab_status mrab_overset_build(const mrab_problem* problem, int8_t** iblank_out,
+                               mrab_donor** donors_out, int64_t* n_out);
+
+/* Release an array returned by mrab_overset_build (NULL is a no-op). */
+void        mrab_free(void* p);
+
 /* Sizes of mesh `mesh` in a plan: points, active points, receivers (any may be NULL). */
 mrab_status mrab_plan_info(const mrab_plan* plan, int mesh, int64_t* n_points,
                            int64_t* n_active, int64_t* n_receivers);
@@ -102,6 +151,14 @@ mrab_status mrab_plan_info(const mrab_plan* plan, int mesh, int64_t* n_points,
 mrab_status mrab_plan_get_tables(const mrab_plan* plan, int mesh, int8_t* iblank,
                                  int64_t* recv_point, int32_t* recv_donor,
                                  int32_t* recv_base, double* recv_weights);
+
+/* SAT face flags of `mesh` (P:279-299 eq:int, P:292-294 edges/corners): flags [n_points],
+ * bit 2*kappa set where the point is the kappa-min end of a segment (penalty side "+"),
+ * bit 2*kappa+1 where it is the kappa-max end (side "-"); the penalty type follows from the
+ * neighbour across that end: a hole or an overset face = interface (qhat interpolated), a
+ * far-field / wall face = the physical SAT (R16).  0 at interior and hole points and across
+ * periodic seams. */
+mrab_status mrab_plan_get_face_flags(const mrab_plan* plan, int mesh, uint8_t* flags);
 
 /* Metric terms of `mesh` (reading R3): jinv [n_points] = J^-1, M [dim][dim][n_points] with
  * M[kappa][i] = J^-1 d kappa / d x_i (zeros at holes). */

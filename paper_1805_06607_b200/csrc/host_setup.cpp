@@ -281,6 +281,17 @@ static void d1_host(const MeshPlan& m, int k, const double* f, double jump, cons
 // the computed arrays by less than that, far inside the 1e-10 parity bar.
 static const double kCartTol = 1e-10;
 
+static bool finish_metrics(MeshPlan& m, Error& err);
+
+// caller-supplied metric terms ([0] = J^-1, [1 + kappa*d + i] = M[kappa][i]; mrab.h)
+static bool copy_metrics(MeshPlan& m, const double* src, Error& err) {
+    const int d = m.dim;
+    const int64_t N = m.npts;
+    m.jinv.assign(src, src + N);
+    m.M.assign(src + N, src + (size_t)(1 + d * d) * N);
+    return finish_metrics(m, err);
+}
+
 static bool compute_metrics(MeshPlan& m, Error& err) {
     const int d = m.dim;
     const int64_t N = m.npts;
@@ -321,7 +332,14 @@ static bool compute_metrics(MeshPlan& m, Error& err) {
                         a02 * (a10 * a21 - a11 * a20);
         }
     }
-    // positivity and Cartesian detection
+    return finish_metrics(m, err);
+}
+
+// positivity and Cartesian detection
+static bool finish_metrics(MeshPlan& m, Error& err) {
+    const int d = m.dim;
+    const int64_t N = m.npts;
+    auto Mp = [&](int kap, int i) { return &m.M[((size_t)kap * d + i) * N]; };
     int64_t first = -1;
     for (int64_t p = 0; p < N; ++p) {
         if (!m.active[p]) continue;
@@ -683,10 +701,60 @@ static void point_xyz(const MeshPlan& m, int64_t p, double* X) {
     for (int c = 0; c < m.dim; ++c) X[c] = m.xyz[(size_t)c * m.npts + p];
 }
 
-static bool build_overset(Plan& P, Error& err) {
+// Caller-supplied donor entries of receiving mesh g (mrab.h mrab_problem.donors): exactly one
+// per receiver; stencils inside the donor mesh and all active; weights verbatim.
+static bool take_donors(Plan& P, const mrab_problem* pb, int g, const std::vector<int64_t>& pts,
+                        std::vector<uint8_t>& todo, Error& err) {
+    MeshPlan& m = P.meshes[g];
     const int G = (int)P.meshes.size();
+    std::vector<int32_t> slot(m.npts, -1);
+    for (size_t r = 0; r < pts.size(); ++r) slot[pts[r]] = (int32_t)r;
+    auto bad = [&](int64_t e, const std::string& why) {
+        err = {MRAB_E_INVALID, "donor entry " + std::to_string(e) + ": " + why};
+        return false;
+    };
+    for (int64_t e = 0; e < pb->n_donors; ++e) {
+        const mrab_donor& dn = pb->donors[e];
+        if (dn.recv_mesh < 0 || dn.recv_mesh >= G) return bad(e, "recv_mesh out of range");
+        if (dn.recv_mesh != g) continue;
+        if (dn.donor_mesh < 0 || dn.donor_mesh >= G || dn.donor_mesh == g)
+            return bad(e, "donor_mesh out of range or equal to recv_mesh");
+        if (dn.recv_index < 0 || dn.recv_index >= m.npts || slot[dn.recv_index] < 0)
+            return bad(e, "recv_index is not a receiver of mesh " + std::to_string(g));
+        const int64_t r = slot[dn.recv_index];
+        if (!todo[r]) return bad(e, "duplicate receiver");
+        const MeshPlan& ma = P.meshes[dn.donor_mesh];
+        int s[3] = {dn.base[0], dn.base[1], ma.dim == 3 ? dn.base[2] : 0};
+        int64_t st[64];
+        if (!stencil_points(ma, s, st)) return bad(e, "donor stencil leaves the donor mesh");
+        for (int a = 0; a < (ma.dim == 2 ? 16 : 64); ++a)
+            if (!ma.active[st[a]]) return bad(e, "donor stencil touches a hole");
+        m.rdonor[r] = dn.donor_mesh;
+        for (int k = 0; k < 3; ++k) {
+            int v = s[k];
+            if (k < ma.dim && ma.periodic[k]) v = ((v % ma.n[k]) + ma.n[k]) % ma.n[k];
+            m.rbase[(size_t)r * 3 + k] = v;
+        }
+        for (int k = 0; k < 3; ++k)
+            for (int a = 0; a < 4; ++a) m.rw[(size_t)r * 12 + k * 4 + a] = dn.w[k][a];
+        if (ma.dim == 2) {
+            double* w = &m.rw[(size_t)r * 12 + 8];
+            w[0] = 1.0;
+            w[1] = w[2] = w[3] = 0.0;
+        }
+        todo[r] = 0;
+    }
+    return true;
+}
+
+static bool build_overset(Plan& P, const mrab_problem* pb, Error& err) {
+    const int G = (int)P.meshes.size();
+    const bool given_donors = pb->n_donors > 0 && pb->donors;
+    bool all_blank = true;
+    for (int g = 0; g < G; ++g) all_blank = all_blank && pb->meshes[g].iblank;
     std::vector<CellIndex> ci(G);
-    for (int g = 0; g < G; ++g) build_cell_index(P.meshes[g], ci[g]);
+    if (!(all_blank && given_donors))          // the cell index serves the geometric searches
+        for (int g = 0; g < G; ++g) build_cell_index(P.meshes[g], ci[g]);
     std::vector<int> order_all(G);
     std::iota(order_all.begin(), order_all.end(), 0);
     auto prio_order = [&](int exclude) {
@@ -704,6 +772,7 @@ static bool build_overset(Plan& P, Error& err) {
         MeshPlan& ma = P.meshes[A];
         inside[A].assign(ma.npts, 0);
         prot[A].assign(ma.npts, 0);
+        if (pb->meshes[A].iblank) continue;    // caller-supplied blanking (mrab.h)
         for (int B = 0; B < G; ++B) {
             if (B == A) continue;
             const MeshPlan& mb = P.meshes[B];
@@ -727,7 +796,7 @@ static bool build_overset(Plan& P, Error& err) {
         }
     }
     // 2. protect the donor stencils of overset-face points
-    for (int B = 0; B < G; ++B) {
+    for (int B = 0; B < G && !all_blank; ++B) {
         const MeshPlan& mb = P.meshes[B];
         std::vector<int64_t> fpts;
         for (int64_t p = 0; p < mb.npts; ++p) {
@@ -744,6 +813,7 @@ static bool build_overset(Plan& P, Error& err) {
         std::vector<uint8_t> todo(fpts.size(), 1);
         for (int A : prio_order(B)) {
             const MeshPlan& ma = P.meshes[A];
+            const bool mark = !pb->meshes[A].iblank;   // caller blanking: no protection marks
             std::vector<std::vector<int64_t>> marks(fpts.size());
 #pragma omp parallel for schedule(dynamic, 64)
             for (int64_t r = 0; r < (int64_t)fpts.size(); ++r) {
@@ -754,7 +824,7 @@ static bool build_overset(Plan& P, Error& err) {
                 int s[3];
                 stencil_base(ma, xi, s);
                 int64_t st[64];
-                if (stencil_points(ma, s, st)) marks[r].assign(st, st + (ma.dim == 2 ? 16 : 64));
+                if (mark && stencil_points(ma, s, st)) marks[r].assign(st, st + (ma.dim == 2 ? 16 : 64));
                 todo[r] = 0;
             }
             for (auto& v : marks)
@@ -765,8 +835,12 @@ static bool build_overset(Plan& P, Error& err) {
     for (int g = 0; g < G; ++g) {
         MeshPlan& m = P.meshes[g];
         m.active.assign(m.npts, 1);
-        for (int64_t p = 0; p < m.npts; ++p)
-            if (inside[g][p] && !prot[g][p]) m.active[p] = 0;
+        if (const int8_t* ib = pb->meshes[g].iblank) {
+            for (int64_t p = 0; p < m.npts; ++p) m.active[p] = ib[p] != 0;
+        } else {
+            for (int64_t p = 0; p < m.npts; ++p)
+                if (inside[g][p] && !prot[g][p]) m.active[p] = 0;
+        }
         if (!compute_segments(m, err)) {
             err.msg = "mesh " + std::to_string(g) + ": " + err.msg;
             return false;
@@ -801,6 +875,9 @@ static bool build_overset(Plan& P, Error& err) {
         m.rbase.assign((size_t)R * 3, 0);
         m.rw.assign((size_t)R * 12, 0.0);
         std::vector<uint8_t> todo(R, 1);
+        if (given_donors) {
+            if (!take_donors(P, pb, g, pts, todo, err)) return false;
+        } else {
         // shift order: sum|delta| ascending, then lexicographic (axis 0 first), 0 < +1 < -1
         std::vector<std::array<int, 3>> shifts;
         {
@@ -852,6 +929,7 @@ static bool build_overset(Plan& P, Error& err) {
                     break;
                 }
             }
+        }
         }
         int64_t orphans = 0, first = -1;
         for (int64_t r = 0; r < R; ++r)
@@ -918,7 +996,7 @@ static bool build_overset(Plan& P, Error& err) {
 }
 
 // ------------------------------------------------------------------------------------
-bool build_plan(const mrab_problem* pb, Plan& P, Error& err) {
+bool build_plan(const mrab_problem* pb, Plan& P, Error& err, bool overset_only) {
     init_rows();
     P.opt = read_options();
     if (!pb || pb->n_meshes < 1 || pb->n_meshes > kMaxMeshes || !pb->meshes || (pb->dim != 2 && pb->dim != 3)) {
@@ -935,6 +1013,10 @@ bool build_plan(const mrab_problem* pb, Plan& P, Error& err) {
     }
     if (!(pb->h > 0)) {
         err = {MRAB_E_INVALID, "h must be positive"};
+        return false;
+    }
+    if (pb->n_donors < 0 || (pb->n_donors > 0 && !pb->donors)) {
+        err = {MRAB_E_INVALID, "n_donors < 0, or n_donors > 0 with donors NULL"};
         return false;
     }
     if (pb->viscous && !(pb->Re > 0)) {
@@ -987,9 +1069,11 @@ bool build_plan(const mrab_problem* pb, Plan& P, Error& err) {
             err = {MRAB_E_MISALIGNED, "every step multiple must divide the largest one"};
             return false;
         }
-    if (!build_overset(P, err)) return false;
+    if (!build_overset(P, pb, err)) return false;
+    if (overset_only) return true;
     for (int g = 0; g < (int)P.meshes.size(); ++g)
-        if (!compute_metrics(P.meshes[g], err)) {
+        if (!(pb->meshes[g].metrics ? copy_metrics(P.meshes[g], pb->meshes[g].metrics, err)
+                                    : compute_metrics(P.meshes[g], err))) {
             err.msg = "mesh " + std::to_string(g) + ": " + err.msg;
             return false;
         }

@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -841,6 +842,66 @@ mrab_status mrab_plan_create(const mrab_problem* problem, mrab_plan** out) {
 }
 
 void mrab_plan_destroy(mrab_plan* plan) { delete plan; }
+
+mrab_status mrab_overset_build(const mrab_problem* problem, int8_t** iblank_out, mrab_donor** donors_out,
+                               int64_t* n_out) {
+    if (!iblank_out || !donors_out || !n_out) return fail(MRAB_E_INVALID, "NULL output pointer");
+    try {
+        Plan P;
+        Error err{MRAB_OK, ""};
+        if (!build_plan(problem, P, err, /*overset_only=*/true)) return fail(err.st, err.msg);
+        int64_t npts = 0, R = 0;
+        for (const auto& m : P.meshes) {
+            npts += m.npts;
+            R += (int64_t)m.rpoint.size();
+        }
+        int8_t* ib = (int8_t*)std::malloc((size_t)std::max<int64_t>(npts, 1));
+        mrab_donor* dn = (mrab_donor*)std::calloc((size_t)std::max<int64_t>(R, 1), sizeof(mrab_donor));
+        if (!ib || !dn) {
+            std::free(ib);
+            std::free(dn);
+            return fail(MRAB_E_INVALID, "out of host memory");
+        }
+        int64_t o = 0, e = 0;
+        for (int g = 0; g < (int)P.meshes.size(); ++g) {
+            const MeshPlan& m = P.meshes[g];
+            for (int64_t p = 0; p < m.npts; ++p) ib[o + p] = m.active[p] ? 1 : 0;
+            o += m.npts;
+            for (size_t r = 0; r < m.rpoint.size(); ++r, ++e) {
+                dn[e].recv_mesh = g;
+                dn[e].donor_mesh = m.rdonor[r];
+                dn[e].recv_index = m.rpoint[r];
+                for (int k = 0; k < 3; ++k) dn[e].base[k] = m.rbase[r * 3 + k];
+                for (int k = 0; k < 3; ++k)
+                    for (int a = 0; a < 4; ++a) dn[e].w[k][a] = m.rw[r * 12 + k * 4 + a];
+            }
+        }
+        *iblank_out = ib;
+        *donors_out = dn;
+        *n_out = R;
+        return MRAB_OK;
+    } catch (const std::exception& ex) {
+        return fail(MRAB_E_INVALID, std::string("overset_build: ") + ex.what());
+    }
+}
+
+void mrab_free(void* p) { std::free(p); }
+
+mrab_status mrab_plan_get_face_flags(const mrab_plan* plan, int mesh, uint8_t* flags) {
+    if (!plan || mesh < 0 || mesh >= (int)plan->P->meshes.size() || !flags)
+        return fail(MRAB_E_INVALID, "bad plan/mesh or NULL flags");
+    const MeshPlan& m = plan->P->meshes[mesh];
+    for (int64_t p = 0; p < m.npts; ++p) {
+        uint8_t f = 0;
+        if (m.active[p])
+            for (int k = 0; k < m.dim; ++k) {
+                if (m.posA[k][p] == 0) f |= (uint8_t)(1u << (2 * k));
+                if (m.posB[k][p] == 0) f |= (uint8_t)(1u << (2 * k + 1));
+            }
+        flags[p] = f;
+    }
+    return MRAB_OK;
+}
 
 mrab_status mrab_plan_info(const mrab_plan* plan, int mesh, int64_t* n_points, int64_t* n_active,
                            int64_t* n_receivers) {

@@ -95,6 +95,7 @@ struct Plan {
 // host setup (host_setup.cpp)
 mrab_status ab_weights(const double* nodes, int m, int n, double a, double b, double* out,
                        std::string* msg);
-bool build_plan(const mrab_problem* pb, Plan& plan, Error& err);
+// overset_only: stop after the overset setup (hole cutting, segments, receivers, donors)
+bool build_plan(const mrab_problem* pb, Plan& plan, Error& err, bool overset_only = false);
 
 }  // namespace mrab

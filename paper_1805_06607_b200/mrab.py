@@ -30,14 +30,27 @@ class MeshDesc(C.Structure):
     _fields_ = [("dim", C.c_int), ("n", C.c_int * 3), ("periodic", C.c_int * 3),
                 ("face_bc", (C.c_int * 2) * 3), ("period", (C.c_double * 3) * 3),
                 ("xyz", C.POINTER(C.c_double)), ("priority", C.c_int),
-                ("step_multiple", C.c_int)]
+                ("step_multiple", C.c_int), ("metrics", C.POINTER(C.c_double)),
+                ("iblank", C.POINTER(C.c_int8))]
+
+
+class Donor(C.Structure):
+    """mrab_donor: one receiver and its donor stencil (include/mrab.h)."""
+    _fields_ = [("recv_mesh", C.c_int32), ("donor_mesh", C.c_int32), ("recv_index", C.c_int64),
+                ("base", C.c_int32 * 3), ("reserved", C.c_int32), ("w", (C.c_double * 4) * 3)]
+
+
+DONOR_DTYPE = np.dtype([("recv_mesh", "<i4"), ("donor_mesh", "<i4"), ("recv_index", "<i8"),
+                        ("base", "<i4", (3,)), ("reserved", "<i4"), ("w", "<f8", (3, 4))])
+assert DONOR_DTYPE.itemsize == C.sizeof(Donor)
 
 
 class ProblemDesc(C.Structure):
     _fields_ = [("dim", C.c_int), ("n_meshes", C.c_int), ("meshes", C.POINTER(MeshDesc)),
                 ("gamma", C.c_double), ("Re", C.c_double), ("Pr", C.c_double),
                 ("viscous", C.c_int), ("q_inf", C.c_double * 5), ("wall_T", C.c_double),
-                ("order_n", C.c_int), ("history_m", C.c_int), ("h", C.c_double)]
+                ("order_n", C.c_int), ("history_m", C.c_int), ("h", C.c_double),
+                ("n_donors", C.c_int64), ("donors", C.c_void_p)]
 
 
 _lib = None
@@ -58,6 +71,11 @@ def lib():
         L.mrab_plan_info.argtypes = [vp, C.c_int, i64p, i64p, i64p]
         L.mrab_plan_get_tables.argtypes = [vp, C.c_int, vp, vp, vp, vp, vp]
         L.mrab_plan_get_metrics.argtypes = [vp, C.c_int, vp, vp]
+        L.mrab_plan_get_face_flags.argtypes = [vp, C.c_int, vp]
+        L.mrab_overset_build.argtypes = [C.POINTER(ProblemDesc), C.POINTER(vp), C.POINTER(vp),
+                                         i64p]
+        L.mrab_free.argtypes = [vp]
+        L.mrab_free.restype = None
         L.mrab_workspace_bytes.argtypes = [vp]
         L.mrab_workspace_bytes.restype = C.c_size_t
         L.mrab_create.argtypes = [vp, C.POINTER(vp), vp, C.c_size_t, vp, C.POINTER(vp)]
@@ -88,7 +106,8 @@ EXPORTED = ["mrab_ab_weights", "mrab_plan_create", "mrab_plan_destroy", "mrab_pl
             "mrab_plan_get_tables", "mrab_plan_get_metrics", "mrab_workspace_bytes",
             "mrab_create", "mrab_destroy", "mrab_step", "mrab_get_state", "mrab_set_state",
             "mrab_rhs", "mrab_get_counters", "mrab_launches_per_macro_step", "mrab_time_kernel",
-            "mrab_set_trace", "mrab_last_error", "mrab_get_history", "mrab_set_history"]
+            "mrab_set_trace", "mrab_last_error", "mrab_get_history", "mrab_set_history",
+            "mrab_overset_build", "mrab_free", "mrab_plan_get_face_flags"]
 
 
 def _check(st):
@@ -124,42 +143,86 @@ def ab_weights(nodes, n, a, b):
     return out
 
 
+def _problem_desc(problem, steps=None, iblank=None, metrics=None, donors=None):
+    keep = []
+    descs = (MeshDesc * len(problem.meshes))()
+    for g, m in enumerate(problem.meshes):
+        d = descs[g]
+        d.dim = problem.dim
+        for k in range(3):
+            d.n[k] = m.shape[k] if k < problem.dim else 1
+            d.periodic[k] = int(m.periodic[k]) if k < problem.dim else 0
+            for s in range(2):
+                d.face_bc[k][s] = int(m.face_bc[k][s]) if k < problem.dim else 3
+            for c in range(3):
+                d.period[k][c] = (float(m.period[k][c])
+                                  if (k < problem.dim and c < problem.dim) else 0.0)
+        xyz = np.ascontiguousarray(m.xyz, dtype=np.float64)
+        keep.append(xyz)
+        d.xyz = _dptr(xyz)
+        d.priority = int(m.priority)
+        d.step_multiple = int(steps[g] if steps is not None else m.step_multiple)
+        npts = int(np.prod(m.shape[:problem.dim]))
+        if metrics is not None and metrics[g] is not None:
+            mt = np.ascontiguousarray(metrics[g], dtype=np.float64)
+            assert mt.size == (1 + problem.dim ** 2) * npts, "metrics: [1 + dim^2][n...]"
+            keep.append(mt)
+            d.metrics = _dptr(mt)
+        if iblank is not None and iblank[g] is not None:
+            ib = np.ascontiguousarray(iblank[g], dtype=np.int8)
+            assert ib.size == npts, "iblank: [n...]"
+            keep.append(ib)
+            d.iblank = ib.ctypes.data_as(C.POINTER(C.c_int8))
+    pb = ProblemDesc()
+    pb.dim = problem.dim
+    pb.n_meshes = len(problem.meshes)
+    pb.meshes = descs
+    pb.gamma, pb.Re, pb.Pr = float(problem.gamma), float(problem.Re), float(problem.Pr)
+    pb.viscous = int(bool(problem.viscous))
+    for c in range(problem.dim + 2):
+        pb.q_inf[c] = float(problem.q_inf[c])
+    pb.wall_T = float(problem.wall_T)
+    pb.order_n, pb.history_m = int(problem.order_n), int(problem.history_m)
+    pb.h = float(problem.h)
+    if donors is not None:
+        dn = np.ascontiguousarray(donors, dtype=DONOR_DTYPE)
+        keep.append(dn)
+        pb.n_donors = len(dn)
+        pb.donors = dn.ctypes.data if len(dn) else None
+    return pb, keep, descs
+
+
+def overset_build(problem, steps=None, iblank=None, donors=None):
+    """mrab_overset_build: (list of per-mesh int8 iblank arrays, DONOR_DTYPE donor table)."""
+    pb, keep, descs = _problem_desc(problem, steps, iblank, None, donors)
+    ib, dn, n = C.c_void_p(), C.c_void_p(), C.c_int64()
+    _check(lib().mrab_overset_build(C.byref(pb), C.byref(ib), C.byref(dn), C.byref(n)))
+    try:
+        sizes = [int(np.prod(m.shape[:problem.dim])) for m in problem.meshes]
+        flat = np.ctypeslib.as_array(C.cast(ib, C.POINTER(C.c_int8)), (sum(sizes),)).copy()
+        out_ib, o = [], 0
+        for sz in sizes:
+            out_ib.append(flat[o:o + sz])
+            o += sz
+        R = n.value
+        raw = (C.c_char * (R * DONOR_DTYPE.itemsize)).from_address(dn.value) if R else b""
+        table = np.frombuffer(bytes(raw), dtype=DONOR_DTYPE).copy()
+    finally:
+        lib().mrab_free(ib)
+        lib().mrab_free(dn)
+    return out_ib, table
+
+
 class Plan:
     """mrab_plan: host setup.  `problem` is any object with the fields of mrab_problem
     (dim, meshes[...], gamma, Re, Pr, viscous, q_inf, wall_T, order_n, history_m, h); each
     mesh has shape, xyz, periodic, face_bc, period, priority, step_multiple."""
 
-    def __init__(self, problem, steps=None):
-        self._keep = []
-        descs = (MeshDesc * len(problem.meshes))()
-        for g, m in enumerate(problem.meshes):
-            d = descs[g]
-            d.dim = problem.dim
-            for k in range(3):
-                d.n[k] = m.shape[k] if k < problem.dim else 1
-                d.periodic[k] = int(m.periodic[k]) if k < problem.dim else 0
-                for s in range(2):
-                    d.face_bc[k][s] = int(m.face_bc[k][s]) if k < problem.dim else 3
-                for c in range(3):
-                    d.period[k][c] = (float(m.period[k][c])
-                                      if (k < problem.dim and c < problem.dim) else 0.0)
-            xyz = np.ascontiguousarray(m.xyz, dtype=np.float64)
-            self._keep.append(xyz)
-            d.xyz = _dptr(xyz)
-            d.priority = int(m.priority)
-            d.step_multiple = int(steps[g] if steps is not None else m.step_multiple)
-        pb = ProblemDesc()
-        pb.dim = problem.dim
-        pb.n_meshes = len(problem.meshes)
-        pb.meshes = descs
-        pb.gamma, pb.Re, pb.Pr = float(problem.gamma), float(problem.Re), float(problem.Pr)
-        pb.viscous = int(bool(problem.viscous))
-        for c in range(problem.dim + 2):
-            pb.q_inf[c] = float(problem.q_inf[c])
-        pb.wall_T = float(problem.wall_T)
-        pb.order_n, pb.history_m = int(problem.order_n), int(problem.history_m)
-        pb.h = float(problem.h)
-        self._descs = descs
+    def __init__(self, problem, steps=None, iblank=None, metrics=None, donors=None):
+        """Optional caller-supplied setup (mrab.h): iblank[g] int8 [n...] and metrics[g]
+        float64 [1 + dim^2][n...] per mesh (None entries = built by the library), donors a
+        DONOR_DTYPE array (None = searched by the library)."""
+        pb, self._keep, self._descs = _problem_desc(problem, steps, iblank, metrics, donors)
         h = C.c_void_p()
         _check(lib().mrab_plan_create(C.byref(pb), C.byref(h)))
         self.h = h
@@ -190,6 +253,14 @@ class Plan:
                                           rd.ctypes.data, rb.ctypes.data, rw.ctypes.data))
         return dict(iblank=ib, point=rp[:R], donor=rd[:R], base=rb[:R], weights=rw[:R])
 
+    def face_flags(self, g):
+        """SAT face flags (mrab_plan_get_face_flags): bit 2k = kappa-min segment end, bit
+        2k+1 = kappa-max segment end."""
+        npts, _, _ = self.info(g)
+        f = np.zeros(npts, np.uint8)
+        _check(lib().mrab_plan_get_face_flags(self.h, g, f.ctypes.data))
+        return f
+
     def metrics(self, g):
         npts, _, _ = self.info(g)
         jinv = np.zeros(npts)
@@ -204,11 +275,17 @@ class Plan:
 class Context:
     """mrab_ctx on the current torch CUDA device and stream."""
 
-    def __init__(self, plan: Plan, q0, stream=None):
+    def __init__(self, plan: Plan, q0, stream=None, workspace=None):
+        """`workspace`: optional caller-owned device buffer (torch uint8 tensor) of at least
+        plan.workspace_bytes() + 256 bytes; the context uses its first 256-byte-aligned
+        address."""
         import torch
         self.plan = plan
         nbytes = plan.workspace_bytes()
-        self.ws = torch.empty(nbytes + 256, dtype=torch.uint8, device="cuda")
+        if workspace is None:
+            workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device="cuda")
+        assert workspace.is_cuda and workspace.numel() >= nbytes + 256
+        self.ws = workspace
         base = self.ws.data_ptr()
         off = (-base) % 256
         qs = [np.ascontiguousarray(q, dtype=np.float64) for q in q0]

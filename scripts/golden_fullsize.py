@@ -23,7 +23,9 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 import synth  # noqa: E402
+import bars  # noqa: E402  (tests/bars.py: the bars' scales, computed with oracle/ only)
 from oracle import rhs as orhs, timeint  # noqa: E402
 
 ORDER = {4: 3, 5: 2}
@@ -89,6 +91,7 @@ def main(cid):
         out[f"m{g}_rhs"] = Rf[:, S[g]]
         out[f"m{g}_rhs_max"] = np.max(np.abs(Rf), axis=1)
     del R0
+    out["rhs_scale"] = bars.rhs_scales(p, st, p.q0)
     t2 = time.time()
     orc = timeint.MRAB(p, setup=st)
     orc.run(1)
@@ -97,6 +100,7 @@ def main(cid):
         Qf = orc.base[g].reshape(p.nc, -1)
         out[f"m{g}_state"] = Qf[:, S[g]]
         out[f"m{g}_state_max"] = np.max(np.abs(Qf), axis=1)
+    out["cmax"] = np.array(bars.state_scales(orc.base, p.gamma)[1] / bars.state_scales(orc.base, p.gamma)[0])
     name = f"fullsize_config{cid}.npz" if scale == "full" else f"dryrun_{scale}_config{cid}.npz"
     path = os.path.join(ROOT, "tests", "golden" if scale == "full" else "/tmp", name)
     np.savez_compressed(path, **out)

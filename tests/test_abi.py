@@ -90,3 +90,92 @@ def test_product_path_is_independent_of_the_oracle():
             if f.endswith(".py"):
                 src = open(os.path.join(d, f)).read()
                 assert not re.search(pat, src, re.M), f
+
+
+def _plan_tables(plan, G):
+    return [plan.tables(g) for g in range(G)]
+
+
+@pytest.mark.parametrize("cid", [1, 3, 4, 5])
+def test_caller_supplied_setup_reproduces_built_plan(cid):
+    """mrab_overset_build exports the blanking and donor table; feeding them (and the plan's
+    metric terms) back through mrab_mesh_desc.iblank / .metrics and mrab_problem.donors gives
+    a plan whose tables and metrics equal the library-built ones bit for bit (§8(b))."""
+    p = synth.make_config(cid, "test")
+    G = len(p.meshes)
+    ref = mrab.Plan(p)
+    ib, dn = mrab.overset_build(p)
+    tb = _plan_tables(ref, G)
+    assert len(dn) == sum(len(t["point"]) for t in tb)
+    for g in range(G):
+        assert np.array_equal(ib[g], tb[g]["iblank"])
+        sel = dn[dn["recv_mesh"] == g]
+        assert np.array_equal(sel["recv_index"], tb[g]["point"])
+        assert np.array_equal(sel["donor_mesh"], tb[g]["donor"])
+        assert np.array_equal(sel["base"], tb[g]["base"])
+        assert np.array_equal(sel["w"], tb[g]["weights"])
+    mets = []
+    for g in range(G):
+        jinv, M = ref.metrics(g)
+        mets.append(np.concatenate([jinv[None], M.reshape(p.dim * p.dim, -1)]))
+    for kw in (dict(iblank=ib), dict(donors=dn, iblank=ib), dict(metrics=mets),
+               dict(iblank=ib, donors=dn, metrics=mets)):
+        pl = mrab.Plan(p, **kw)
+        for g, t in enumerate(_plan_tables(pl, G)):
+            for key in ("iblank", "point", "donor", "base", "weights"):
+                assert np.array_equal(t[key], tb[g][key]), (kw.keys(), g, key)
+            j1, M1 = pl.metrics(g)
+            j0, M0 = ref.metrics(g)
+            assert np.array_equal(j1, j0) and np.array_equal(M1, M0)
+            assert np.array_equal(pl.face_flags(g), ref.face_flags(g))
+
+
+@pytest.mark.parametrize("cid", [1, 3, 4])
+def test_face_flags_match_oracle_sat_faces(cid):
+    """mrab_plan_get_face_flags against the oracle's SAT groups (eq:int): bit 2k =
+    side + (kappa-min end), bit 2k+1 = side - (kappa-max end), bit for bit."""
+    p = synth.make_config(cid, "test")
+    plan = mrab.Plan(p)
+    st = orhs.build(p)
+    for g in range(len(p.meshes)):
+        want = np.zeros(int(np.prod(p.meshes[g].shape[:p.dim])), np.uint8)
+        for pts, k, side, _typ in st.geom[g].sat:
+            want[pts] |= np.uint8(1 << (2 * k + (0 if side > 0 else 1)))
+        assert np.array_equal(plan.face_flags(g), want)
+
+
+def test_caller_supplied_setup_errors():
+    p = synth.make_config(1, "test")
+    ib, dn = mrab.overset_build(p)
+    with pytest.raises(mrab.MrabError, match="ORPHAN"):
+        mrab.Plan(p, iblank=ib, donors=dn[1:])                  # a receiver without a donor
+    d2 = dn.copy()
+    d2["recv_index"][0] = 0 if dn["recv_index"][0] != 0 else 1  # not a receiver
+    d2 = np.concatenate([d2, dn[:1]])
+    with pytest.raises(mrab.MrabError, match="INVALID"):
+        mrab.Plan(p, iblank=ib, donors=d2)
+    d3 = np.concatenate([dn, dn[:1]])                           # duplicate
+    with pytest.raises(mrab.MrabError, match="INVALID"):
+        mrab.Plan(p, iblank=ib, donors=d3)
+    d4 = dn.copy()
+    d4["donor_mesh"][0] = d4["recv_mesh"][0]                    # self-donation
+    with pytest.raises(mrab.MrabError, match="INVALID"):
+        mrab.Plan(p, iblank=ib, donors=d4)
+    # a donor stencil over the background's hole
+    d5 = dn.copy()
+    r = int(np.nonzero(dn["donor_mesh"] == 0)[0][0])
+    d5["base"][r, :2] = [19, 19]
+    with pytest.raises(mrab.MrabError, match="INVALID"):
+        mrab.Plan(p, iblank=ib, donors=d5)
+    mets = []
+    for g in range(2):
+        jinv, M = mrab.Plan(p).metrics(g)
+        mets.append(np.concatenate([jinv[None], M.reshape(4, -1)]))
+    mets[1][0, 7] = -1.0                                        # J^-1 <= 0
+    with pytest.raises(mrab.MrabError, match="INVALID"):
+        mrab.Plan(p, metrics=mets)
+    ib2 = [b.copy() for b in ib]
+    n0, n1 = p.meshes[1].shape[:2]
+    ib2[1][n0 * (n1 // 2) + 4] = 0                              # leaves a 4-point segment
+    with pytest.raises(mrab.MrabError, match="SEGMENT"):
+        mrab.Plan(p, iblank=ib2)
