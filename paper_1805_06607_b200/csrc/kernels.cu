@@ -19,74 +19,12 @@
 #include "kernels.cuh"
 #include "mrab_internal.h"
 #include "stencil_table.cuh"
+#include "rhs3d_common.cuh"
 
 namespace mrab {
 
 void upload_stencil_rows() {}
 
-static constexpr double kP0 = 17.0 / 48.0;   // H_00 of the SBP norm (R14)
-
-// ------------------------------------------------------------------------------------
-// SAT characteristic penalty K^s(n; q) dq (analytic Euler eigensystem; readings R14/R15)
-// ------------------------------------------------------------------------------------
-template <int D>
-__device__ __forceinline__ void kchar(const double* q, const double* n, double side,
-                                      const double* dq, double gamma, double* out) {
-    // divisions as reciprocal multiplies (rcp64: the IEEE divide costs 128 cycles of latency)
-    const double rho = q[0];
-    const double irho = rcp64(rho);
-    double u[D], ke = 0.0;
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-        u[i] = q[1 + i] * irho;
-        ke += u[i] * u[i];
-    }
-    const double p = (gamma - 1.0) * (q[D + 1] - 0.5 * rho * ke);
-    const double c2 = gamma * p * irho;
-    const double c = sqrt(c2);
-    const double ic2 = rcp64(c2);
-    const double H = (q[D + 1] + p) * irho;
-    double nn = 0.0;
-#pragma unroll
-    for (int i = 0; i < D; ++i) nn += n[i] * n[i];
-    nn = sqrt(nn);
-    const double inn = rcp64(nn);
-    double nh[D], un = 0.0;
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-        nh[i] = n[i] * inn;
-        un += u[i] * nh[i];
-    }
-    double du[D], udm = 0.0;
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-        du[i] = (dq[1 + i] - u[i] * dq[0]) * irho;
-        udm += u[i] * dq[1 + i];
-    }
-    const double dp = (gamma - 1.0) * (dq[D + 1] - udm + 0.5 * ke * dq[0]);
-    double dun = 0.0;
-#pragma unroll
-    for (int i = 0; i < D; ++i) dun += du[i] * nh[i];
-    const double ap = (dp + rho * c * dun) * (0.5 * ic2);
-    const double am = (dp - rho * c * dun) * (0.5 * ic2);
-    const double a0 = dq[0] - dp * ic2;
-    const double l0 = fmax(side * un * nn, 0.0);
-    const double lp = fmax(side * (un + c) * nn, 0.0);
-    const double lm = fmax(side * (un - c) * nn, 0.0);
-    double udt = 0.0, dut[D];
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-        dut[i] = du[i] - dun * nh[i];
-        udt += u[i] * dut[i];
-    }
-    const double wp = lp * ap, wm = lm * am, w0 = l0 * a0;
-    out[0] = wp + wm + w0;
-#pragma unroll
-    for (int i = 0; i < D; ++i)
-        out[1 + i] = wp * (u[i] + c * nh[i]) + wm * (u[i] - c * nh[i]) + w0 * u[i] +
-                     l0 * rho * dut[i];
-    out[D + 1] = wp * (H + c * un) + wm * (H - c * un) + w0 * (0.5 * ke) + l0 * rho * udt;
-}
 
 // 8^3 tiles of the donor-flux kernel
 namespace {
@@ -303,60 +241,6 @@ __global__ void __launch_bounds__(NT3, 2) k_visc3d_x(DevMesh m, const double* __
     }
 }
 
-// SAT penalties at one 3-D point (eq:int P:279-299; edges/corners sum over the flagged
-// directions; readings R14-R16), added to R.  q: the point's state; nv[k][i] =
-// (grad kappa_k)_i = J M_{k i}; fv[i][j]: the point's Cartesian viscous fluxes F^V_i (j < 3:
-// tau_ij, j = 3: energy).
-template <bool VISC>
-__device__ __forceinline__ void sat3(const DevMesh& m, const Gas& g, const double* q, int64_t p,
-                                     const int* idx, unsigned code, const double (&nv)[3][3],
-                                     const double (&fv)[3][4], double* R) {
-    constexpr int NC = 5;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        const int cl = (code >> (4 * k)) & 15;
-        if (cl != CLS_L0 && cl != CLS_R0) continue;
-        const int sidx = (cl == CLS_L0) ? 0 : 1;
-        const double side = (cl == CLS_L0) ? 1.0 : -1.0;
-        const bool at_face = !m.periodic[k] && (sidx == 0 ? idx[k] == 0 : idx[k] == m.n[k] - 1);
-        const int typ = at_face ? m.face_bc[k][sidx] : MRAB_BC_OVERSET;
-        double qh[NC], dq[NC];
-        int slot = -1;
-        if (typ == MRAB_BC_OVERSET) {
-            slot = m.recv_slot[p];
-#pragma unroll
-            for (int c = 0; c < NC; ++c) qh[c] = m.qhat[c * m.nrecv + slot];
-        } else if (typ == MRAB_BC_FARFIELD) {
-#pragma unroll
-            for (int c = 0; c < NC; ++c) qh[c] = g.q_inf[c];
-        } else {   // isothermal no-slip wall
-            qh[0] = q[0];
-            qh[1] = qh[2] = qh[3] = 0.0;
-            qh[4] = q[0] * g.wall_T / (g.gamma * (g.gamma - 1.0));
-        }
-#pragma unroll
-        for (int c = 0; c < NC; ++c) dq[c] = q[c] - qh[c];
-        double kd[NC];
-        kchar<3>(q, nv[k], side, dq, g.gamma, kd);
-        double sig1 = 0.0;
-        if (VISC) sig1 = 0.5 * g.iRe * (nv[k][0] * nv[k][0] + nv[k][1] * nv[k][1] + nv[k][2] * nv[k][2]);
-#pragma unroll
-        for (int c = 0; c < NC; ++c) R[c] -= (0.5 * kd[c] + sig1 * dq[c]) * (1.0 / kP0);
-        if (VISC && typ != MRAB_BC_WALL) {
-            // F^V_kappa - Fhat^V_kappa contracted with grad(kappa)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                double fk = 0.0, fh = 0.0;
-#pragma unroll
-                for (int i = 0; i < 3; ++i) {
-                    fk += nv[k][i] * fv[i][j];
-                    if (typ == MRAB_BC_OVERSET) fh += nv[k][i] * m.fvhat[(int64_t)(i * 4 + j) * m.nrecv + slot];
-                }
-                R[1 + j] += 0.5 * side * (fk - fh) * (1.0 / kP0);
-            }
-        }
-    }
-}
 
 // =====================================================================================
 // k_rhs3z: the 3-D RHS of one mesh in one HBM pass.
