@@ -36,6 +36,7 @@ Options read_options() {
     o.interp_box = (int)env_or("MRAB_INTERP_BOX", o.interp_box);
     o.interp_quad = (int)env_or("MRAB_INTERP_QUAD", o.interp_quad);
     o.z3_fused = (int)env_or("MRAB_3D_FUSED", o.z3_fused);
+    o.overlap3d = (int)env_or("MRAB_OVERLAP3D", o.overlap3d);
     return o;
 }
 const Options& opts() { return g_opt; }

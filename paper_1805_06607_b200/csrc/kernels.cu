@@ -1767,6 +1767,31 @@ static int sm_count() {
     return n;
 }
 
+// Launch priority of the 3-D launches that follow on this thread (the multi-stream 3-D schedule
+// sets it per node; it travels with the launch into a captured graph, which is instantiated
+// with cudaGraphInstantiateFlagUseNodePriority).  has = 0: plain launches.
+static thread_local int tl_has_prio = 0, tl_prio = 0;
+void set_launch_priority(int has, int prio) {
+    tl_has_prio = has;
+    tl_prio = prio;
+}
+template <class... KArgs, class... Args>
+static void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    if (tl_has_prio) {
+        at[0].id = cudaLaunchAttributePriority;
+        at[0].val.priority = tl_prio;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+    }
+    cudaLaunchKernelEx(&cfg, kern, KArgs(args)...);
+}
+
 void launch_visc(const DevMesh& m, const double* Q, double* FV, const Box& box, const int32_t* tiles,
                  int ntiles, const Gas& gas, cudaStream_t st) {
     static bool init = false;
@@ -1785,8 +1810,8 @@ void launch_visc(const DevMesh& m, const double* Q, double* FV, const Box& box, 
         grid = dim3((box.hi[0] - box.lo[0] + T3X) / T3X, (box.hi[1] - box.lo[1] + T3Y) / T3Y,
                     (box.hi[2] - box.lo[2] + T3Z) / T3Z);
     }
-    if (m.cart) k_visc3d_x<true><<<grid, NT3, SMEMX, st>>>(m, Q, FV, box, tiles, gas);
-    else k_visc3d_x<false><<<grid, NT3, SMEMX, st>>>(m, Q, FV, box, tiles, gas);
+    if (m.cart) launch_k(k_visc3d_x<true>, grid, dim3(NT3), SMEMX, st, m, Q, FV, box, tiles, gas);
+    else launch_k(k_visc3d_x<false>, grid, dim3(NT3), SMEMX, st, m, Q, FV, box, tiles, gas);
 }
 
 void launch_rhs2d(const DevMesh& m, const double* Q, const Gas& g, const Epilogue& ep,
@@ -1898,11 +1923,11 @@ void launch_flux3d(const DevMesh& m, const double* Q, const Gas& gas, cudaStream
     const dim3 grid(tile3_blocks(m.n));
     double* FH = const_cast<double*>(m.fh);
     if (gas.viscous) {
-        if (m.cart) k_flux3d<true, true><<<grid, NT3, SMEMX, st>>>(m, Q, FH, m.fv, m.fvtile, gas);
-        else k_flux3d<true, false><<<grid, NT3, SMEMX, st>>>(m, Q, FH, m.fv, m.fvtile, gas);
+        if (m.cart) launch_k(k_flux3d<true, true>, grid, dim3(NT3), SMEMX, st, m, Q, FH, m.fv, m.fvtile, gas);
+        else launch_k(k_flux3d<true, false>, grid, dim3(NT3), SMEMX, st, m, Q, FH, m.fv, m.fvtile, gas);
     } else {
-        if (m.cart) k_flux3d<false, true><<<grid, NT3, SMEMX, st>>>(m, Q, FH, m.fv, m.fvtile, gas);
-        else k_flux3d<false, false><<<grid, NT3, SMEMX, st>>>(m, Q, FH, m.fv, m.fvtile, gas);
+        if (m.cart) launch_k(k_flux3d<false, true>, grid, dim3(NT3), SMEMX, st, m, Q, FH, m.fv, m.fvtile, gas);
+        else launch_k(k_flux3d<false, false>, grid, dim3(NT3), SMEMX, st, m, Q, FH, m.fv, m.fvtile, gas);
     }
 }
 
@@ -1914,7 +1939,17 @@ static void launch_div3d(const DevMesh& m, const double* Q, const Gas& gas, cons
         init = true;
     }
     const dim3 grid(tile3_blocks(m.n));
-    k_rhs3d<VISC, CART, true><<<grid, NT3, SMEM3, st>>>(m, Q, m.fv, gas, ep, m.fh);
+    launch_k(k_rhs3d<VISC, CART, true>, grid, dim3(NT3), SMEM3, st, m, Q, (const double*)m.fv, gas, ep, m.fh);
+}
+
+void launch_div3d_pass(const DevMesh& m, const double* Q, const Gas& gas, const Epilogue& ep, cudaStream_t st) {
+    if (gas.viscous) {
+        if (m.cart) launch_div3d<true, true>(m, Q, gas, ep, st);
+        else launch_div3d<true, false>(m, Q, gas, ep, st);
+    } else {
+        if (m.cart) launch_div3d<false, true>(m, Q, gas, ep, st);
+        else launch_div3d<false, false>(m, Q, gas, ep, st);
+    }
 }
 
 void launch_rhs(int dim, const DevMesh& m, const double* Q, const Gas& gas, const Epilogue& ep,
@@ -1936,13 +1971,43 @@ void launch_rhs(int dim, const DevMesh& m, const double* Q, const Gas& gas, cons
     }
     // two passes: contravariant fluxes, then divergence + SAT + epilogue
     launch_flux3d(m, Q, gas, st);
-    if (gas.viscous) {
-        if (m.cart) launch_div3d<true, true>(m, Q, gas, ep, st);
-        else launch_div3d<true, false>(m, Q, gas, ep, st);
-    } else {
-        if (m.cart) launch_div3d<false, true>(m, Q, gas, ep, st);
-        else launch_div3d<false, false>(m, Q, gas, ep, st);
+    launch_div3d_pass(m, Q, gas, ep, st);
+}
+
+// the same on a list of 8^3 tiles (flat tile index, x fastest): partial donors whose stencils
+// form a shell (nested meshes) combine only the tiles the gathers and the viscous pass read
+__global__ void __launch_bounds__(256) k_combine_t(int nc, int64_t N, int n0, int n1, int n2,
+                                                   const int32_t* __restrict__ tiles, CombineArgs a,
+                                                   double* __restrict__ out) {
+    const int ntx = (n0 + 7) / 8, nty = (n1 + 7) / 8;
+    const int t = tiles[blockIdx.x];
+    const int i0 = (t % ntx) * 8, j0 = ((t / ntx) % nty) * 8, k0 = (t / (ntx * nty)) * 8;
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+        const int l = threadIdx.x + s * 256;
+        const int gi = i0 + (l & 7), gj = j0 + ((l >> 3) & 7), gk = k0 + (l >> 6);
+        if (gi >= n0 || gj >= n1 || gk >= n2) continue;
+        const int64_t p = gi + (int64_t)n0 * (gj + (int64_t)n1 * gk);
+        for (int c = 0; c < nc; ++c) {
+            double v = a.base[c * N + p];
+            for (int k = 0; k < a.nsrc; ++k) v += a.c[k] * a.src[k][c * N + p];
+            out[c * N + p] = v;
+        }
     }
+}
+
+void launch_combine_tiles(int nc, const DevMesh& m, const int32_t* tiles, int ntiles, const double* base,
+                          int nsrc, const double* const* src, const double* csrc, double* out,
+                          cudaStream_t st) {
+    if (ntiles <= 0) return;
+    CombineArgs a{};
+    a.base = base;
+    a.nsrc = nsrc;
+    for (int s = 0; s < nsrc; ++s) {
+        a.src[s] = src[s];
+        a.c[s] = csrc[s];
+    }
+    launch_k(k_combine_t, dim3(ntiles), dim3(256), 0, st, nc, m.npts, m.n[0], m.n[1], m.n[2], tiles, a, out);
 }
 
 void launch_combine(int nc, const DevMesh& m, const Box& box, const double* base, int nsrc,
@@ -1957,7 +2022,7 @@ void launch_combine(int nc, const DevMesh& m, const Box& box, const double* base
     int64_t tot = (int64_t)(box.hi[0] - box.lo[0] + 1) * (box.hi[1] - box.lo[1] + 1) *
                   (box.hi[2] - box.lo[2] + 1);
     if (tot <= 0) return;
-    k_combine<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(nc, m.npts, m.n[0], m.n[1], box, a, out);
+    launch_k(k_combine, dim3((unsigned)((tot + 255) / 256)), dim3(256), 0, st, nc, m.npts, m.n[0], m.n[1], box, a, out);
 }
 
 void launch_interp(int viscous, const RecvList& rl, const DonorSet& ds, cudaStream_t st) {
@@ -1970,12 +2035,12 @@ void launch_interp(int viscous, const RecvList& rl, const DonorSet& ds, cudaStre
             cudaFuncSetAttribute(k_interp3b<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double) * 17 * IBOXN));
             init = true;
         }
-        if (viscous) k_interp3b<true><<<rl.ngroups, 128, bytes, st>>>(rl, ds);
-        else k_interp3b<false><<<rl.ngroups, 128, bytes, st>>>(rl, ds);
+        if (viscous) launch_k(k_interp3b<true>, dim3(rl.ngroups), dim3(128), bytes, st, rl, ds);
+        else launch_k(k_interp3b<false>, dim3(rl.ngroups), dim3(128), bytes, st, rl, ds);
     } else {
         const unsigned nbq = (unsigned)((rl.n * 4 + 127) / 128);
-        if (viscous) k_interp3q<true><<<nbq, 128, 0, st>>>(rl, ds);
-        else k_interp3q<false><<<nbq, 128, 0, st>>>(rl, ds);
+        if (viscous) launch_k(k_interp3q<true>, dim3(nbq), dim3(128), 0, st, rl, ds);
+        else launch_k(k_interp3q<false>, dim3(nbq), dim3(128), 0, st, rl, ds);
     }
 }
 
@@ -1998,6 +2063,11 @@ __global__ void k_scrub_read(const double4* __restrict__ b, size_t n, double* si
         acc += v.x + v.y + v.z + v.w;
     }
     if (acc == 12345.678) *sink = acc;   // keeps the loads alive, never true for scrub data
+}
+
+__global__ void k_stamp(unsigned long long* buf, int tag) { trace_rec(buf, tag, gtimer()); }
+void launch_stamp(unsigned long long* trace, int tag, cudaStream_t st) {
+    if (trace) launch_k(k_stamp, dim3(1), dim3(1), 0, st, trace, tag);
 }
 
 void launch_l2_scrub(void* a, void* b, size_t bytes, int tag, cudaStream_t st) {

@@ -185,6 +185,14 @@ void launch_visc(const DevMesh& m, const double* Q, double* FV, const Box& box, 
 // receivers from `ds`.
 void launch_rhs(int dim, const DevMesh& m, const double* Q, const Gas& gas, const Epilogue& ep,
                 const DonorSet& ds, cudaStream_t st);
+// 3-D two-pass RHS, pass by pass (the MRAB schedules run every stepping mesh's flux pass, then
+// the gathers -- which read the F^V the flux pass wrote on the donor-stencil tiles -- then the
+// divergence passes)
+void launch_flux3d(const DevMesh& m, const double* Q, const Gas& gas, cudaStream_t st);
+void launch_div3d_pass(const DevMesh& m, const double* Q, const Gas& gas, const Epilogue& ep, cudaStream_t st);
+void launch_combine_tiles(int nc, const DevMesh& m, const int32_t* tiles, int ntiles, const double* base,
+                          int nsrc, const double* const* src, const double* csrc, double* out,
+                          cudaStream_t st);
 void launch_combine(int nc, const DevMesh& m, const Box& box, const double* base, int nsrc,
                     const double* const* src, const double* csrc, double* out, cudaStream_t st);
 void launch_interp(int viscous, const RecvList& rl, const DonorSet& ds, cudaStream_t st);
@@ -194,6 +202,10 @@ void upload_stencil_rows();
 void launch_l2_scrub(void* a, void* b, size_t bytes, int tag, cudaStream_t st);
 // sets *flag (device int) if any of the n doubles is not finite
 void launch_finite(const double* a, size_t n, int* flag, cudaStream_t st);
+// launch priority of the 3-D launches that follow on this thread (has = 0: plain launches)
+void set_launch_priority(int has, int prio);
+// timeline stamp (mrab_set_trace): one record (tag, now, now) appended by a 1-thread kernel
+void launch_stamp(unsigned long long* trace, int tag, cudaStream_t st);
 
 #ifdef __CUDACC__
 // 1/x in fp64 without the IEEE division sequence: MUFU reciprocal seed refined by two

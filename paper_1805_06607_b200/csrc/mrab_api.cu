@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <numeric>
 #include <string>
@@ -50,6 +51,8 @@ struct MeshDev {
     double* FV = nullptr;
     int32_t* fvlist = nullptr;    // 3-D: the 8^3 tiles holding donor-stencil points (F^V there)
     int nfv = 0;
+    int32_t* cblist = nullptr;    // 3-D: fvlist tiles and their face neighbours (intermediate donor states)
+    int ncb = 0;
     double* FH = nullptr;         // 3-D two-pass RHS: contravariant fluxes [3][5][N]
     uint8_t* fvtile = nullptr;    // 3-D two-pass RHS: per 8^3 tile, SAT points inside (F^V written)
     Z3Table z3tab;                // 3-D: TMA tensor maps of the state-shaped buffers
@@ -114,8 +117,11 @@ struct mrab_ctx {
     std::vector<std::vector<int64_t>> evals_per_phase;
     int64_t launches_last = 0;
     int64_t launch_counter = 0;
+    int64_t graph_k0 = 0;         // MRAB macro-step index the phase-0 graph was captured at
     // 2-D multi-stream schedule: one stream per mesh (priority by rate) + a gather stream
-    cudaStream_t side[2 * kMaxMeshes + 1] = {};   // meshes, gathers, bulk launches of split meshes
+    // 2-D: meshes [0, G), the gather stream G, bulk launches of split meshes G+1+g;
+    // 3-D: meshes [0, G), donor-preparation streams G+1+h, gather streams 2G+1+g
+    cudaStream_t side[3 * kMaxMeshes + 1] = {};
     std::vector<cudaEvent_t> evpool;
     size_t evnext = 0;
     bool overlap = true;
@@ -157,9 +163,11 @@ static size_t plan_bytes(const Plan& P, bool dry, mrab_ctx* ctx, Bump* bump, boo
         if (d == 3) {
             const size_t nt = (size_t)((m.n[0] + 7) / 8) * ((m.n[1] + 7) / 8) * ((m.n[2] + 7) / 8);
             void* b = take(nt * sizeof(int32_t));
+            void* b2 = take(nt * sizeof(int32_t));
             void* f = P.opt.z3_fused ? nullptr : take((size_t)15 * N * sizeof(double));
             void* t = take(nt);
             if (D) {
+                D->cblist = (int32_t*)b2;
                 D->fvlist = (int32_t*)b;
                 D->FH = (double*)f;
                 D->fvtile = (uint8_t*)t;
@@ -389,13 +397,46 @@ static void issue_rhs(mrab_ctx* c, int g, const double* Q, const Epilogue& ep,
     c->launch_counter++;
 }
 
+// 3-D: donor data of mesh g at micro index j of the macro step where g does not step: the
+// intermediate state base + h_g sum_k beta_k^(j) R_k (MRAB Steps 2/5) and its
+// Cartesian viscous fluxes, formed into dstate / FV on the donor-stencil tiles (and their
+// face neighbours for the state: the viscous pass reads tile + 3 along each axis)
+static void issue_partial_donor(mrab_ctx* c, int g, int j, cudaStream_t st, const double* base = nullptr) {
+    const Plan& P = *c->P;
+    MeshDev& D = c->md[g];
+    const MeshPlan& mp = P.meshes[g];
+    const int m = P.history_m;
+    const int jj = j % mp.s;
+    const double hg = P.h * mp.s;
+    const double* src[kMaxHist];
+    double cs[kMaxHist];
+    for (int k = 0; k < m; ++k) {
+        int slot = ((c->book.head[g] - (m - 1) + k) % m + m) % m;   // oldest first
+        src[k] = D.ring[slot];
+        cs[k] = hg * P.coef[g][jj][k];
+    }
+    if (!base) base = D.Q[c->book.cur[g]];
+    launch_combine_tiles(P.nc, D.dm, P.viscous ? D.cblist : D.fvlist, P.viscous ? D.ncb : D.nfv, base, m, src,
+                         cs, D.dstate, st);
+    c->launch_counter++;
+    if (P.viscous && D.nfv > 0) {
+        launch_visc(D.dm, D.dstate, D.FV, Box{}, D.fvlist, D.nfv, c->gas, st);
+        c->launch_counter++;
+    }
+}
+
 // one MRAB macro step (host bookkeeping + launches)
 static void issue_macro_step_dag2d(mrab_ctx* c);
+static void issue_macro_step_dag3d(mrab_ctx* c);
 
 static void issue_macro_step(mrab_ctx* c) {
     const Plan& P = *c->P;
     if (P.dim == 2) {
         issue_macro_step_dag2d(c);
+        return;
+    }
+    if (P.opt.overlap3d) {
+        issue_macro_step_dag3d(c);
         return;
     }
     const int G = (int)P.meshes.size(), m = P.history_m;
@@ -408,38 +449,12 @@ static void issue_macro_step(mrab_ctx* c) {
                 if (stepping[h] && P.donor_of[g][h]) partial[g] = 1;
         }
         std::vector<const double*> state_of(G, nullptr);
-        if (P.dim == 2) {
-            // donor states on the fly: stepping meshes at their current state, the others at
-            // base + h_g sum_k beta_k R_k (partial integral of the extrapolant)
-            SrcSet ss{};
-            std::vector<int> ev;
-            for (int g = 0; g < G; ++g) {
-                MeshDev& D = c->md[g];
-                if (stepping[g]) {
-                    if (c->book.pending[g]) {
-                        c->book.cur[g] ^= 1;
-                        c->book.pending[g] = 0;
-                    }
-                    ev.push_back(g);
-                }
-                ss.base[g] = D.Q[c->book.cur[g]];
-                state_of[g] = ss.base[g];
-                ss.nsrc[g] = 0;
-                if (!stepping[g] && partial[g]) {
-                    const MeshPlan& mp = P.meshes[g];
-                    const int jj = j % mp.s;
-                    const double hg = P.h * mp.s;
-                    ss.nsrc[g] = m;
-                    for (int k = 0; k < m; ++k) {
-                        int slot = ((c->book.head[g] - (m - 1) + k) % m + m) % m;   // oldest first
-                        ss.src[g][k] = D.ring[slot];
-                        ss.c[g][k] = hg * P.coef[g][jj][k];
-                    }
-                }
-            }
-            issue_donor2d(c, ev, ss);
-        }
-        for (int g = 0; g < G && P.dim == 3; ++g) {
+        // 3-D two-pass RHS: the flux pass of every stepping mesh first (it writes F^V on the
+        // SAT and donor-stencil tiles), then the gathers, then the divergence passes; the
+        // one-pass kernel (Options::z3_fused) takes k_visc3d_x on the donor tiles instead
+        bool two = !opts().z3_fused;
+        for (int g = 0; g < G; ++g) two = two && c->md[g].FH;
+        for (int g = 0; g < G; ++g) {
             MeshDev& D = c->md[g];
             if (stepping[g]) {
                 if (c->book.pending[g]) {
@@ -448,25 +463,17 @@ static void issue_macro_step(mrab_ctx* c) {
                 }
                 const double* Q = D.Q[c->book.cur[g]];
                 state_of[g] = Q;
-                bool read_now = false;
-                for (int h = 0; h < G; ++h) read_now = read_now || (h != g && stepping[h] && P.donor_of[g][h]);
-                if (read_now) issue_step_visc(c, g, Q);
-            } else if (partial[g]) {
-                const MeshPlan& mp = P.meshes[g];
-                const int jj = j % mp.s;
-                const double hg = P.h * mp.s;
-                const double* src[kMaxHist];
-                double cs[kMaxHist];
-                for (int k = 0; k < m; ++k) {
-                    int slot = ((c->book.head[g] - (m - 1) + k) % m + m) % m;   // oldest first
-                    src[k] = D.ring[slot];
-                    cs[k] = hg * P.coef[g][jj][k];
+                if (two) {
+                    launch_flux3d(D.dm, Q, c->gas, c->st);
+                    c->launch_counter++;
+                } else {
+                    bool read_now = false;
+                    for (int h = 0; h < G; ++h) read_now = read_now || (h != g && stepping[h] && P.donor_of[g][h]);
+                    if (read_now) issue_step_visc(c, g, Q);
                 }
-                const double* base = D.Q[c->book.cur[g]];
-                launch_combine(P.nc, D.dm, make_box(mp.st_lo, mp.st_hi), base, m, src, cs, D.dstate, c->st);
-                c->launch_counter++;
+            } else if (partial[g]) {
+                issue_partial_donor(c, g, j, c->st);
                 state_of[g] = D.dstate;
-                issue_visc(c, g, D.dstate, make_box(mp.fv_lo, mp.fv_hi));
             }
         }
         for (int g = 0; g < G; ++g)
@@ -489,7 +496,12 @@ static void issue_macro_step(mrab_ctx* c) {
                 ep.src[k] = D.ring[slot];
                 ep.csrc[k] = hg * al[k];
             }
-            issue_rhs(c, g, D.Q[c->book.cur[g]], ep, state_of.data());
+            if (two) {
+                launch_div3d_pass(D.dm, ep.base, c->gas, ep, c->st);
+                c->launch_counter++;
+            } else {
+                issue_rhs(c, g, D.Q[c->book.cur[g]], ep, state_of.data());
+            }
             c->book.head[g] = newslot;
             c->book.pending[g] = 1;
             c->evals[g]++;
@@ -724,6 +736,267 @@ static void issue_macro_step_dag2d(mrab_ctx* c) {
     // join (bulk streams only if they joined the step)
     for (int s = 0; s <= 2 * G; ++s) {
         if (s > G && !bulk_used[s - G - 1]) continue;
+        cudaEvent_t e = dag_event(c);
+        cudaEventRecord(e, c->side[s]);
+        cudaStreamWaitEvent(c->st, e, 0);
+    }
+}
+
+
+// ----------------------------------------------------------------------------------------
+// 3-D macro step as a multi-stream task flow (captured into the phase graph).
+//
+// Launches are issued in a valid sequential order; every launch declares the buffers it reads
+// and writes, and the tracker below inserts the event waits that keep exactly those
+// dependencies (RAW, WAR, WAW) between streams.  Streams: one per mesh for its RHS (both
+// passes), one per donor mesh for the preparation of its donor data (intermediate state on
+// the donor box, Cartesian viscous fluxes), one per receiving mesh for its gathers.  The
+// donor data of a micro index jj is prepared and gathered as soon as its producers have been
+// issued (into the qhat/fvhat set jj of the receiver), so the latency-bound small kernels of
+// the fast substeps run beside the large RHS launches instead of between them -- the
+// single-GPU analogue of the paper's interleaved interpolation exchange.
+// Priorities (per node): preparation and gathers highest, then the meshes by rate.
+// ----------------------------------------------------------------------------------------
+namespace {
+struct Flow {
+    mrab_ctx* c;
+    struct Res {
+        DagNode w;
+        std::vector<DagNode> r;
+    };
+    std::map<const void*, Res> res;
+    std::vector<const void*> rd, wr;
+    int stream = -1;
+    std::vector<char> used;
+    cudaEvent_t fork = nullptr;
+    explicit Flow(mrab_ctx* c_) : c(c_), used(3 * kMaxMeshes + 1, 0) {}
+    // waits of a launch on stream s that reads `reads` and writes `writes`
+    void begin(int s, std::initializer_list<const void*> reads, std::initializer_list<const void*> writes) {
+        stream = s;
+        if (!used[s]) {   // a stream joins the step (and the capture) at its first launch
+            cudaStreamWaitEvent(c->side[s], fork, 0);
+            used[s] = 1;
+        }
+        rd.assign(reads.begin(), reads.end());
+        wr.assign(writes.begin(), writes.end());
+        for (const void* k : rd)
+            if (k) dag_wait(c, s, res[k].w);
+        for (const void* k : wr) {
+            if (!k) continue;
+            Res& R = res[k];
+            dag_wait(c, s, R.w);
+            for (auto& n : R.r) dag_wait(c, s, n);
+        }
+    }
+    void add_read(const void* k) {
+        if (!k) return;
+        dag_wait(c, stream, res[k].w);
+        rd.push_back(k);
+    }
+    void end() {
+        const DagNode n = dag_done(c, stream);
+        for (const void* k : rd)
+            if (k) res[k].r.push_back(n);
+        for (const void* k : wr) {
+            if (!k) continue;
+            Res& R = res[k];
+            R.w = n;
+            R.r.clear();
+        }
+    }
+};
+}  // namespace
+
+static void issue_macro_step_dag3d(mrab_ctx* c) {
+    const Plan& P = *c->P;
+    const int G = (int)P.meshes.size(), m = P.history_m, S = P.S;
+    c->evnext = 0;
+    Flow F(c);
+    auto sp = [&](int h) { return G + 1 + h; };        // donor-preparation stream of mesh h
+    auto sg = [&](int g) { return 2 * G + 1 + g; };    // gather stream of mesh g
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    // priority of a mesh's RHS by rate rank (fastest just below the small kernels)
+    std::vector<int> ranks;
+    for (auto& q : P.meshes) ranks.push_back(q.s);
+    std::sort(ranks.begin(), ranks.end());
+    ranks.erase(std::unique(ranks.begin(), ranks.end()), ranks.end());
+    auto mesh_prio = [&](int g) {
+        const int r = (int)(std::find(ranks.begin(), ranks.end(), P.meshes[g].s) - ranks.begin());
+        return std::min(least, greatest + 1 + r);
+    };
+    F.fork = dag_event(c);
+    cudaEventRecord(F.fork, c->st);
+    int tq[kMaxMeshes][2], tring[kMaxMeshes];
+    for (int g = 0; g < G; ++g) {
+        const int sgm = P.meshes[g].s;
+        const int cur = c->book.cur[g];
+        tq[g][cur] = -sgm;
+        tq[g][cur ^ 1] = 0;
+        tring[g] = -sgm;
+    }
+    auto buf_at = [&](int g, int t) -> int {
+        if (tq[g][0] == t) return 0;
+        if (tq[g][1] == t) return 1;
+        return -1;
+    };
+    auto steps_at = [&](int g, int j) { return j % P.meshes[g].s == 0; };
+    std::vector<std::vector<int>> emitted(G, std::vector<int>(S, 0));
+    auto stamp = [&](int s, int kind, int g, int j, int end) {
+        if (c->trace) launch_stamp(c->trace, (end << 15) | (kind << 12) | (g << 8) | (j & 0xff), c->side[s]);
+    };
+    bool two = !opts().z3_fused;
+    for (int g = 0; g < G; ++g) two = two && c->md[g].FH;
+    for (int j = 0; j < S; ++j) {
+        // ---- flux pass of the meshes stepping at j (two-pass RHS): Fhat everywhere, F^V on the
+        //      SAT and donor-stencil tiles ----
+        for (int g = 0; g < G; ++g) {
+            if (!steps_at(g, j)) continue;
+            MeshDev& D = c->md[g];
+            if (c->book.pending[g]) {
+                c->book.cur[g] ^= 1;
+                c->book.pending[g] = 0;
+            }
+            if (!two) continue;
+            const double* Q = D.Q[c->book.cur[g]];
+            F.begin(g, {Q}, {D.FV, D.FH});
+            set_launch_priority(1, mesh_prio(g));
+            stamp(g, 4, g, j, 0);
+            launch_flux3d(D.dm, Q, c->gas, c->side[g]);
+            stamp(g, 4, g, j, 1);
+            c->launch_counter++;
+            F.end();
+        }
+        // ---- donor data of every micro index jj >= j whose producers have been issued ----
+        for (int jj = j; jj < S; ++jj) {
+            std::vector<int> recv;
+            for (int g = 0; g < G; ++g)
+                if (steps_at(g, jj) && !emitted[g][jj]) recv.push_back(g);
+            if (recv.empty()) continue;
+            std::vector<int> need(G, 0);
+            for (int g : recv)
+                for (int h = 0; h < G; ++h)
+                    if (h != g && P.donor_of[h][g] && !P.meshes[g].rpoint.empty()) need[h] = 1;
+            bool ready = true;
+            for (int h = 0; h < G && ready; ++h) {
+                if (!need[h]) continue;
+                if (steps_at(h, jj)) {
+                    // a stepping donor's F^V comes from its flux pass at jj (two-pass), else from
+                    // k_visc3d_x on its state, known once its previous RHS has been issued
+                    ready = two ? jj == j : (buf_at(h, jj) >= 0 && (jj - P.meshes[h].s < j));
+                } else {
+                    const int th = jj - jj % P.meshes[h].s;
+                    ready = th < j && tring[h] == th;
+                }
+            }
+            if (!ready) continue;   // (jj == j is always ready: its producers precede j)
+            set_launch_priority(1, greatest);
+            std::vector<const double*> state_of(G, nullptr);
+            for (int h = 0; h < G; ++h) {
+                MeshDev& D = c->md[h];
+                const MeshPlan& mh = P.meshes[h];
+                if (steps_at(h, jj)) {
+                    const int b = buf_at(h, jj);
+                    state_of[h] = D.Q[b < 0 ? c->book.cur[h] : b];
+                    if (!two && need[h] && P.viscous && D.nfv > 0) {
+                        F.begin(sp(h), {state_of[h]}, {D.FV});
+                        stamp(sp(h), 6, h, jj, 0);
+                        launch_visc(D.dm, state_of[h], D.FV, Box{}, D.fvlist, D.nfv, c->gas, c->side[sp(h)]);
+                        stamp(sp(h), 6, h, jj, 1);
+                        c->launch_counter++;
+                        F.end();
+                    }
+                } else if (need[h]) {
+                    const int th = jj - jj % mh.s;
+                    const int b = buf_at(h, th);
+                    const double* base = D.Q[b < 0 ? c->book.cur[h] : b];
+                    F.begin(sp(h), {base}, {D.dstate, D.FV});
+                    for (int k = 0; k < m; ++k) F.add_read(D.ring[k]);
+                    stamp(sp(h), 6, h, jj, 0);
+                    issue_partial_donor(c, h, jj, c->side[sp(h)], base);
+                    stamp(sp(h), 6, h, jj, 1);
+                    F.end();
+                    state_of[h] = D.dstate;
+                } else {
+                    state_of[h] = D.Q[c->book.cur[h]];   // not read
+                }
+            }
+            for (int g : recv) {
+                emitted[g][jj] = 1;
+                MeshDev& D = c->md[g];
+                const MeshPlan& mg = P.meshes[g];
+                if (mg.rpoint.empty()) continue;
+                RecvList rl{};
+                rl.n = (int64_t)mg.rpoint.size();
+                rl.point = D.rpoint;
+                rl.donor = D.rdonor;
+                rl.base = D.rbase;
+                rl.w = D.rw;
+                rl.qhat = qhat_set(c, g, jj);
+                rl.fvhat = fvhat_set(c, g, jj);
+                rl.gorder = D.gorder;
+                rl.ginfo = D.ginfo;
+                rl.ngroups = D.ngroups;
+                F.begin(sg(g), {}, {rl.qhat});
+                for (int h = 0; h < G; ++h) {
+                    if (h == g || !P.donor_of[h][g]) continue;
+                    F.add_read(state_of[h]);
+                    if (P.viscous) F.add_read(c->md[h].FV);
+                }
+                stamp(sg(g), 7, g, jj, 0);
+                launch_interp(P.viscous, rl, make_ds(c, state_of.data()), c->side[sg(g)]);
+                stamp(sg(g), 7, g, jj, 1);
+                c->launch_counter++;
+                F.end();
+            }
+        }
+        // ---- divergence + SAT + AB update of the meshes stepping at j ----
+        for (int g = 0; g < G; ++g) {
+            if (!steps_at(g, j)) continue;
+            MeshDev& D = c->md[g];
+            const MeshPlan& mp = P.meshes[g];
+            const double hg = P.h * mp.s;
+            const int newslot = (c->book.head[g] + 1) % m;
+            Epilogue ep{};
+            ep.r_out = D.ring[newslot];
+            ep.y_out = D.Q[c->book.cur[g] ^ 1];
+            ep.base = D.Q[c->book.cur[g]];
+            const std::vector<double>& al = P.coef[g][mp.s];
+            ep.c_new = hg * al[m - 1];
+            ep.nsrc = m - 1;
+            double* qh = qhat_set(c, g, j);
+            // (the divergence pass reads FV at the SAT points and FH; declared as writes so that
+            // it also orders against the gathers still reading FV)
+            F.begin(g, {ep.base, mp.rpoint.empty() ? nullptr : qh}, {ep.r_out, ep.y_out, D.FV, D.FH});
+            for (int k = 0; k < m - 1; ++k) {
+                const int slot = ((c->book.head[g] - (m - 2) + k) % m + m) % m;
+                ep.src[k] = D.ring[slot];
+                ep.csrc[k] = hg * al[k];
+                F.add_read(ep.src[k]);
+            }
+            DevMesh dm = D.dm;
+            dm.qhat = qh;
+            dm.fvhat = fvhat_set(c, g, j);
+            ep.has_prio = 1;
+            ep.prio = mesh_prio(g);
+            set_launch_priority(1, ep.prio);
+            stamp(g, 5, g, j, 0);
+            if (two) launch_div3d_pass(dm, ep.base, c->gas, ep, c->side[g]);
+            else launch_rhs(3, dm, ep.base, c->gas, ep, DonorSet{}, c->side[g]);
+            stamp(g, 5, g, j, 1);
+            c->launch_counter++;
+            F.end();
+            c->book.head[g] = newslot;
+            c->book.pending[g] = 1;
+            c->evals[g]++;
+            tring[g] = j;
+            tq[g][c->book.cur[g] ^ 1] = j + mp.s;
+        }
+    }
+    set_launch_priority(0, 0);
+    // join
+    for (int s = 0; s <= 3 * G; ++s) {
+        if (!c->side[s] || !F.used[s]) continue;
         cudaEvent_t e = dag_event(c);
         cudaEventRecord(e, c->side[s]);
         cudaStreamWaitEvent(c->st, e, 0);
@@ -972,9 +1245,14 @@ mrab_status mrab_create(const mrab_plan* plan, const double* const* q0, void* d_
             CK(cudaStreamCreateWithPriority(&c->side[g], cudaStreamNonBlocking, prio));
         }
         CK(cudaStreamCreateWithPriority(&c->side[P.meshes.size()], cudaStreamNonBlocking, greatest));
-        // bulk tiles of split meshes run on their own streams, concurrent with the critical tiles
-        for (int g = 0; g < (int)P.meshes.size(); ++g)
-            CK(cudaStreamCreateWithPriority(&c->side[P.meshes.size() + 1 + g], cudaStreamNonBlocking, least));
+        // 2-D: bulk tiles of split meshes run on their own streams, concurrent with the critical
+        // tiles; 3-D: donor-preparation and gather streams (highest priority)
+        for (int g = 0; g < (int)P.meshes.size(); ++g) {
+            CK(cudaStreamCreateWithPriority(&c->side[P.meshes.size() + 1 + g], cudaStreamNonBlocking,
+                                            P.dim == 3 ? greatest : least));
+            if (P.dim == 3)
+                CK(cudaStreamCreateWithPriority(&c->side[2 * P.meshes.size() + 1 + g], cudaStreamNonBlocking, greatest));
+        }
         // critical/bulk split of slow meshes with per-node launch priorities (on by default;
         // config 3: 0.1205 -> 0.110 ms per macro step; Options::overlap = 0 disables)
         c->overlap = P.opt.overlap != 0;
@@ -1038,6 +1316,36 @@ mrab_status mrab_create(const mrab_plan* plan, const double* const* q0, void* d_
             D.nfv = (int)lst.size();
             if (!lst.empty())
                 CK(cudaMemcpy(D.fvlist, lst.data(), lst.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+            // intermediate donor states are formed on these tiles and their face neighbours (the
+            // viscous pass reads the cross-shaped region tile + 3 along each axis)
+            {
+                std::vector<uint8_t> cb(fl);
+                const int nt3[3] = {tx, ty, tz};
+                for (int32_t t : lst) {
+                    const int tc[3] = {t % tx, (t / tx) % ty, t / (tx * ty)};
+                    for (int a = 0; a < 3; ++a)
+                        for (int sgn = -1; sgn <= 1; sgn += 2) {
+                            int q[3] = {tc[0], tc[1], tc[2]};
+                            // one tile on; two when that tile is a last partial tile thinner
+                            // than the reach of 3
+                            for (int hop = 0; hop < 2; ++hop) {
+                                q[a] += sgn;
+                                if (q[a] < 0 || q[a] >= nt3[a]) {
+                                    if (!m.periodic[a]) break;
+                                    q[a] = (q[a] + nt3[a]) % nt3[a];
+                                }
+                                cb[(size_t)q[0] + tx * ((size_t)q[1] + (size_t)ty * q[2])] = 1;
+                                if (m.n[a] - 8 * q[a] >= 3) break;
+                            }
+                        }
+                }
+                std::vector<int32_t> cl;
+                for (size_t t = 0; t < cb.size(); ++t)
+                    if (cb[t]) cl.push_back((int32_t)t);
+                D.ncb = (int)cl.size();
+                if (!cl.empty())
+                    CK(cudaMemcpy(D.cblist, cl.data(), cl.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+            }
             // two-pass RHS: the 8^3 tiles holding SAT points (k_flux3d writes F^V there)
             std::vector<uint8_t> st((size_t)tx * ty * tz, 0);
             for (int k = 0; k < m.n[2]; ++k)
@@ -1051,6 +1359,8 @@ mrab_status mrab_create(const mrab_plan* plan, const double* const* q0, void* d_
                         }
                         if (need) st[(size_t)(i / 8) + tx * ((size_t)(jj / 8) + (size_t)ty * (k / 8))] = 1;
                     }
+            // ... and the donor-stencil tiles (the gathers read F^V there at stepping times)
+            for (size_t t = 0; t < st.size(); ++t) st[t] = st[t] || fl[t];
             CK(cudaMemcpy(D.fvtile, st.data(), st.size(), cudaMemcpyHostToDevice));
         }
         CK(cudaMemcpy(D.recv_slot, m.recv_slot.data(), N * sizeof(int32_t), cudaMemcpyHostToDevice));
@@ -1170,6 +1480,7 @@ void mrab_destroy(mrab_ctx* c) {
 // or instantiation lands inside a later (timed) macro step.
 static mrab_status ensure_graphs(mrab_ctx* c) {
     if (c->graphs[0]) return MRAB_OK;
+    c->graph_k0 = std::max<int64_t>(c->macro - (c->P->history_m - 1), 0);
     const Book book0 = c->book;
     const std::vector<int64_t> ev_start = c->evals;
     for (int phase = 0; phase < c->period; ++phase) {
@@ -1214,9 +1525,9 @@ mrab_status mrab_step(mrab_ctx* c, int n_macro) {
             CK(cudaGetLastError());
         } else {
             const int64_t k = c->macro - nboot_macro;
-            const int phase = (int)(k % c->period);
             mrab_status st = ensure_graphs(c);
             if (st != MRAB_OK) return st;
+            const int phase = (int)((k - c->graph_k0) % c->period);
             c->book = c->book_after[phase];
             for (size_t g = 0; g < c->evals.size(); ++g) c->evals[g] += c->evals_per_phase[phase][g];
             CK(cudaGraphLaunch(c->graphs[phase], c->st));

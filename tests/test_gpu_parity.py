@@ -124,15 +124,17 @@ def test_nonfinite_reported():
     ctx.close()
 
 
-@pytest.mark.parametrize("cid,kw", [(3, {"sr": 4}), (2, {})])
+@pytest.mark.parametrize("cid,kw", [(3, {"sr": 4}), (2, {}), (4, {}), (5, {"order_n": 4}), (5, {"order_n": 2})])
 def test_overlapped_schedule_is_bitwise_serial(cid, kw, monkeypatch):
-    """The overlapped macro step (critical/bulk split of the slow mesh on two streams, node
-    priorities) only reorders independent launches: states equal the serial schedule's bit for
-    bit."""
+    """The overlapped macro step (2-D: critical/bulk split of the slow mesh on two streams;
+    3-D: per-mesh RHS, donor-preparation and gather streams with the donor data of later micro
+    indices prepared ahead; node priorities) only reorders independent launches: states equal
+    the serial schedule's bit for bit."""
     p = synth.make_config(cid, "test", **kw)
     out = []
     for ov in ("0", "1"):
         monkeypatch.setenv("MRAB_OVERLAP", ov)
+        monkeypatch.setenv("MRAB_OVERLAP3D", ov)
         plan = mrab.Plan(p)
         ctx = mrab.Context(plan, p.q0)
         ctx.step(p.history_m - 1 + 6)
