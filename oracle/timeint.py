@@ -17,6 +17,7 @@ recording RHS values at the mesh-aligned times.  R8 the N-rate generalisation:
     2. meshes with j mod s_g == 0: R_g = RHS_g(all y) at t + j h
     3. for those: push R_g into ring_g, base_g <- y_g, t_g <- t + j h.
 SRAB (single-rate AB) is the same code with every s_g = 1.
+macro_step_var(H): the same with a macro step that changes from step to step.
 """
 from __future__ import annotations
 
@@ -88,6 +89,9 @@ class MRAB:
         self.counts = [0] * G
         self.macro = 0
         self._w = {}
+        self.rtimes = None                           # variable-step mode: history node times
+        self.time = None
+        self.tgp = None
 
     def weights(self, theta):
         key = Fr(theta)
@@ -119,6 +123,8 @@ class MRAB:
             assert len(self.rings[g]) == self.m
 
     def macro_step(self):
+        if self.rtimes is not None:                  # after variable steps: nodes are not uniform
+            return self.macro_step_var(self.S * Fr(self.h))
         G = len(self.base)
         for j in range(1, self.S + 1):
             tj = self.t + j
@@ -139,6 +145,42 @@ class MRAB:
                 self.tg[g] = tj
                 self.counts[g] += 1
         self.t = self.t + self.S
+        self.macro += 1
+
+    def macro_step_var(self, H):
+        """One macro step of size H (physical time) with h = H / S_max: "The macro-timestep
+        H_i can change on a per-macrostep basis, with the micro-timestep h_i defined such that
+        h_i = H_i/SR".  The history values of a mesh then sit at non-uniform times,
+        so the weights of every (partial) integral come from eq:vandermonde with
+        the actual node times: y_g = base_g + sum_k w_k R_{g,k}, w = ab_weights(nodes - t_g,
+        n, 0, t + j h - t_g) (physical time units; reduces to macro_step for constant H)."""
+        G = len(self.base)
+        if self.rtimes is None:
+            h0 = Fr(self.h)
+            self.time = h0 * self.t
+            self.rtimes = [[self.time - (self.m - 1 - k) * self.s[g] * h0 for k in range(self.m)]
+                           for g in range(G)]
+            self.tgp = [self.time] * G
+        h = Fr(H) / self.S
+        for j in range(1, self.S + 1):
+            tj = self.time + j * h
+            ys = []
+            for g in range(G):
+                nodes = [tau - self.tgp[g] for tau in self.rtimes[g]]
+                w = abcoef.ab_weights(nodes, self.n, 0, tj - self.tgp[g])
+                y = self.base[g].copy()
+                for wk, Rk in zip(w, self.rings[g]):
+                    y = y + float(wk) * Rk
+                ys.append(y)
+            stepping = [g for g in range(G) if j % self.s[g] == 0]
+            R = self.rhs_fn(ys, which=stepping)
+            for g in stepping:
+                self.rings[g] = self.rings[g][1:] + [R[g]]
+                self.rtimes[g] = self.rtimes[g][1:] + [tj]
+                self.base[g] = ys[g]
+                self.tgp[g] = tj
+                self.counts[g] += 1
+        self.time = self.time + Fr(H)
         self.macro += 1
 
     def run(self, n_macro):
