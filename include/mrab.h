@@ -180,6 +180,25 @@ void        mrab_destroy(mrab_ctx* ctx);
  * steps).  Asynchronous on the context stream.  Errors: CUDA, INVALID. */
 mrab_status mrab_step(mrab_ctx* ctx, int n_macro);
 
+/* Variable macro step ("The macro-timestep H_i can change on a per-macrostep basis,
+ * with the micro-timestep h_i defined such that h_i = H_i/SR"): advance n_macro MRAB macro
+ * steps of size H (micro step H / S_max).  The history values of a mesh then sit at
+ * non-uniform times; every (partial) AB weight set is recomputed from eq:vandermonde
+ * with the actual node times, on the host, per launch (no CUDA graph: the
+ * weights are launch arguments).  After the first call, mrab_step also takes this path with
+ * H = S_max h.  Asynchronous on the caller's stream.  Errors: INVALID (H <= 0),
+ * INSUFFICIENT_HISTORY (called before the m-1 bootstrap macro steps), CUDA. */
+mrab_status mrab_step_h(mrab_ctx* ctx, int n_macro, double H);
+
+/* Stable-timestep estimate on the device (eq:ts_inv, eq:ts_visc, eq:ts_overall, P:620-643;
+ * reading R20 of DESIGN.md for the garbled parentheses): dt_mesh[g] (host, [n_meshes]) =
+ * min over the active points of mesh g, at its current state, of
+ *   J^-1 / [ sum_k (|U . M_k| + c |M_k|) + 2 nu* J (sum_k |M_k|)^2 ],  M_k = J^-1 grad(kappa_k),
+ * nu* = max(1, gamma/Pr)/(rho Re) (viscous problems; Euler: the first sum only).  One
+ * reduction kernel per mesh; synchronises (8 bytes per mesh come back).  The caller forms
+ * H = CFL * S_max * min_g dt_mesh[g] / s_g and passes it to mrab_step_h.  Errors: INVALID, CUDA. */
+mrab_status mrab_dt(mrab_ctx* ctx, double* dt_mesh);
+
 /* Copy mesh `mesh`'s state at the current macro boundary to dst (host or device, dense
  * [nc][n...]); *t (may be NULL) receives the time.  Synchronises. */
 mrab_status mrab_get_state(mrab_ctx* ctx, int mesh, double* dst, double* t);

@@ -2070,6 +2070,73 @@ void launch_stamp(unsigned long long* trace, int tag, cudaStream_t st) {
     if (trace) launch_k(k_stamp, dim3(1), dim3(1), 0, st, trace, tag);
 }
 
+// ------------------------------------------------------------------------------------
+// K9: stable-timestep estimate of one mesh (eq:ts_inv / eq:ts_visc / eq:ts_overall, P:620-643;
+// reading R20): per active point, with M_k = J^-1 grad(kappa_k),
+//   dt = J^-1 / [ sum_k (|U . M_k| + c |M_k|) + 2 nu* J (sum_k |M_k|)^2 ],
+//   nu* = max(1, gamma/Pr) / (rho Re)  (the last term for viscous problems only),
+// then the minimum over the mesh: warp shuffles, one atomicMin per CTA on the bit pattern
+// (positive doubles order like unsigned integers).
+// ------------------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(256) k_dt(DevMesh m, const double* __restrict__ Q, Gas g,
+                                            unsigned long long* __restrict__ out) {
+    const int64_t N = m.npts;
+    double best = __longlong_as_double(0x7ff0000000000000LL);   // +inf
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < N; p += (int64_t)gridDim.x * blockDim.x) {
+        if (!m.cls[p]) continue;
+        const double rho = Q[p];
+        double u[D], ke = 0.0;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            u[i] = Q[(1 + i) * N + p] / rho;
+            ke += u[i] * u[i];
+        }
+        const double pr = g.gm1 * (Q[(D + 1) * N + p] - 0.5 * rho * ke);
+        const double c = sqrt(g.gamma * pr / rho);
+        const double J = m.cart ? m.cJ : m.J[p];
+        double conv = 0.0, msum = 0.0;
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            double un = 0.0, mm = 0.0;
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+                const double mk = m.cart ? (i == k ? m.cM[k] : 0.0) : m.M[(int64_t)(k * D + i) * N + p];
+                un += u[i] * mk;
+                mm += mk * mk;
+            }
+            mm = sqrt(mm);
+            conv += fabs(un) + c * mm;
+            msum += mm;
+        }
+        const double Jinv = 1.0 / J;
+        double dt = Jinv / conv;
+        if (g.viscous) {
+            const double nu = fmax(1.0, g.gamma / g.Pr) / (rho * g.Re);
+            dt = fmin(dt, Jinv / (conv + 2.0 * nu * J * msum * msum));
+        }
+        best = fmin(best, dt);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) best = fmin(best, __shfl_xor_sync(0xffffffffu, best, o));
+    __shared__ double wb[8];
+    if ((threadIdx.x & 31) == 0) wb[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; ++w) best = fmin(best, wb[w]);
+        atomicMin(out, (unsigned long long)__double_as_longlong(best));
+    }
+}
+
+void launch_dt(int dim, const DevMesh& m, const double* Q, const Gas& gas, double* out, cudaStream_t st) {
+    // out starts at +inf
+    static const unsigned long long inf = 0x7ff0000000000000ULL;
+    cudaMemcpyAsync(out, &inf, sizeof(inf), cudaMemcpyHostToDevice, st);
+    const unsigned grid = (unsigned)std::min<int64_t>((m.npts + 255) / 256, (int64_t)sm_count() * 8);
+    if (dim == 2) k_dt<2><<<grid, 256, 0, st>>>(m, Q, gas, (unsigned long long*)out);
+    else k_dt<3><<<grid, 256, 0, st>>>(m, Q, gas, (unsigned long long*)out);
+}
+
 void launch_l2_scrub(void* a, void* b, size_t bytes, int tag, cudaStream_t st) {
     cudaMemsetAsync(a, tag & 0xff, bytes, st);
     k_scrub_read<<<148 * 8, 256, 0, st>>>((const double4*)b, bytes / sizeof(double4), (double*)a);

@@ -202,6 +202,8 @@ void upload_stencil_rows();
 void launch_l2_scrub(void* a, void* b, size_t bytes, int tag, cudaStream_t st);
 // sets *flag (device int) if any of the n doubles is not finite
 void launch_finite(const double* a, size_t n, int* flag, cudaStream_t st);
+// K9: *out (device double) = min over the active points of mesh m of the eq:ts timestep
+void launch_dt(int dim, const DevMesh& m, const double* Q, const Gas& gas, double* out, cudaStream_t st);
 // launch priority of the 3-D launches that follow on this thread (has = 0: plain launches)
 void set_launch_priority(int has, int prio);
 // timeline stamp (mrab_set_trace): one record (tag, now, now) appended by a 1-thread kernel

@@ -118,6 +118,13 @@ struct mrab_ctx {
     int64_t launches_last = 0;
     int64_t launch_counter = 0;
     int64_t graph_k0 = 0;         // MRAB macro-step index the phase-0 graph was captured at
+    // variable macro step (mrab_step_h): micro step of the macro step being issued
+    // and the times of the ring entries relative to its start (valid once var_mode is set)
+    bool var_mode = false;
+    double h_cur = 0.0;
+    double time_extra = 0.0;      // simulated time taken in variable steps
+    int64_t macro_fixed = 0;      // macro steps taken at the plan's fixed step
+    double ring_t[kMaxMeshes][kMaxHist] = {};
     // 2-D multi-stream schedule: one stream per mesh (priority by rate) + a gather stream
     // 2-D: meshes [0, G), the gather stream G, bulk launches of split meshes G+1+g;
     // 3-D: meshes [0, G), donor-preparation streams G+1+h, gather streams 2G+1+g
@@ -397,6 +404,59 @@ static void issue_rhs(mrab_ctx* c, int g, const double* Q, const Epilogue& ep,
     c->launch_counter++;
 }
 
+// ----------------------------------------------------------------------------------------
+// step size and AB weights of the macro step being issued: the plan's tables (fixed step), or
+// -- variable macro step, P:581-583 -- eq:vandermonde with the actual history node times
+// ----------------------------------------------------------------------------------------
+static double h_micro(const mrab_ctx* c) { return c->var_mode ? c->h_cur : c->P->h; }
+
+// weights (oldest first, m entries) of y = base + h_g sum_k w_k R_k over [0, (j - th)/s_g] for
+// mesh g at micro index j, from its ring as it stands (newest entry at its last step th)
+static void weights_partial(const mrab_ctx* c, int g, int j, double* w) {
+    const Plan& P = *c->P;
+    const int m = P.history_m, sg = P.meshes[g].s;
+    if (!c->var_mode) {
+        for (int k = 0; k < m; ++k) w[k] = P.coef[g][j % sg][k];
+        return;
+    }
+    const double hg = c->h_cur * sg;
+    const int head = c->book.head[g];
+    const double tg = c->ring_t[g][head];
+    double nodes[kMaxHist];
+    for (int k = 0; k < m; ++k) {
+        const int slot = ((head - (m - 1) + k) % m + m) % m;
+        nodes[k] = (c->ring_t[g][slot] - tg) / hg;
+    }
+    nodes[m - 1] = 0.0;
+    ab_weights(nodes, m, P.order_n, 0.0, (double)(j % sg) / sg, w, nullptr);
+}
+
+// weights of the full step mesh g takes at micro index j: its m - 1 newest ring entries and
+// the evaluation at j (node 0), over [0, 1] in units of h_g
+static void weights_full(const mrab_ctx* c, int g, int j, double* w) {
+    const Plan& P = *c->P;
+    const int m = P.history_m, sg = P.meshes[g].s;
+    if (!c->var_mode) {
+        for (int k = 0; k < m; ++k) w[k] = P.coef[g][sg][k];
+        return;
+    }
+    const double hg = c->h_cur * sg;
+    const int head = c->book.head[g];
+    const double tg = j * c->h_cur;
+    double nodes[kMaxHist];
+    for (int k = 0; k < m - 1; ++k) {
+        const int slot = ((head - (m - 2) + k) % m + m) % m;
+        nodes[k] = (c->ring_t[g][slot] - tg) / hg;
+    }
+    nodes[m - 1] = 0.0;
+    ab_weights(nodes, m, P.order_n, 0.0, 1.0, w, nullptr);
+}
+
+// bookkeeping of a push by mesh g at micro index j
+static void note_push(mrab_ctx* c, int g, int j, int newslot) {
+    if (c->var_mode) c->ring_t[g][newslot] = j * c->h_cur;
+}
+
 // 3-D: donor data of mesh g at micro index j of the macro step where g does not step: the
 // intermediate state base + h_g sum_k beta_k^(j) R_k (MRAB Steps 2/5) and its
 // Cartesian viscous fluxes, formed into dstate / FV on the donor-stencil tiles (and their
@@ -406,14 +466,14 @@ static void issue_partial_donor(mrab_ctx* c, int g, int j, cudaStream_t st, cons
     MeshDev& D = c->md[g];
     const MeshPlan& mp = P.meshes[g];
     const int m = P.history_m;
-    const int jj = j % mp.s;
-    const double hg = P.h * mp.s;
+    const double hg = h_micro(c) * mp.s;
     const double* src[kMaxHist];
-    double cs[kMaxHist];
+    double cs[kMaxHist], w[kMaxHist];
+    weights_partial(c, g, j, w);
     for (int k = 0; k < m; ++k) {
         int slot = ((c->book.head[g] - (m - 1) + k) % m + m) % m;   // oldest first
         src[k] = D.ring[slot];
-        cs[k] = hg * P.coef[g][jj][k];
+        cs[k] = hg * w[k];
     }
     if (!base) base = D.Q[c->book.cur[g]];
     launch_combine_tiles(P.nc, D.dm, P.viscous ? D.cblist : D.fvlist, P.viscous ? D.ncb : D.nfv, base, m, src,
@@ -482,13 +542,14 @@ static void issue_macro_step(mrab_ctx* c) {
             if (!stepping[g]) continue;
             MeshDev& D = c->md[g];
             const MeshPlan& mp = P.meshes[g];
-            const double hg = P.h * mp.s;
+            const double hg = h_micro(c) * mp.s;
             const int newslot = (c->book.head[g] + 1) % m;
             Epilogue ep{};
             ep.r_out = D.ring[newslot];
             ep.y_out = D.Q[c->book.cur[g] ^ 1];
             ep.base = D.Q[c->book.cur[g]];
-            const std::vector<double>& al = P.coef[g][mp.s];   // full step, oldest first
+            double al[kMaxHist];   // full step, oldest first
+            weights_full(c, g, j, al);
             ep.c_new = hg * al[m - 1];
             ep.nsrc = m - 1;
             for (int k = 0; k < m - 1; ++k) {
@@ -503,6 +564,7 @@ static void issue_macro_step(mrab_ctx* c) {
                 issue_rhs(c, g, D.Q[c->book.cur[g]], ep, state_of.data());
             }
             c->book.head[g] = newslot;
+            note_push(c, g, j, newslot);
             c->book.pending[g] = 1;
             c->evals[g]++;
         }
@@ -625,12 +687,14 @@ static void issue_macro_step_dag2d(mrab_ctx* c) {
                     const int th = jj - jj % mh.s;
                     int b = buf_at(h, th);
                     ss.base[h] = c->md[h].Q[b < 0 ? 0 : b];
-                    const double hg = P.h * mh.s;
+                    const double hg = h_micro(c) * mh.s;
                     ss.nsrc[h] = m;
+                    double w[kMaxHist];
+                    weights_partial(c, h, jj, w);
                     for (int k = 0; k < m; ++k) {
                         int slot = ((c->book.head[h] - (m - 1) + k) % m + m) % m;
                         ss.src[h][k] = c->md[h].ring[slot];
-                        ss.c[h][k] = hg * P.coef[h][jj % mh.s][k];
+                        ss.c[h][k] = hg * w[k];
                     }
                 }
             }
@@ -666,13 +730,14 @@ static void issue_macro_step_dag2d(mrab_ctx* c) {
             }
             dag_wait(c, g, gnode[g][j]);
             for (auto& r : readers[g]) dag_wait(c, g, r);     // WAR on ring slot / state buffer
-            const double hg = P.h * mp.s;
+            const double hg = h_micro(c) * mp.s;
             const int newslot = (c->book.head[g] + 1) % m;
             Epilogue ep{};
             ep.r_out = D.ring[newslot];
             ep.y_out = D.Q[c->book.cur[g] ^ 1];
             ep.base = D.Q[c->book.cur[g]];
-            const std::vector<double>& al = P.coef[g][mp.s];
+            double al[kMaxHist];
+            weights_full(c, g, j, al);
             ep.c_new = hg * al[m - 1];
             ep.nsrc = m - 1;
             for (int k = 0; k < m - 1; ++k) {
@@ -727,6 +792,7 @@ static void issue_macro_step_dag2d(mrab_ctx* c) {
             }
             readers[g].clear();
             c->book.head[g] = newslot;
+            note_push(c, g, j, newslot);
             c->book.pending[g] = 1;
             c->evals[g]++;
             tring[g] = j;
@@ -955,13 +1021,14 @@ static void issue_macro_step_dag3d(mrab_ctx* c) {
             if (!steps_at(g, j)) continue;
             MeshDev& D = c->md[g];
             const MeshPlan& mp = P.meshes[g];
-            const double hg = P.h * mp.s;
+            const double hg = h_micro(c) * mp.s;
             const int newslot = (c->book.head[g] + 1) % m;
             Epilogue ep{};
             ep.r_out = D.ring[newslot];
             ep.y_out = D.Q[c->book.cur[g] ^ 1];
             ep.base = D.Q[c->book.cur[g]];
-            const std::vector<double>& al = P.coef[g][mp.s];
+            double al[kMaxHist];
+            weights_full(c, g, j, al);
             ep.c_new = hg * al[m - 1];
             ep.nsrc = m - 1;
             double* qh = qhat_set(c, g, j);
@@ -987,6 +1054,7 @@ static void issue_macro_step_dag3d(mrab_ctx* c) {
             c->launch_counter++;
             F.end();
             c->book.head[g] = newslot;
+            note_push(c, g, j, newslot);
             c->book.pending[g] = 1;
             c->evals[g]++;
             tring[g] = j;
@@ -1512,6 +1580,37 @@ static mrab_status join_user(mrab_ctx* c) {
     return MRAB_OK;
 }
 
+static const double* current_state(mrab_ctx* c, int g);
+
+// uniform history node times (ring entries at -h_g, -2 h_g, ... relative to the macro boundary)
+static void uniform_ring_times(mrab_ctx* c) {
+    const Plan& P = *c->P;
+    const int m = P.history_m;
+    for (size_t g = 0; g < P.meshes.size(); ++g)
+        for (int k = 0; k < m; ++k) {
+            const int slot = ((c->book.head[g] - k) % m + m) % m;   // k-th newest
+            c->ring_t[g][slot] = -(double)(k + 1) * P.meshes[g].s * P.h;
+        }
+}
+
+// one MRAB macro step of size H issued directly (no graph): the weights depend on H and on
+// the history node times, which change from step to step
+static mrab_status var_macro_step(mrab_ctx* c, double H) {
+    const Plan& P = *c->P;
+    if (!c->var_mode) {
+        uniform_ring_times(c);
+        c->var_mode = true;
+    }
+    c->h_cur = H / P.S;
+    issue_macro_step(c);
+    CK(cudaGetLastError());
+    for (size_t g = 0; g < P.meshes.size(); ++g)
+        for (int k = 0; k < P.history_m; ++k) c->ring_t[g][k] -= H;
+    c->time_extra += H;
+    c->macro++;
+    return MRAB_OK;
+}
+
 mrab_status mrab_step(mrab_ctx* c, int n_macro) {
     if (!c || n_macro < 0) return fail(MRAB_E_INVALID, "bad ctx / n_macro");
     const Plan& P = *c->P;
@@ -1520,6 +1619,12 @@ mrab_status mrab_step(mrab_ctx* c, int n_macro) {
     CK(cudaStreamWaitEvent(c->st, c->ev_in, 0));
     const int64_t nboot_macro = P.history_m - 1;
     for (int it = 0; it < n_macro; ++it) {
+        if (c->macro >= nboot_macro && c->var_mode) {
+            // after variable steps the history is not uniform: the fixed-step graphs do not apply
+            mrab_status st = var_macro_step(c, P.S * P.h);
+            if (st != MRAB_OK) return st;
+            continue;
+        }
         if (c->macro < nboot_macro) {
             for (int s = 0; s < P.S; ++s) issue_rk_step(c);
             CK(cudaGetLastError());
@@ -1533,6 +1638,7 @@ mrab_status mrab_step(mrab_ctx* c, int n_macro) {
             CK(cudaGraphLaunch(c->graphs[phase], c->st));
         }
         c->macro++;
+        c->macro_fixed++;
         if (c->macro == nboot_macro) {
             mrab_status st = ensure_graphs(c);
             if (st != MRAB_OK) return st;
@@ -1541,6 +1647,36 @@ mrab_status mrab_step(mrab_ctx* c, int n_macro) {
     CK(cudaGetLastError());
     CK(cudaEventRecord(c->ev_out, c->st));
     CK(cudaStreamWaitEvent(c->user, c->ev_out, 0));
+    return MRAB_OK;
+}
+
+mrab_status mrab_step_h(mrab_ctx* c, int n_macro, double H) {
+    if (!c || n_macro < 0 || !(H > 0.0)) return fail(MRAB_E_INVALID, "bad ctx / n_macro / H");
+    const Plan& P = *c->P;
+    if (c->macro < P.history_m - 1)
+        return fail(MRAB_E_INSUFFICIENT_HISTORY, "variable steps start after the RK bootstrap: call mrab_step(history_m - 1) first");
+    set_options(P.opt);
+    CK(cudaEventRecord(c->ev_in, c->user));
+    CK(cudaStreamWaitEvent(c->st, c->ev_in, 0));
+    for (int it = 0; it < n_macro; ++it) {
+        mrab_status st = var_macro_step(c, H);
+        if (st != MRAB_OK) return st;
+    }
+    CK(cudaEventRecord(c->ev_out, c->st));
+    CK(cudaStreamWaitEvent(c->user, c->ev_out, 0));
+    return MRAB_OK;
+}
+
+mrab_status mrab_dt(mrab_ctx* c, double* dt_mesh) {
+    if (!c || !dt_mesh) return fail(MRAB_E_INVALID, "bad arguments");
+    const Plan& P = *c->P;
+    if (join_user(c) != MRAB_OK) return MRAB_E_CUDA;
+    double* dbuf = reinterpret_cast<double*>(reinterpret_cast<char*>(c->dflag) + 64);
+    for (size_t g = 0; g < P.meshes.size(); ++g)
+        launch_dt(P.dim, c->md[g].dm, current_state(c, (int)g), c->gas, dbuf + g, c->st);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(dt_mesh, dbuf, P.meshes.size() * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
     return MRAB_OK;
 }
 
@@ -1563,7 +1699,7 @@ mrab_status mrab_get_state(mrab_ctx* c, int mesh, double* dst, double* t) {
     int bad = 0;
     CK(cudaMemcpyAsync(&bad, c->dflag, sizeof(int), cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
-    if (t) *t = (double)c->macro * P.S * P.h;
+    if (t) *t = (double)c->macro_fixed * P.S * P.h + c->time_extra;
     if (bad)
         return fail(MRAB_E_NONFINITE, "mesh " + std::to_string(mesh) +
                                           ": non-finite state (rhs blowup); the state was copied");
@@ -1618,6 +1754,7 @@ mrab_status mrab_set_history(mrab_ctx* c, int mesh, int k, const double* src) {
     CK(cudaStreamSynchronize(c->st));
     CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->st));
     CK(cudaStreamSynchronize(c->st));
+    if (c->var_mode) uniform_ring_times(c);   // the entries are defined at uniform nodes (R-SM)
     return MRAB_OK;
 }
 

@@ -82,6 +82,8 @@ def lib():
         L.mrab_destroy.argtypes = [vp]
         L.mrab_destroy.restype = None
         L.mrab_step.argtypes = [vp, C.c_int]
+        L.mrab_step_h.argtypes = [vp, C.c_int, C.c_double]
+        L.mrab_dt.argtypes = [vp, dp]
         L.mrab_get_state.argtypes = [vp, C.c_int, vp, dp]
         L.mrab_set_state.argtypes = [vp, C.c_int, vp]
         L.mrab_get_history.argtypes = [vp, C.c_int, C.c_int, vp]
@@ -96,7 +98,7 @@ def lib():
                      "mrab_plan_get_tables", "mrab_plan_get_metrics", "mrab_create",
                      "mrab_step", "mrab_get_state", "mrab_set_state", "mrab_rhs",
                      "mrab_get_history", "mrab_set_history", "mrab_get_counters",
-                     "mrab_launches_per_macro_step", "mrab_time_kernel"):
+                     "mrab_launches_per_macro_step", "mrab_time_kernel", "mrab_step_h", "mrab_dt"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -107,7 +109,7 @@ EXPORTED = ["mrab_ab_weights", "mrab_plan_create", "mrab_plan_destroy", "mrab_pl
             "mrab_create", "mrab_destroy", "mrab_step", "mrab_get_state", "mrab_set_state",
             "mrab_rhs", "mrab_get_counters", "mrab_launches_per_macro_step", "mrab_time_kernel",
             "mrab_set_trace", "mrab_last_error", "mrab_get_history", "mrab_set_history",
-            "mrab_overset_build", "mrab_free", "mrab_plan_get_face_flags"]
+            "mrab_overset_build", "mrab_free", "mrab_plan_get_face_flags", "mrab_step_h", "mrab_dt"]
 
 
 def _check(st):
@@ -309,6 +311,16 @@ class Context:
 
     def step(self, n_macro=1):
         _check(lib().mrab_step(self.h, int(n_macro)))
+
+    def step_h(self, H, n_macro=1):
+        """n_macro MRAB macro steps of size H (variable macro step, mrab_step_h)."""
+        _check(lib().mrab_step_h(self.h, int(n_macro), float(H)))
+
+    def dt(self):
+        """Per-mesh minimum of the eq:ts stable timestep at the current states (mrab_dt)."""
+        out = (C.c_double * len(self.plan.shapes))()
+        _check(lib().mrab_dt(self.h, out))
+        return [float(v) for v in out]
 
     def get_state(self, g, out=None):
         """Copy mesh g's state into `out` (numpy array, or torch tensor on host or device)
