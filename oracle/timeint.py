@@ -18,6 +18,7 @@ recording RHS values at the mesh-aligned times.  R8 the N-rate generalisation:
     3. for those: push R_g into ring_g, base_g <- y_g, t_g <- t + j h.
 SRAB (single-rate AB) is the same code with every s_g = 1.
 macro_step_var(H): the same with a macro step that changes from step to step.
+macro_step_sf(reextrap): the two-rate slowest-first variants of P:536-548 (reading R-SF).
 """
 from __future__ import annotations
 
@@ -183,9 +184,81 @@ class MRAB:
         self.time = self.time + Fr(H)
         self.macro += 1
 
-    def run(self, n_macro):
+    def macro_step_sf(self, reextrap=False):
+        """Two-rate slowest-first macro step ("an algorithm in which the slow
+        component is instead advanced first", with "the choice of whether or not to
+        re-extrapolate the slow state after additional state and right-hand side information is
+        gathered at the micro-timestep level"; the paper gives no steps, reading R-SF of
+        DESIGN.md §2, after [gear1984multirate]).  Meshes with s_g = S are slow, s_g = 1 fast.
+          1. slow: y_s(t+H) = s(t) + H sum_k alpha_k R_{s,k}  (the AB step);
+             fast, extrapolated over the whole macro step: f~(t+H) = f(t) + h sum_k w_k(S) R_{f,k};
+          2. R_s(t+H) = a_s(f~(t+H), y_s(t+H))  -- the slow component is evaluated first;
+          3. for j = 1..S: f(t+jh) by its AB step; the slow state the fast RHS sees at t + j h,
+             j < S, is s(t) + H * (partial integral over [0, j/S] of the slow extrapolant):
+               reextrap = False: the extrapolant of Step 1 (history up to t);
+               reextrap = True : re-formed with R_s(t+H) as its newest node (nodes
+                                 -(m-2), ..., 0, 1 in units of H), i.e. an interpolant;
+             at j = S it is y_s(t+H); evaluate a_f, push;
+          4. push R_s(t+H), s(t+H) = y_s(t+H)."""
+        G = len(self.base)
+        S = self.S
+        slow = [g for g in range(G) if self.s[g] == S]
+        fast = [g for g in range(G) if self.s[g] == 1]
+        if S == 1 or len(slow) + len(fast) != G:
+            raise ValueError("slowest-first is defined here for two rates (1 and S > 1)")
+        H = self.h * S
+        m, n = self.m, self.n
+        nodes = abcoef.uniform_nodes(m)
+        w_full = [float(x) for x in abcoef.ab_weights(nodes, n, 0, 1)]
+        w_long = [float(x) for x in abcoef.ab_weights(nodes, n, 0, S)]
+
+        def comb(g, step, w, hist):
+            y = self.base[g].copy()
+            for wk, Rk in zip(w, hist):
+                y = y + (step * wk) * Rk
+            return y
+        ys = [None] * G
+        for g in slow:
+            ys[g] = comb(g, H, w_full, self.rings[g])
+        for g in fast:
+            ys[g] = comb(g, self.h, w_long, self.rings[g])
+        Rs = self.rhs_fn(ys, which=slow)
+        y_slow_end = {g: ys[g] for g in slow}
+        for g in slow:
+            self.counts[g] += 1
+        for j in range(1, S + 1):
+            ys = [None] * G
+            for g in fast:
+                ys[g] = comb(g, self.h, w_full, self.rings[g])
+            for g in slow:
+                if j == S:
+                    ys[g] = y_slow_end[g]
+                elif reextrap:
+                    nd = [Fr(-(m - 2) + k) for k in range(m)]          # ..., 0, 1
+                    w = [float(x) for x in abcoef.ab_weights(nd, n, 0, Fr(j, S))]
+                    ys[g] = comb(g, H, w, self.rings[g][1:] + [Rs[g]])
+                else:
+                    w = [float(x) for x in abcoef.ab_weights(nodes, n, 0, Fr(j, S))]
+                    ys[g] = comb(g, H, w, self.rings[g])
+            R = self.rhs_fn(ys, which=fast)
+            for g in fast:
+                self.rings[g] = self.rings[g][1:] + [R[g]]
+                self.base[g] = ys[g]
+                self.counts[g] += 1
+        for g in slow:
+            self.rings[g] = self.rings[g][1:] + [Rs[g]]
+            self.base[g] = y_slow_end[g]
+        self.t = self.t + S
+        self.tg = [self.t] * G
+        self.macro += 1
+
+    def run(self, n_macro, scheme="fastest_first"):
         if not self.rings[0]:
             self.bootstrap()
+        if scheme != "fastest_first":
+            for _ in range(n_macro):
+                self.macro_step_sf(reextrap=(scheme == "slowest_first_reextrap"))
+            return self.base
         for _ in range(n_macro):
             self.macro_step()
         return self.base
