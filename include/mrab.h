@@ -190,6 +190,19 @@ mrab_status mrab_step(mrab_ctx* ctx, int n_macro);
  * INSUFFICIENT_HISTORY (called before the m-1 bootstrap macro steps), CUDA. */
 mrab_status mrab_step_h(mrab_ctx* ctx, int n_macro, double H);
 
+/* MRAB evaluation order ("The order in which we evaluate and advance the solution
+ * components" and "whether or not to re-extrapolate the slow state"; the paper prints steps for
+ * fastest-first only, reading R-SF of DESIGN.md §2 for the other two).  mrab_step_scheme with
+ * MRAB_SCHEME_FASTEST_FIRST is mrab_step.  The slowest-first schemes need exactly two rates
+ * (step multiples 1 and S > 1): per macro step the slow meshes' RHS at t + H is evaluated
+ * first, from the fast meshes' states extrapolated over [t, t + H]; the fast substeps then
+ * read slow states from the extrapolant with history up to t (SLOWEST_FIRST) or re-formed
+ * with R_s(t + H) as its newest node (SLOWEST_FIRST_REEXTRAP).  Same kernels, launched
+ * directly (no CUDA graph).  The scheme of a context is fixed by its first MRAB step; the
+ * history accessors and mrab_step_h apply to fastest-first contexts.  Errors: INVALID. */
+enum { MRAB_SCHEME_FASTEST_FIRST = 0, MRAB_SCHEME_SLOWEST_FIRST = 1, MRAB_SCHEME_SLOWEST_FIRST_REEXTRAP = 2 };
+mrab_status mrab_step_scheme(mrab_ctx* ctx, int n_macro, int scheme);
+
 /* Stable-timestep estimate on the device (eq:ts_inv, eq:ts_visc, eq:ts_overall, P:620-643;
  * reading R20 of DESIGN.md for the garbled parentheses): dt_mesh[g] (host, [n_meshes]) =
  * min over the active points of mesh g, at its current state, of

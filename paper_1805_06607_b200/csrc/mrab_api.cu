@@ -120,6 +120,8 @@ struct mrab_ctx {
     int64_t graph_k0 = 0;         // MRAB macro-step index the phase-0 graph was captured at
     // variable macro step (mrab_step_h): micro step of the macro step being issued
     // and the times of the ring entries relative to its start (valid once var_mode is set)
+    int scheme = -1;              // MRAB scheme of this context, fixed by its first MRAB step
+    bool sf_primed = false;       // slowest-first: R_s(t) sits uncommitted in the spare buffer
     bool var_mode = false;
     double h_cur = 0.0;
     double time_extra = 0.0;      // simulated time taken in variable steps
@@ -461,6 +463,19 @@ static void note_push(mrab_ctx* c, int g, int j, int newslot) {
 // intermediate state base + h_g sum_k beta_k^(j) R_k (MRAB Steps 2/5) and its
 // Cartesian viscous fluxes, formed into dstate / FV on the donor-stencil tiles (and their
 // face neighbours for the state: the viscous pass reads tile + 3 along each axis)
+static void issue_partial_donor_w(mrab_ctx* c, int g, cudaStream_t st, const double* base, int nsrc,
+                                  const double* const* src, const double* cs) {
+    const Plan& P = *c->P;
+    MeshDev& D = c->md[g];
+    launch_combine_tiles(P.nc, D.dm, P.viscous ? D.cblist : D.fvlist, P.viscous ? D.ncb : D.nfv, base, nsrc,
+                         src, cs, D.dstate, st);
+    c->launch_counter++;
+    if (P.viscous && D.nfv > 0) {
+        launch_visc(D.dm, D.dstate, D.FV, Box{}, D.fvlist, D.nfv, c->gas, st);
+        c->launch_counter++;
+    }
+}
+
 static void issue_partial_donor(mrab_ctx* c, int g, int j, cudaStream_t st, const double* base = nullptr) {
     const Plan& P = *c->P;
     MeshDev& D = c->md[g];
@@ -476,13 +491,7 @@ static void issue_partial_donor(mrab_ctx* c, int g, int j, cudaStream_t st, cons
         cs[k] = hg * w[k];
     }
     if (!base) base = D.Q[c->book.cur[g]];
-    launch_combine_tiles(P.nc, D.dm, P.viscous ? D.cblist : D.fvlist, P.viscous ? D.ncb : D.nfv, base, m, src,
-                         cs, D.dstate, st);
-    c->launch_counter++;
-    if (P.viscous && D.nfv > 0) {
-        launch_visc(D.dm, D.dstate, D.FV, Box{}, D.fvlist, D.nfv, c->gas, st);
-        c->launch_counter++;
-    }
+    issue_partial_donor_w(c, g, st, base, m, src, cs);
 }
 
 // one MRAB macro step (host bookkeeping + launches)
@@ -1071,6 +1080,168 @@ static void issue_macro_step_dag3d(mrab_ctx* c) {
     }
 }
 
+// ----------------------------------------------------------------------------------------
+// Two-rate slowest-first macro step (reading R-SF): the slow meshes' RHS at t + H is
+// evaluated first, with the fast meshes' states extrapolated over the whole macro step; the
+// fast substeps then see slow states from the old extrapolant (reextrap = false) or from the
+// one re-formed with R_s(t + H) as its newest node (reextrap = true).  Same kernels, issued
+// directly on the context stream (weights are launch arguments).
+// In the fused, deferred formulation a slow mesh holds s(t) and s(t + H) in its
+// two state buffers and R_s(t + H) uncommitted in a spare buffer; at the start of the next macro
+// step the spare is swapped into the ring and s(t + 2H) is formed by a pointwise combination.
+// ----------------------------------------------------------------------------------------
+static mrab_status issue_macro_step_sf(mrab_ctx* c, bool reextrap) {
+    const Plan& P = *c->P;
+    const int G = (int)P.meshes.size(), m = P.history_m, S = P.S, n = P.order_n;
+    const double h = P.h, H = P.h * S;
+    std::vector<int> slow, fast, all(G);
+    std::iota(all.begin(), all.end(), 0);
+    for (int g = 0; g < G; ++g) (P.meshes[g].s == S ? slow : fast).push_back(g);
+    double w_full[kMaxHist], w_long[kMaxHist], nodes[kMaxHist];
+    for (int k = 0; k < m; ++k) nodes[k] = -(double)(m - 1) + k;
+    ab_weights(nodes, m, n, 0.0, 1.0, w_full, nullptr);
+    ab_weights(nodes, m, n, 0.0, (double)S, w_long, nullptr);
+    auto ring_oldest_first = [&](int g, const double** src) {
+        for (int k = 0; k < m; ++k) src[k] = c->md[g].ring[((c->book.head[g] - (m - 1) + k) % m + m) % m];
+    };
+    // gather for the receivers of `recv` with donor states given per mesh as base + sum cs src
+    auto gather = [&](const std::vector<int>& recv, const SrcSet& ss) {
+        if (P.dim == 2) {
+            issue_donor2d(c, recv, ss);
+            return;
+        }
+        std::vector<const double*> state_of(G);
+        for (int hh = 0; hh < G; ++hh) {
+            bool need = false;
+            for (int g : recv) need = need || (hh != g && P.donor_of[hh][g] && !P.meshes[g].rpoint.empty());
+            state_of[hh] = ss.base[hh];
+            if (!need) continue;
+            MeshDev& D = c->md[hh];
+            if (ss.nsrc[hh] == 0) {
+                if (P.viscous && D.nfv > 0) {
+                    launch_visc(D.dm, ss.base[hh], D.FV, Box{}, D.fvlist, D.nfv, c->gas, c->st);
+                    c->launch_counter++;
+                }
+            } else {
+                issue_partial_donor_w(c, hh, c->st, ss.base[hh], ss.nsrc[hh], ss.src[hh], ss.c[hh]);
+                state_of[hh] = D.dstate;
+            }
+        }
+        for (int g : recv) issue_interp(c, g, state_of.data());
+    };
+    // fused evaluation + AB step of mesh g at its current state (weights w_full, step hg)
+    auto fused_step = [&](int g) {
+        MeshDev& D = c->md[g];
+        const double hg = h * P.meshes[g].s;
+        const int newslot = (c->book.head[g] + 1) % m;
+        Epilogue ep{};
+        ep.r_out = D.ring[newslot];
+        ep.y_out = D.Q[c->book.cur[g] ^ 1];
+        ep.base = D.Q[c->book.cur[g]];
+        ep.c_new = hg * w_full[m - 1];
+        ep.nsrc = m - 1;
+        for (int k = 0; k < m - 1; ++k) {
+            ep.src[k] = D.ring[((c->book.head[g] - (m - 2) + k) % m + m) % m];
+            ep.csrc[k] = hg * w_full[k];
+        }
+        std::vector<const double*> dummy(G, nullptr);
+        issue_rhs(c, g, ep.base, ep, dummy.data());
+        c->book.head[g] = newslot;
+        c->book.pending[g] = 1;
+        c->evals[g]++;
+    };
+    SrcSet plain{};
+    // ---- j = 0 ----
+    for (int g = 0; g < G; ++g)
+        if (c->book.pending[g]) {
+            c->book.cur[g] ^= 1;
+            c->book.pending[g] = 0;
+        }
+    for (int g = 0; g < G; ++g) {
+        plain.base[g] = c->md[g].Q[c->book.cur[g]];
+        plain.nsrc[g] = 0;
+    }
+    if (!c->sf_primed) {
+        gather(all, plain);
+        for (int g = 0; g < G; ++g) fused_step(g);
+    } else {
+        for (int g : slow) {
+            // commit R_s(t) (evaluated early in the previous macro step), then s(t + H)
+            MeshDev& D = c->md[g];
+            const int newslot = (c->book.head[g] + 1) % m;
+            std::swap(D.ring[newslot], D.kbuf[0]);
+            c->book.head[g] = newslot;
+            const double* src[kMaxHist];
+            double cs[kMaxHist];
+            ring_oldest_first(g, src);
+            for (int k = 0; k < m; ++k) cs[k] = H * w_full[k];
+            launch_combine(P.nc, D.dm, whole_box(P.meshes[g]), D.Q[c->book.cur[g]], m, src, cs,
+                           D.Q[c->book.cur[g] ^ 1], c->st);
+            c->launch_counter++;
+            c->book.pending[g] = 1;
+        }
+        gather(fast, plain);
+        for (int g : fast) fused_step(g);
+    }
+    // ---- the slow meshes' RHS at t + H, fast donors extrapolated over [t, t + H] ----
+    {
+        SrcSet ss{};
+        for (int g : fast) {
+            ss.base[g] = c->md[g].Q[c->book.cur[g]];      // f(t); f(t + h) is pending
+            ss.nsrc[g] = m;
+            ring_oldest_first(g, ss.src[g]);
+            for (int k = 0; k < m; ++k) ss.c[g][k] = h * w_long[k];
+        }
+        for (int g : slow) {
+            ss.base[g] = c->md[g].Q[c->book.cur[g] ^ 1];  // s(t + H)
+            ss.nsrc[g] = 0;
+        }
+        gather(slow, ss);
+        for (int g : slow) {
+            MeshDev& D = c->md[g];
+            Epilogue ep{};
+            ep.r_out = D.kbuf[0];
+            std::vector<const double*> dummy(G, nullptr);
+            issue_rhs(c, g, ss.base[g], ep, dummy.data());
+            c->evals[g]++;
+        }
+    }
+    // ---- fast substeps j = 1 .. S-1 ----
+    for (int j = 1; j < S; ++j) {
+        SrcSet ss{};
+        for (int g : fast) {
+            c->book.cur[g] ^= 1;
+            c->book.pending[g] = 0;
+            ss.base[g] = c->md[g].Q[c->book.cur[g]];
+            ss.nsrc[g] = 0;
+        }
+        for (int g : slow) {
+            MeshDev& D = c->md[g];
+            ss.base[g] = D.Q[c->book.cur[g]];             // s(t)
+            ss.nsrc[g] = m;
+            double w[kMaxHist];
+            if (reextrap) {
+                // nodes -(m-2), ..., 0, 1: the m-1 newest committed entries and R_s(t + H)
+                double nd[kMaxHist];
+                for (int k = 0; k < m; ++k) nd[k] = -(double)(m - 2) + k;
+                ab_weights(nd, m, n, 0.0, (double)j / S, w, nullptr);
+                for (int k = 0; k < m - 1; ++k)
+                    ss.src[g][k] = D.ring[((c->book.head[g] - (m - 2) + k) % m + m) % m];
+                ss.src[g][m - 1] = D.kbuf[0];
+            } else {
+                ab_weights(nodes, m, n, 0.0, (double)j / S, w, nullptr);
+                ring_oldest_first(g, ss.src[g]);
+            }
+            for (int k = 0; k < m; ++k) ss.c[g][k] = H * w[k];
+        }
+        gather(fast, ss);
+        for (int g : fast) fused_step(g);
+    }
+    c->sf_primed = true;
+    CK(cudaGetLastError());
+    return MRAB_OK;
+}
+
 // one coupled RK micro step of the bootstrap
 static void issue_rk_step(mrab_ctx* c) {
     const Plan& P = *c->P;
@@ -1597,6 +1768,8 @@ static void uniform_ring_times(mrab_ctx* c) {
 // the history node times, which change from step to step
 static mrab_status var_macro_step(mrab_ctx* c, double H) {
     const Plan& P = *c->P;
+    if (c->scheme > 0) return fail(MRAB_E_INVALID, "this context runs a slowest-first scheme (fixed step only)");
+    c->scheme = 0;
     if (!c->var_mode) {
         uniform_ring_times(c);
         c->var_mode = true;
@@ -1629,6 +1802,8 @@ mrab_status mrab_step(mrab_ctx* c, int n_macro) {
             for (int s = 0; s < P.S; ++s) issue_rk_step(c);
             CK(cudaGetLastError());
         } else {
+            if (c->scheme > 0) return fail(MRAB_E_INVALID, "this context runs a slowest-first scheme: use mrab_step_scheme");
+            c->scheme = 0;
             const int64_t k = c->macro - nboot_macro;
             mrab_status st = ensure_graphs(c);
             if (st != MRAB_OK) return st;
@@ -1661,6 +1836,42 @@ mrab_status mrab_step_h(mrab_ctx* c, int n_macro, double H) {
     for (int it = 0; it < n_macro; ++it) {
         mrab_status st = var_macro_step(c, H);
         if (st != MRAB_OK) return st;
+    }
+    CK(cudaEventRecord(c->ev_out, c->st));
+    CK(cudaStreamWaitEvent(c->user, c->ev_out, 0));
+    return MRAB_OK;
+}
+
+mrab_status mrab_step_scheme(mrab_ctx* c, int n_macro, int scheme) {
+    if (!c || n_macro < 0 || scheme < 0 || scheme > 2) return fail(MRAB_E_INVALID, "bad ctx / n_macro / scheme");
+    if (scheme == MRAB_SCHEME_FASTEST_FIRST) return mrab_step(c, n_macro);
+    const Plan& P = *c->P;
+    bool two_rate = P.S > 1;
+    int nfast = 0, nslow = 0;
+    for (auto& mp : P.meshes) {
+        two_rate = two_rate && (mp.s == 1 || mp.s == P.S);
+        (mp.s == 1 ? nfast : nslow)++;
+    }
+    if (!two_rate || !nfast || !nslow)
+        return fail(MRAB_E_INVALID, "slowest-first schemes need exactly two rates (step multiples 1 and S > 1)");
+    if (P.opt.z3_fused) return fail(MRAB_E_INVALID, "slowest-first schemes run on the default (two-pass) 3-D kernels");
+    set_options(P.opt);
+    CK(cudaEventRecord(c->ev_in, c->user));
+    CK(cudaStreamWaitEvent(c->st, c->ev_in, 0));
+    const int64_t nboot_macro = P.history_m - 1;
+    for (int it = 0; it < n_macro; ++it) {
+        if (c->macro < nboot_macro) {
+            for (int s = 0; s < P.S; ++s) issue_rk_step(c);
+            CK(cudaGetLastError());
+        } else {
+            if (c->scheme >= 0 && c->scheme != scheme)
+                return fail(MRAB_E_INVALID, "the MRAB scheme of a context is fixed by its first MRAB step");
+            c->scheme = scheme;
+            mrab_status st = issue_macro_step_sf(c, scheme == MRAB_SCHEME_SLOWEST_FIRST_REEXTRAP);
+            if (st != MRAB_OK) return st;
+        }
+        c->macro++;
+        c->macro_fixed++;
     }
     CK(cudaEventRecord(c->ev_out, c->st));
     CK(cudaStreamWaitEvent(c->user, c->ev_out, 0));
