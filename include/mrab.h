@@ -203,6 +203,13 @@ mrab_status mrab_step_h(mrab_ctx* ctx, int n_macro, double H);
 enum { MRAB_SCHEME_FASTEST_FIRST = 0, MRAB_SCHEME_SLOWEST_FIRST = 1, MRAB_SCHEME_SLOWEST_FIRST_REEXTRAP = 2 };
 mrab_status mrab_step_scheme(mrab_ctx* ctx, int n_macro, int scheme);
 
+/* Reference Runge-Kutta integrator (r_RK4 = dt / dt_RK4 normalises the stability
+ * tables): n_steps coupled single-rate steps of size h of every mesh with the classical RK4
+ * (order 4) or Heun's RK3 (order 3, reading R5), the same stage kernels as the bootstrap.  The
+ * AB histories are not touched, so a context driven this way is an RK integrator (do not mix
+ * with MRAB steps).  Asynchronous on the caller's stream.  Errors: INVALID, CUDA. */
+mrab_status mrab_rk_step(mrab_ctx* ctx, int n_steps, int order, double h);
+
 /* Stable-timestep estimate on the device (eq:ts_inv, eq:ts_visc, eq:ts_overall, P:620-643;
  * reading R20 of DESIGN.md for the garbled parentheses): dt_mesh[g] (host, [n_meshes]) =
  * min over the active points of mesh g, at its current state, of

@@ -1243,10 +1243,13 @@ static mrab_status issue_macro_step_sf(mrab_ctx* c, bool reextrap) {
 }
 
 // one coupled RK micro step of the bootstrap
-static void issue_rk_step(mrab_ctx* c) {
+// record: bootstrap mode (stage-1 RHS of mesh-aligned steps go to the rings, R6); otherwise a
+// plain RK step of size hstep (mrab_rk_step: the RK4 reference integrator of P:861-878)
+static void issue_rk_step(mrab_ctx* c, bool record = true, int order = 0, double hstep = 0.0) {
     const Plan& P = *c->P;
     const int G = (int)P.meshes.size(), m = P.history_m;
-    const bool rk4 = P.order_n >= 4;
+    const bool rk4 = (order ? order : P.order_n) >= 4;
+    const double hh = record ? P.h : hstep;
     const int ns = rk4 ? 4 : 3;
     // Heun RK3 (R5) / classical RK4: a[s][j], b[j]
     double a[4][4] = {{0}}, b[4] = {0};
@@ -1274,7 +1277,7 @@ static void issue_rk_step(mrab_ctx* c) {
             c->book.pending[g] = 0;
         }
         const int s = P.meshes[g].s;
-        bool rec = (left % s == 0) && (left / s <= m - 1);
+        bool rec = record && (left % s == 0) && (left / s <= m - 1);
         for (int q = 0; q < ns; ++q) kp[g * 4 + q] = c->md[g].kbuf[q];
         if (rec) {
             int newslot = (c->book.head[g] + 1) % m;
@@ -1298,21 +1301,21 @@ static void issue_rk_step(mrab_ctx* c) {
             ep.base = D.Q[c->book.cur[g]];
             if (s < ns - 1) {
                 ep.y_out = D.dstate;
-                ep.c_new = P.h * a[s + 1][s];
+                ep.c_new = hh * a[s + 1][s];
                 ep.nsrc = 0;
                 for (int jx = 0; jx < s; ++jx)
                     if (a[s + 1][jx] != 0.0) {
                         ep.src[ep.nsrc] = kp[g * 4 + jx];
-                        ep.csrc[ep.nsrc++] = P.h * a[s + 1][jx];
+                        ep.csrc[ep.nsrc++] = hh * a[s + 1][jx];
                     }
             } else {
                 ep.y_out = D.Q[c->book.cur[g] ^ 1];
-                ep.c_new = P.h * b[s];
+                ep.c_new = hh * b[s];
                 ep.nsrc = 0;
                 for (int jx = 0; jx < s; ++jx)
                     if (b[jx] != 0.0) {
                         ep.src[ep.nsrc] = kp[g * 4 + jx];
-                        ep.csrc[ep.nsrc++] = P.h * b[jx];
+                        ep.csrc[ep.nsrc++] = hh * b[jx];
                     }
             }
             issue_rhs(c, g, state_of[g], ep, state_of.data());
@@ -1322,7 +1325,7 @@ static void issue_rk_step(mrab_ctx* c) {
             for (int g = 0; g < G; ++g) std::swap(c->md[g].dstate, c->md[g].ystage);
     }
     for (int g = 0; g < G; ++g) c->book.pending[g] = 1;
-    c->boot_micro++;
+    if (record) c->boot_micro++;
 }
 
 // ----------------------------------------------------------------------------------------
@@ -1873,6 +1876,20 @@ mrab_status mrab_step_scheme(mrab_ctx* c, int n_macro, int scheme) {
         c->macro++;
         c->macro_fixed++;
     }
+    CK(cudaEventRecord(c->ev_out, c->st));
+    CK(cudaStreamWaitEvent(c->user, c->ev_out, 0));
+    return MRAB_OK;
+}
+
+mrab_status mrab_rk_step(mrab_ctx* c, int n_steps, int order, double h) {
+    if (!c || n_steps < 0 || (order != 3 && order != 4) || !(h > 0.0))
+        return fail(MRAB_E_INVALID, "bad ctx / n_steps / order (3 or 4) / h");
+    set_options(c->P->opt);
+    CK(cudaEventRecord(c->ev_in, c->user));
+    CK(cudaStreamWaitEvent(c->st, c->ev_in, 0));
+    for (int it = 0; it < n_steps; ++it) issue_rk_step(c, false, order, h);
+    CK(cudaGetLastError());
+    c->time_extra += n_steps * h;
     CK(cudaEventRecord(c->ev_out, c->st));
     CK(cudaStreamWaitEvent(c->user, c->ev_out, 0));
     return MRAB_OK;

@@ -84,6 +84,7 @@ def lib():
         L.mrab_step.argtypes = [vp, C.c_int]
         L.mrab_step_h.argtypes = [vp, C.c_int, C.c_double]
         L.mrab_step_scheme.argtypes = [vp, C.c_int, C.c_int]
+        L.mrab_rk_step.argtypes = [vp, C.c_int, C.c_int, C.c_double]
         L.mrab_dt.argtypes = [vp, dp]
         L.mrab_get_state.argtypes = [vp, C.c_int, vp, dp]
         L.mrab_set_state.argtypes = [vp, C.c_int, vp]
@@ -99,7 +100,7 @@ def lib():
                      "mrab_plan_get_tables", "mrab_plan_get_metrics", "mrab_create",
                      "mrab_step", "mrab_get_state", "mrab_set_state", "mrab_rhs",
                      "mrab_get_history", "mrab_set_history", "mrab_get_counters",
-                     "mrab_launches_per_macro_step", "mrab_time_kernel", "mrab_step_h", "mrab_dt", "mrab_step_scheme"):
+                     "mrab_launches_per_macro_step", "mrab_time_kernel", "mrab_step_h", "mrab_dt", "mrab_step_scheme", "mrab_rk_step"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -110,7 +111,7 @@ EXPORTED = ["mrab_ab_weights", "mrab_plan_create", "mrab_plan_destroy", "mrab_pl
             "mrab_create", "mrab_destroy", "mrab_step", "mrab_get_state", "mrab_set_state",
             "mrab_rhs", "mrab_get_counters", "mrab_launches_per_macro_step", "mrab_time_kernel",
             "mrab_set_trace", "mrab_last_error", "mrab_get_history", "mrab_set_history",
-            "mrab_overset_build", "mrab_free", "mrab_plan_get_face_flags", "mrab_step_h", "mrab_dt", "mrab_step_scheme"]
+            "mrab_overset_build", "mrab_free", "mrab_plan_get_face_flags", "mrab_step_h", "mrab_dt", "mrab_step_scheme", "mrab_rk_step"]
 
 
 def _check(st):
@@ -317,6 +318,10 @@ class Context:
             _check(lib().mrab_step(self.h, int(n_macro)))
         else:
             _check(lib().mrab_step_scheme(self.h, int(n_macro), self.SCHEMES[scheme]))
+
+    def rk_step(self, h, n_steps=1, order=4):
+        """n_steps coupled single-rate RK steps of size h (mrab_rk_step)."""
+        _check(lib().mrab_rk_step(self.h, int(n_steps), int(order), float(h)))
 
     def step_h(self, H, n_macro=1):
         """n_macro MRAB macro steps of size H (variable macro step, mrab_step_h)."""

@@ -110,10 +110,15 @@ def test_fullsize_3d_against_oracle_golden(cid):
         ji = gd[f"m{g}_jinv"]
         assert np.max(np.abs(jinv[idx] - ji)) <= 1e-13 * np.max(np.abs(ji))
         Mg = gd[f"m{g}_M"]
+        # M_ki = D_c(x_k D_b x_j) - D_b(x_k D_c x_j) (reading R3): sums of products of two
+        # coordinates times stencil coefficients that cancel down to O(h^2).  Where the summation
+        # order differs (closure rows; everywhere else the values agree bit for bit) the rounding
+        # difference is a few eps of that cancellation scale max|x|^2, not of |M|
+        x2 = float(np.max(np.abs(p.meshes[g].xyz))) ** 2
         for k in range(3):
             sc = max(float(np.max(np.abs(Mg[k, k]))), 1e-300)
             for i in range(3):
-                assert np.max(np.abs(M[k, i][idx] - Mg[k, i])) <= 1e-13 * sc
+                assert np.max(np.abs(M[k, i][idx] - Mg[k, i])) <= 1e-13 * sc + 32 * 2.3e-16 * x2
     ctx = mrab.Context(plan, p.q0)
     Rg = ctx.rhs(p.q0)
     nc = p.nc
