@@ -57,6 +57,104 @@ class StepMap:
         return self.read()
 
 
+class RKMap:
+    """phi -> phi' = one step of size h of the reference Runge-Kutta integrator (classical RK4
+    by default; P:861-878 normalises the stability tables by its maximum stable step) on the
+    GPU (mrab_rk_step).  The integrator vector is the states only."""
+
+    def __init__(self, ctx: "mrab.Context", h, order=4):
+        self.ctx, self.h, self.order = ctx, float(h), int(order)
+        P = ctx.plan
+        self.shapes = [(P.nc,) + tuple(reversed(P.shapes[g])) for g in range(P.n_meshes)]
+        self.sizes = [int(np.prod(s)) for s in self.shapes]
+        self.dim = sum(self.sizes)
+
+    def read(self):
+        return np.concatenate([self.ctx.get_state(g)[0].ravel() for g in range(len(self.shapes))])
+
+    def write(self, phi):
+        o = 0
+        for g, (shp, n) in enumerate(zip(self.shapes, self.sizes)):
+            self.ctx.set_state(g, np.ascontiguousarray(phi[o:o + n].reshape(shp)))
+            o += n
+
+    def __call__(self, phi):
+        self.write(phi)
+        self.ctx.rk_step(self.h, 1, self.order)
+        return self.read()
+
+
+def spectral_radius_arnoldi(smap, phi0, k=80, restarts=6, eps=EPS, seed=0, res_tol=1e-6):
+    """Largest modulus among the CONVERGED eigenvalues of G_eps, by explicitly restarted Arnoldi
+    on the matrix-free operator v -> (step(phi0 + eps v/|v|) - step(phi0)) |v| / eps: k steps
+    build an orthonormal Krylov basis (Gram-Schmidt twice); a Ritz pair (theta, V y) counts as
+    converged when its residual |h_{k+1,k}| |y_k| <= res_tol |theta| (Ritz values of a
+    non-normal step matrix that have not converged can lie outside its spectrum, so they are
+    not used); the iteration restarts from the sum of the leading Ritz vectors until the leading
+    pair has converged.  A plain stand-in for the Krylov-Schur solver the paper uses.
+    Non-finite steps (blow-up) return inf; no converged pair returns 0.  Returns (rho, matvecs)."""
+    base = smap(phi0)
+    if not np.all(np.isfinite(base)):
+        return float("inf"), 1
+    n = phi0.size
+    v = np.random.default_rng(seed).standard_normal(n)
+    nmv, best = 1, 0.0
+    for _ in range(restarts):
+        V = np.zeros((k + 1, n))
+        Hm = np.zeros((k + 1, k))
+        V[0] = v / np.linalg.norm(v)
+        kk = k
+        for j in range(k):
+            w = (smap(phi0 + eps * V[j]) - base) / eps
+            nmv += 1
+            if not np.all(np.isfinite(w)):
+                return float("inf"), nmv
+            for _pass in range(2):
+                c = V[:j + 1] @ w
+                w = w - c @ V[:j + 1]
+                Hm[:j + 1, j] += c
+            Hm[j + 1, j] = np.linalg.norm(w)
+            if Hm[j + 1, j] < 1e-14:
+                kk = j + 1
+                break
+            V[j + 1] = w / Hm[j + 1, j]
+        ev, Y = np.linalg.eig(Hm[:kk, :kk])
+        res = np.abs(Hm[kk, kk - 1]) * np.abs(Y[kk - 1, :]) if kk == k else np.zeros(kk)
+        order = np.argsort(-np.abs(ev))
+        conv = [i for i in order if res[i] <= res_tol * max(abs(ev[i]), 1e-300)]
+        if conv:
+            best = max(best, float(abs(ev[conv[0]])))
+        if res[order[0]] <= res_tol * abs(ev[order[0]]):
+            break                                     # the leading pair itself has converged
+        lead = order[:min(4, kk)]
+        v = np.real(Y[:, lead].sum(axis=1)) @ V[:kk]
+        if np.linalg.norm(v) < 1e-12:
+            v = np.imag(Y[:, lead].sum(axis=1)) @ V[:kk]
+    return best, nmv
+
+
+def growth_rate(smap, phi0, iters=300, eps=EPS, seed=0):
+    """Asymptotic growth factor per step of a perturbation under the linearised map:
+    exp(mean log-norm slope over the second half of `iters` renormalised power iterations).
+    It approaches rho(G_eps) from the dominant mode and, unlike unconverged Ritz values, does
+    not overshoot once the transient has decayed.  Blow-up returns inf."""
+    base = smap(phi0)
+    if not np.all(np.isfinite(base)):
+        return float("inf")
+    v = np.random.default_rng(seed).standard_normal(phi0.size)
+    v /= np.linalg.norm(v)
+    logs = []
+    for _ in range(iters):
+        w = (smap(phi0 + eps * v) - base) / eps
+        nw = float(np.linalg.norm(w))
+        if not np.isfinite(nw) or nw == 0.0:
+            return float("inf") if not np.isfinite(nw) else 0.0
+        logs.append(np.log(nw))
+        v = w / nw
+    half = iters // 2
+    return float(np.exp(np.mean(logs[half:])))
+
+
 def step_matrix(smap: StepMap, phi0, eps=EPS, cols=None):
     """G_eps (eq:sm_form), all columns or the listed ones."""
     base = smap(phi0)

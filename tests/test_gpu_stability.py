@@ -88,3 +88,45 @@ def test_history_accessor_errors(setup):
     buf = np.zeros(16)
     assert mrab.lib().mrab_get_history(ctx.h, 2, 0, buf.ctypes.data) == 1    # MRAB_E_INVALID
     assert mrab.lib().mrab_get_history(ctx.h, 0, 0, None) == 1
+
+
+def test_rk_step_matches_oracle_rk4_and_heun():
+    """mrab_rk_step (the reference integrator of the stability tables) against the
+    oracle's rk_step on the coupled SBP-SAT RHS: 3 steps of RK4 and of Heun's RK3."""
+    import synth
+    from oracle import rhs as orhs, timeint
+    p = synth.make_config(1, "test")
+    st = orhs.build(p)
+    rhs_fn = lambda s, which=None: orhs.rhs(p, st, s, which)  # noqa: E731
+    for order in (4, 3):
+        ctx = mrab.Context(mrab.Plan(p), p.q0)
+        h = 2.5 * p.h
+        ctx.rk_step(h, 3, order)
+        y = [q.copy() for q in p.q0]
+        for _ in range(3):
+            y = timeint.rk_step(rhs_fn, y, h, timeint.rk_tableau(order))
+        for g in range(len(p.meshes)):
+            q = ctx.get_state(g)[0]
+            assert np.max(np.abs(q - y[g])) <= 1e-12 * np.max(np.abs(y[g]))
+        ctx.close()
+
+
+def test_arnoldi_matches_dense_rho():
+    """Restarted Arnoldi on the matrix-free step map against the dense eigensolve of every
+    eq:sm_form column (13 x 13 App. C box-in-box, rates 2:1, AB3)."""
+    from paper_1805_06607_b200 import stability as gs
+    p = synth.configs.vortex_box_in_box(9)
+    p.order_n, p.history_m, p.h = 3, 3, 0.004
+    ctx = mrab.Context(mrab.Plan(p, steps=[2, 1]), p.q0)
+    ctx.step(p.history_m - 1)
+    sm = gs.StepMap(ctx)
+    phi = sm.read()
+    dense = gs.spectral_radius(gs.step_matrix(sm, phi))
+    arn, nmv = gs.spectral_radius_arnoldi(sm, phi, k=80, restarts=8)
+    # only converged Ritz values count, so the estimate never exceeds the spectrum; it equals
+    # rho when the leading eigenvalue has converged
+    gr = gs.growth_rate(sm, phi, iters=300)
+    print("dense", dense, "arnoldi", arn, nmv, "power", gr)
+    assert arn <= dense * (1 + 1e-5), (arn, dense, nmv)
+    assert dense - 5e-3 <= gr <= dense * (1 + 2e-4), (gr, dense)
+    ctx.close()

@@ -66,3 +66,24 @@ def test_krylov_and_power_match_dense_on_fake_linear_map():
     phi = sm.read()
     assert abs(stability.spectral_radius_krylov(sm, phi, eps=1e-3, tol=1e-10) - 2.0) < 1e-6
     assert abs(stability.power_estimate(sm, phi, iters=40, eps=1e-3) - 2.0) < 1e-6
+
+
+def test_arnoldi_uses_converged_ritz_values_only():
+    """Explicitly restarted Arnoldi on a fake non-normal linear step map: an isolated unstable
+    eigenvalue is found to 1e-6; with a stable spectrum clustered below 1 the estimate stays
+    below 1 (unconverged Ritz values, which can leave the spectrum of a non-normal matrix, are
+    not used)."""
+    from paper_1805_06607_b200 import stability as gs
+    rng = np.random.default_rng(1)
+    n = 400
+    lam = np.concatenate([1 - 0.2 * rng.random(n - 1) ** 3, [-1.004]])
+    X = np.eye(n) + 0.3 * rng.standard_normal((n, n)) / np.sqrt(n)
+    Xi = np.linalg.inv(X)
+    phi0 = rng.standard_normal(n)
+    A = X @ np.diag(lam) @ Xi
+    rho, _ = gs.spectral_radius_arnoldi(lambda p: A @ p, phi0, k=60)
+    assert abs(rho - 1.004) <= 1e-6
+    lam[-1] = -0.99
+    A2 = X @ np.diag(lam) @ Xi
+    rho, _ = gs.spectral_radius_arnoldi(lambda p: A2 @ p, phi0, k=60)
+    assert rho <= 1.0
