@@ -203,6 +203,32 @@ mrab_status mrab_step_h(mrab_ctx* ctx, int n_macro, double H);
 enum { MRAB_SCHEME_FASTEST_FIRST = 0, MRAB_SCHEME_SLOWEST_FIRST = 1, MRAB_SCHEME_SLOWEST_FIRST_REEXTRAP = 2 };
 mrab_status mrab_step_scheme(mrab_ctx* ctx, int n_macro, int scheme);
 
+/* Multi-GPU: the meshes of a problem are
+ * partitioned over the ranks (one process per GPU) and each rank steps the meshes it owns; per
+ * RHS evaluation the only exchange is the interpolated donor data, formed on the rank that owns
+ * the donor mesh and sent to the rank that owns the receivers (qhat [nc][R], fvhat
+ * [d(d+1)][R]), one grouped NCCL send/recv exchange per evaluation round over NVLink.
+ *   mrab_partition   owner[g] (host [n_meshes]) by longest-processing-time-first on the weight
+ *                    active points x RHS evaluations per macro step (the paper's load-balance
+ *                    lesson: rank counts follow work, not points); load (host [nranks], may be
+ *                    NULL) receives the per-rank weights.  Deterministic, host only.
+ *   mrab_dist_unique_id   128-byte NCCL id (rank 0; broadcast it to the other ranks).
+ *   mrab_dist_attach transport MRAB_TRANSPORT_NCCL (id = the 128-byte unique id) or
+ *                    MRAB_TRANSPORT_LOOPBACK (id = int* world id: contexts of one process on
+ *                    one device play the ranks from separate host threads; test transport).
+ *                    Every rank creates the context of the whole problem (same plan, same q0)
+ *                    and attaches before its first step; mrab_step / mrab_step_h / mrab_rhs then
+ *                    advance (return) the owned meshes only, and mrab_get_state is meaningful
+ *                    for owned meshes.  Steps are launched directly (no CUDA graph).
+ *   mrab_dist_stats  bytes and messages this rank has sent.
+ * Errors: INVALID, CUDA (NCCL missing or failing). */
+enum { MRAB_TRANSPORT_NCCL = 0, MRAB_TRANSPORT_LOOPBACK = 1 };
+mrab_status mrab_partition(const mrab_plan* plan, int nranks, int* owner, double* load);
+mrab_status mrab_dist_unique_id(void* out128);
+mrab_status mrab_dist_attach(mrab_ctx* ctx, int transport, const void* id, int rank, int nranks,
+                             const int* owner);
+mrab_status mrab_dist_stats(mrab_ctx* ctx, int64_t* bytes_sent, int64_t* messages);
+
 /* Reference Runge-Kutta integrator (r_RK4 = dt / dt_RK4 normalises the stability
  * tables): n_steps coupled single-rate steps of size h of every mesh with the classical RK4
  * (order 4) or Heun's RK3 (order 3, reading R5), the same stage kernels as the bootstrap.  The

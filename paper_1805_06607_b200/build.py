@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libmrab.so")
-SOURCES = ["mrab_api.cu", "kernels.cu", "kernels2d.cu", "host_setup.cpp"]
+SOURCES = ["mrab_api.cu", "kernels.cu", "kernels2d.cu", "host_setup.cpp", "dist.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = [*(["-DMRAB_Z3_PROF"] if os.environ.get("MRAB_Z3_PROF") else []), "-O3", "-std=c++17", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
@@ -59,7 +59,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         for _, e in res:
             sys.stderr.write(e)
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", LIB,
-           "-Xcompiler", "-fopenmp", "-cudart", "static"]
+           "-Xcompiler", "-fopenmp", "-cudart", "static", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")

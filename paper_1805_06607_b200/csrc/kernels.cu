@@ -2137,6 +2137,21 @@ void launch_dt(int dim, const DevMesh& m, const double* Q, const Gas& gas, doubl
     else k_dt<3><<<grid, 256, 0, st>>>(m, Q, gas, (unsigned long long*)out);
 }
 
+// multi-GPU: dst[row][r] = src[row][r] for the receivers r whose donor mesh is owned by src_rank
+// (the rows another rank gathered from the donor meshes it owns)
+__global__ void __launch_bounds__(256) k_merge_recv(int rows, int64_t R, const int32_t* __restrict__ rdonor,
+                                                    OwnerTable ot, int src_rank, const double* __restrict__ src,
+                                                    double* __restrict__ dst) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= R || ot.owner[rdonor[r]] != src_rank) return;
+    for (int row = 0; row < rows; ++row) dst[row * R + r] = src[row * R + r];
+}
+void launch_merge_recv(int rows, int64_t R, const int32_t* rdonor, const OwnerTable& ot, int src_rank,
+                       const double* src, double* dst, cudaStream_t st) {
+    if (R <= 0) return;
+    k_merge_recv<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(rows, R, rdonor, ot, src_rank, src, dst);
+}
+
 void launch_l2_scrub(void* a, void* b, size_t bytes, int tag, cudaStream_t st) {
     cudaMemsetAsync(a, tag & 0xff, bytes, st);
     k_scrub_read<<<148 * 8, 256, 0, st>>>((const double4*)b, bytes / sizeof(double4), (double*)a);

@@ -202,6 +202,12 @@ void upload_stencil_rows();
 void launch_l2_scrub(void* a, void* b, size_t bytes, int tag, cudaStream_t st);
 // sets *flag (device int) if any of the n doubles is not finite
 void launch_finite(const double* a, size_t n, int* flag, cudaStream_t st);
+// multi-GPU (mesh-partitioned): which rank owns each mesh; merge of received donor data
+struct OwnerTable {
+    int owner[8];
+};
+void launch_merge_recv(int rows, int64_t R, const int32_t* rdonor, const OwnerTable& ot, int src_rank,
+                       const double* src, double* dst, cudaStream_t st);
 // K9: *out (device double) = min over the active points of mesh m of the eq:ts timestep
 void launch_dt(int dim, const DevMesh& m, const double* Q, const Gas& gas, double* out, cudaStream_t st);
 // launch priority of the 3-D launches that follow on this thread (has = 0: plain launches)

@@ -20,6 +20,7 @@
 #include <string>
 #include <vector>
 
+#include "dist.h"
 #include "kernels.cuh"
 #include "mrab_internal.h"
 
@@ -120,6 +121,17 @@ struct mrab_ctx {
     int64_t graph_k0 = 0;         // MRAB macro-step index the phase-0 graph was captured at
     // variable macro step (mrab_step_h): micro step of the macro step being issued
     // and the times of the ring entries relative to its start (valid once var_mode is set)
+    // multi-GPU: meshes partitioned over ranks, donor data exchanged per RHS evaluation
+    struct DistState {
+        int rank = 0, nranks = 1;
+        OwnerTable ot{};
+        std::unique_ptr<Transport> tp;
+        double* tmp = nullptr;    // receive staging (library-owned)
+        size_t tmp_bytes = 0;
+        std::string err;
+        int64_t bytes_sent = 0, messages = 0;
+    };
+    std::unique_ptr<DistState> dist;
     int scheme = -1;              // MRAB scheme of this context, fixed by its first MRAB step
     bool sf_primed = false;       // slowest-first: R_s(t) sits uncommitted in the spare buffer
     bool var_mode = false;
@@ -1242,6 +1254,184 @@ static mrab_status issue_macro_step_sf(mrab_ctx* c, bool reextrap) {
     return MRAB_OK;
 }
 
+// ----------------------------------------------------------------------------------------
+// Multi-GPU: the meshes are partitioned over the ranks (weight = active points x RHS
+// evaluations per macro step, the paper's load-balance lesson); each
+// rank steps the meshes it owns.  Per RHS evaluation the only exchange is the interpolated donor
+// data: the rank owning a donor mesh forms that mesh's donor state and viscous
+// fluxes, interpolates them at the receivers of the evaluating mesh and sends the result
+// (qhat [nc][R], fvhat [d(d+1)][R]) to the rank owning the receivers, which keeps the rows whose
+// donor mesh the sender owns.  One grouped exchange per evaluation round.
+// ----------------------------------------------------------------------------------------
+static bool owns(const mrab_ctx* c, int g) { return !c->dist || c->dist->ot.owner[g] == c->dist->rank; }
+
+static void dist_gather(mrab_ctx* c, const std::vector<int>& recv, const SrcSet& ss) {
+    const Plan& P = *c->P;
+    const int G = (int)P.meshes.size(), d = P.dim, nc = P.nc;
+    mrab_ctx::DistState& D = *c->dist;
+    const int me = D.rank;
+    auto rank_donates = [&](int q, int g) {
+        for (int h = 0; h < G; ++h)
+            if (h != g && P.donor_of[h][g] && D.ot.owner[h] == q) return true;
+        return false;
+    };
+    std::vector<int> mine;
+    for (int g : recv)
+        if (!P.meshes[g].rpoint.empty() && rank_donates(me, g)) mine.push_back(g);
+    if (!mine.empty()) {
+        if (d == 2) {
+            issue_donor2d(c, mine, ss);
+        } else {
+            std::vector<const double*> state_of(G);
+            for (int h = 0; h < G; ++h) {
+                state_of[h] = ss.base[h];
+                bool need = D.ot.owner[h] == me;
+                if (need) {
+                    need = false;
+                    for (int g : mine) need = need || (h != g && P.donor_of[h][g]);
+                }
+                if (!need) continue;
+                MeshDev& M = c->md[h];
+                if (ss.nsrc[h] == 0) {
+                    if (P.viscous && M.nfv > 0) {
+                        launch_visc(M.dm, ss.base[h], M.FV, Box{}, M.fvlist, M.nfv, c->gas, c->st);
+                        c->launch_counter++;
+                    }
+                } else {
+                    issue_partial_donor_w(c, h, c->st, ss.base[h], ss.nsrc[h], ss.src[h], ss.c[h]);
+                    state_of[h] = M.dstate;
+                }
+            }
+            for (int g : mine) issue_interp(c, g, state_of.data());
+        }
+    }
+    if (D.nranks == 1) return;
+    const int rows_f = d * (d + 1);
+    // receive staging: one slot per (mesh I own in recv, donating rank)
+    struct Slot {
+        int g, q;
+        size_t off;
+    };
+    std::vector<Slot> slots;
+    size_t need_bytes = 0;
+    for (int g : recv) {
+        const size_t R = P.meshes[g].rpoint.size();
+        if (!R || D.ot.owner[g] != me) continue;
+        for (int q = 0; q < D.nranks; ++q)
+            if (q != me && rank_donates(q, g)) {
+                slots.push_back({g, q, need_bytes});
+                need_bytes += R * (nc + (P.viscous ? rows_f : 0)) * sizeof(double);
+            }
+    }
+    if (need_bytes > D.tmp_bytes) {
+        cudaStreamSynchronize(c->st);
+        if (D.tmp) cudaFree(D.tmp);
+        D.tmp = nullptr;
+        if (cudaMalloc((void**)&D.tmp, need_bytes) != cudaSuccess) {
+            D.err = "receive staging allocation failed";
+            return;
+        }
+        D.tmp_bytes = need_bytes;
+    }
+    bool ok = D.tp->begin();
+    for (int g : recv) {
+        const size_t R = P.meshes[g].rpoint.size();
+        if (!R) continue;
+        const int og = D.ot.owner[g];
+        MeshDev& M = c->md[g];
+        for (int q = 0; q < D.nranks && ok; ++q) {
+            if (q == og || !rank_donates(q, g)) continue;
+            if (me == q) {
+                ok = ok && D.tp->send(M.qhat, R * nc * sizeof(double), og, 2 * g, c->st);
+                if (P.viscous) ok = ok && D.tp->send(M.fvhat, R * rows_f * sizeof(double), og, 2 * g + 1, c->st);
+                D.bytes_sent += (int64_t)(R * (nc + (P.viscous ? rows_f : 0)) * sizeof(double));
+                D.messages += P.viscous ? 2 : 1;
+            } else if (me == og) {
+                for (const Slot& s : slots)
+                    if (s.g == g && s.q == q) {
+                        char* b = reinterpret_cast<char*>(D.tmp) + s.off;
+                        ok = ok && D.tp->recv(b, R * nc * sizeof(double), q, 2 * g, c->st);
+                        if (P.viscous)
+                            ok = ok && D.tp->recv(b + R * nc * sizeof(double), R * rows_f * sizeof(double), q,
+                                                  2 * g + 1, c->st);
+                    }
+            }
+        }
+    }
+    ok = D.tp->end(c->st) && ok;
+    if (!ok) {
+        D.err = D.tp->err.empty() ? "exchange failed" : D.tp->err;
+        return;
+    }
+    for (const Slot& s : slots) {
+        const size_t R = P.meshes[s.g].rpoint.size();
+        MeshDev& M = c->md[s.g];
+        const double* b = reinterpret_cast<const double*>(reinterpret_cast<char*>(D.tmp) + s.off);
+        launch_merge_recv(nc, (int64_t)R, M.rdonor, D.ot, s.q, b, M.qhat, c->st);
+        if (P.viscous) launch_merge_recv(rows_f, (int64_t)R, M.rdonor, D.ot, s.q, b + R * nc, M.fvhat, c->st);
+    }
+}
+
+// fastest-first MRAB macro step of a rank (serial launches, weights as launch arguments)
+static void issue_macro_step_dist(mrab_ctx* c) {
+    const Plan& P = *c->P;
+    const int G = (int)P.meshes.size(), m = P.history_m;
+    for (int j = 0; j < P.S; ++j) {
+        std::vector<int> stepping;
+        SrcSet ss{};
+        for (int g = 0; g < G; ++g) {
+            MeshDev& D = c->md[g];
+            const MeshPlan& mp = P.meshes[g];
+            if (j % mp.s == 0) {
+                stepping.push_back(g);
+                if (c->book.pending[g]) {
+                    c->book.cur[g] ^= 1;
+                    c->book.pending[g] = 0;
+                }
+                ss.base[g] = D.Q[c->book.cur[g]];
+                ss.nsrc[g] = 0;
+            } else {
+                double w[kMaxHist];
+                weights_partial(c, g, j, w);
+                const double hg = h_micro(c) * mp.s;
+                ss.base[g] = D.Q[c->book.cur[g]];
+                ss.nsrc[g] = m;
+                for (int k = 0; k < m; ++k) {
+                    ss.src[g][k] = D.ring[((c->book.head[g] - (m - 1) + k) % m + m) % m];
+                    ss.c[g][k] = hg * w[k];
+                }
+            }
+        }
+        dist_gather(c, stepping, ss);
+        for (int g : stepping) {
+            MeshDev& D = c->md[g];
+            const MeshPlan& mp = P.meshes[g];
+            const double hg = h_micro(c) * mp.s;
+            const int newslot = (c->book.head[g] + 1) % m;
+            if (owns(c, g)) {
+                Epilogue ep{};
+                ep.r_out = D.ring[newslot];
+                ep.y_out = D.Q[c->book.cur[g] ^ 1];
+                ep.base = D.Q[c->book.cur[g]];
+                double al[kMaxHist];
+                weights_full(c, g, j, al);
+                ep.c_new = hg * al[m - 1];
+                ep.nsrc = m - 1;
+                for (int k = 0; k < m - 1; ++k) {
+                    ep.src[k] = D.ring[((c->book.head[g] - (m - 2) + k) % m + m) % m];
+                    ep.csrc[k] = hg * al[k];
+                }
+                std::vector<const double*> dummy(G, nullptr);
+                issue_rhs(c, g, ep.base, ep, dummy.data());
+                c->evals[g]++;
+            }
+            c->book.head[g] = newslot;
+            note_push(c, g, j, newslot);
+            c->book.pending[g] = 1;
+        }
+    }
+}
+
 // one coupled RK micro step of the bootstrap
 // record: bootstrap mode (stage-1 RHS of mesh-aligned steps go to the rings, R6); otherwise a
 // plain RK step of size hstep (mrab_rk_step: the RK4 reference integrator of P:861-878)
@@ -1291,7 +1481,13 @@ static void issue_rk_step(mrab_ctx* c, bool record = true, int order = 0, double
             MeshDev& D = c->md[g];
             state_of[g] = (s == 0) ? D.Q[c->book.cur[g]] : D.ystage;
         }
-        issue_all_donors(c, state_of.data());
+        if (c->dist) {
+            std::vector<int> allm(G);
+            std::iota(allm.begin(), allm.end(), 0);
+            dist_gather(c, allm, plain_states(c, state_of.data()));
+        } else {
+            issue_all_donors(c, state_of.data());
+        }
         // every mesh reads its own stage state; the next stage state goes to a second
         // buffer (dstate) so that no mesh overwrites what another still gathers from.
         for (int g = 0; g < G; ++g) {
@@ -1318,6 +1514,7 @@ static void issue_rk_step(mrab_ctx* c, bool record = true, int order = 0, double
                         ep.csrc[ep.nsrc++] = hh * b[jx];
                     }
             }
+            if (!owns(c, g)) continue;
             issue_rhs(c, g, state_of[g], ep, state_of.data());
             c->evals[g]++;
         }
@@ -1710,6 +1907,7 @@ void mrab_destroy(mrab_ctx* c) {
     for (auto& s : c->side)
         if (s) cudaStreamDestroy(s);
     for (auto& e : c->evpool) cudaEventDestroy(e);
+    if (c->dist && c->dist->tmp) cudaFree(c->dist->tmp);
     if (c->ev_in) cudaEventDestroy(c->ev_in);
     if (c->ev_out) cudaEventDestroy(c->ev_out);
     if (c->st) cudaStreamDestroy(c->st);
@@ -1778,7 +1976,12 @@ static mrab_status var_macro_step(mrab_ctx* c, double H) {
         c->var_mode = true;
     }
     c->h_cur = H / P.S;
-    issue_macro_step(c);
+    if (c->dist) {
+        issue_macro_step_dist(c);
+        if (!c->dist->err.empty()) return fail(MRAB_E_CUDA, "exchange: " + c->dist->err);
+    } else {
+        issue_macro_step(c);
+    }
     CK(cudaGetLastError());
     for (size_t g = 0; g < P.meshes.size(); ++g)
         for (int k = 0; k < P.history_m; ++k) c->ring_t[g][k] -= H;
@@ -1795,6 +1998,17 @@ mrab_status mrab_step(mrab_ctx* c, int n_macro) {
     CK(cudaStreamWaitEvent(c->st, c->ev_in, 0));
     const int64_t nboot_macro = P.history_m - 1;
     for (int it = 0; it < n_macro; ++it) {
+        if (c->dist && c->macro >= nboot_macro && !c->var_mode) {
+            // multi-GPU: direct launches (the exchange sits between them)
+            if (c->scheme > 0) return fail(MRAB_E_INVALID, "multi-GPU contexts run the fastest-first scheme");
+            c->scheme = 0;
+            issue_macro_step_dist(c);
+            CK(cudaGetLastError());
+            if (!c->dist->err.empty()) return fail(MRAB_E_CUDA, "exchange: " + c->dist->err);
+            c->macro++;
+            c->macro_fixed++;
+            continue;
+        }
         if (c->macro >= nboot_macro && c->var_mode) {
             // after variable steps the history is not uniform: the fixed-step graphs do not apply
             mrab_status st = var_macro_step(c, P.S * P.h);
@@ -1878,6 +2092,61 @@ mrab_status mrab_step_scheme(mrab_ctx* c, int n_macro, int scheme) {
     }
     CK(cudaEventRecord(c->ev_out, c->st));
     CK(cudaStreamWaitEvent(c->user, c->ev_out, 0));
+    return MRAB_OK;
+}
+
+mrab_status mrab_partition(const mrab_plan* plan, int nranks, int* owner, double* load) {
+    if (!plan || nranks < 1 || !owner) return fail(MRAB_E_INVALID, "bad plan / nranks / owner");
+    const Plan& P = *plan->P;
+    const int G = (int)P.meshes.size();
+    // longest-processing-time-first: heaviest mesh to the least loaded rank (ties: lowest index)
+    std::vector<double> w(G), L(nranks, 0.0);
+    std::vector<int> ord(G);
+    std::iota(ord.begin(), ord.end(), 0);
+    for (int g = 0; g < G; ++g) w[g] = (double)P.meshes[g].nactive * (P.S / P.meshes[g].s);
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return w[a] > w[b]; });
+    for (int g : ord) {
+        int r = 0;
+        for (int q = 1; q < nranks; ++q)
+            if (L[q] < L[r]) r = q;
+        owner[g] = r;
+        L[r] += w[g];
+    }
+    if (load)
+        for (int q = 0; q < nranks; ++q) load[q] = L[q];
+    return MRAB_OK;
+}
+
+mrab_status mrab_dist_unique_id(void* out128) {
+    if (!out128) return fail(MRAB_E_INVALID, "out128 is NULL");
+    std::string err;
+    if (!nccl_unique_id(out128, &err)) return fail(MRAB_E_CUDA, err);
+    return MRAB_OK;
+}
+
+mrab_status mrab_dist_attach(mrab_ctx* c, int transport, const void* id, int rank, int nranks, const int* owner) {
+    if (!c || !id || !owner || nranks < 1 || rank < 0 || rank >= nranks || (transport != 0 && transport != 1))
+        return fail(MRAB_E_INVALID, "bad arguments");
+    if (c->macro != 0 || c->dist) return fail(MRAB_E_INVALID, "attach once, before the first step");
+    const int G = (int)c->P->meshes.size();
+    for (int g = 0; g < G; ++g)
+        if (owner[g] < 0 || owner[g] >= nranks) return fail(MRAB_E_INVALID, "owner out of range");
+    std::unique_ptr<mrab_ctx::DistState> D(new mrab_ctx::DistState());
+    D->rank = rank;
+    D->nranks = nranks;
+    for (int g = 0; g < 8; ++g) D->ot.owner[g] = g < G ? owner[g] : 0;
+    std::string err;
+    if (transport == MRAB_TRANSPORT_NCCL) D->tp = make_nccl_transport(id, rank, nranks, &err);
+    else D->tp = make_loopback_transport(*(const int*)id, rank, nranks);
+    if (!D->tp) return fail(MRAB_E_CUDA, err);
+    c->dist = std::move(D);
+    return MRAB_OK;
+}
+
+mrab_status mrab_dist_stats(mrab_ctx* c, int64_t* bytes_sent, int64_t* messages) {
+    if (!c || !c->dist) return fail(MRAB_E_INVALID, "not a multi-GPU context");
+    if (bytes_sent) *bytes_sent = c->dist->bytes_sent;
+    if (messages) *messages = c->dist->messages;
     return MRAB_OK;
 }
 
@@ -1999,8 +2268,16 @@ mrab_status mrab_rhs(mrab_ctx* c, const double* const* q, double* const* rhs_out
         CK(cudaMemcpyAsync(c->md[g].ystage, q[g], bytes, cudaMemcpyDefault, c->st));
         state_of[g] = c->md[g].ystage;
     }
-    issue_all_donors(c, state_of.data());
+    if (c->dist) {
+        std::vector<int> allm(G);
+        std::iota(allm.begin(), allm.end(), 0);
+        dist_gather(c, allm, plain_states(c, state_of.data()));
+        if (!c->dist->err.empty()) return fail(MRAB_E_CUDA, "exchange: " + c->dist->err);
+    } else {
+        issue_all_donors(c, state_of.data());
+    }
     for (int g = 0; g < G; ++g) {
+        if (!owns(c, g)) continue;   // (a rank returns the RHS of the meshes it owns)
         Epilogue ep{};
         ep.r_out = c->md[g].kbuf[3];
         issue_rhs(c, g, state_of[g], ep, state_of.data());

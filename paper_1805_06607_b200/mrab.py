@@ -85,6 +85,10 @@ def lib():
         L.mrab_step_h.argtypes = [vp, C.c_int, C.c_double]
         L.mrab_step_scheme.argtypes = [vp, C.c_int, C.c_int]
         L.mrab_rk_step.argtypes = [vp, C.c_int, C.c_int, C.c_double]
+        L.mrab_partition.argtypes = [vp, C.c_int, C.POINTER(C.c_int), dp]
+        L.mrab_dist_unique_id.argtypes = [vp]
+        L.mrab_dist_attach.argtypes = [vp, C.c_int, vp, C.c_int, C.c_int, C.POINTER(C.c_int)]
+        L.mrab_dist_stats.argtypes = [vp, i64p, i64p]
         L.mrab_dt.argtypes = [vp, dp]
         L.mrab_get_state.argtypes = [vp, C.c_int, vp, dp]
         L.mrab_set_state.argtypes = [vp, C.c_int, vp]
@@ -100,7 +104,8 @@ def lib():
                      "mrab_plan_get_tables", "mrab_plan_get_metrics", "mrab_create",
                      "mrab_step", "mrab_get_state", "mrab_set_state", "mrab_rhs",
                      "mrab_get_history", "mrab_set_history", "mrab_get_counters",
-                     "mrab_launches_per_macro_step", "mrab_time_kernel", "mrab_step_h", "mrab_dt", "mrab_step_scheme", "mrab_rk_step"):
+                     "mrab_launches_per_macro_step", "mrab_time_kernel", "mrab_step_h", "mrab_dt", "mrab_step_scheme", "mrab_rk_step", "mrab_partition", "mrab_dist_unique_id", "mrab_dist_attach",
+                     "mrab_dist_stats"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -111,7 +116,8 @@ EXPORTED = ["mrab_ab_weights", "mrab_plan_create", "mrab_plan_destroy", "mrab_pl
             "mrab_create", "mrab_destroy", "mrab_step", "mrab_get_state", "mrab_set_state",
             "mrab_rhs", "mrab_get_counters", "mrab_launches_per_macro_step", "mrab_time_kernel",
             "mrab_set_trace", "mrab_last_error", "mrab_get_history", "mrab_set_history",
-            "mrab_overset_build", "mrab_free", "mrab_plan_get_face_flags", "mrab_step_h", "mrab_dt", "mrab_step_scheme", "mrab_rk_step"]
+            "mrab_overset_build", "mrab_free", "mrab_plan_get_face_flags", "mrab_step_h", "mrab_dt", "mrab_step_scheme", "mrab_rk_step", "mrab_partition", "mrab_dist_unique_id", "mrab_dist_attach",
+            "mrab_dist_stats"]
 
 
 def _check(st):
@@ -276,6 +282,16 @@ class Plan:
         return int(lib().mrab_workspace_bytes(self.h))
 
 
+def partition(plan, nranks):
+    """owner[g] and per-rank load by the work weight active points x evaluations per macro
+    step (mrab_partition)."""
+    G = plan.n_meshes
+    ow = (C.c_int * G)()
+    ld = (C.c_double * nranks)()
+    _check(lib().mrab_partition(plan.h, int(nranks), ow, ld))
+    return [int(x) for x in ow], [float(x) for x in ld]
+
+
 class Context:
     """mrab_ctx on the current torch CUDA device and stream."""
 
@@ -318,6 +334,34 @@ class Context:
             _check(lib().mrab_step(self.h, int(n_macro)))
         else:
             _check(lib().mrab_step_scheme(self.h, int(n_macro), self.SCHEMES[scheme]))
+
+    def attach_loopback(self, world_id, rank, nranks, owner):
+        """Multi-GPU test transport: this context plays `rank` of `nranks` in process-local
+        world `world_id` (mrab_dist_attach, MRAB_TRANSPORT_LOOPBACK)."""
+        wid = C.c_int(int(world_id))
+        ow = (C.c_int * len(owner))(*[int(o) for o in owner])
+        _check(lib().mrab_dist_attach(self.h, 1, C.byref(wid), int(rank), int(nranks), ow))
+        self.owner, self.rank = list(owner), int(rank)
+
+    def attach_nccl(self, dist, owner):
+        """One process per GPU: rank 0 draws the NCCL unique id, torch.distributed broadcasts it,
+        every rank attaches (mrab_dist_attach, MRAB_TRANSPORT_NCCL)."""
+        import torch
+        rank, world = dist.get_rank(), dist.get_world_size()
+        buf = C.create_string_buffer(128)
+        if rank == 0:
+            _check(lib().mrab_dist_unique_id(buf))
+        t = torch.tensor(list(buf.raw), dtype=torch.uint8, device="cuda")
+        dist.broadcast(t, 0)
+        raw = bytes(t.cpu().tolist())
+        ow = (C.c_int * len(owner))(*[int(o) for o in owner])
+        _check(lib().mrab_dist_attach(self.h, 0, C.create_string_buffer(raw, 128), rank, world, ow))
+        self.owner, self.rank = list(owner), rank
+
+    def dist_stats(self):
+        b, m = C.c_int64(), C.c_int64()
+        _check(lib().mrab_dist_stats(self.h, C.byref(b), C.byref(m)))
+        return b.value, m.value
 
     def rk_step(self, h, n_steps=1, order=4):
         """n_steps coupled single-rate RK steps of size h (mrab_rk_step)."""
