@@ -277,6 +277,13 @@ def run_gpu(args):
     p = _problem(args.config, "full", args.sr)
     plan = mrab.Plan(p)
     ctx = mrab.Context(plan, p.q0)
+    part = None
+    if ws > 1 and args.dist:
+        # one problem over the ranks: meshes partitioned by work, donor data over NCCL
+        owner, load = mrab.partition(plan, ws)
+        ctx.attach_nccl(dist, owner)
+        part = {"owner": owner, "load": load}
+        args.no_srab = args.no_secondary = True
     stream = torch.cuda.current_stream()
     G = len(p.meshes)
     nboot = p.history_m - 1
@@ -458,13 +465,14 @@ def run_gpu(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong" if part else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": p.notes["workload"], "config": args.config,
                        "order_n": p.order_n, "history_m": p.history_m,
                        "step_multiples": [m.step_multiple for m in p.meshes],
                        "points": [plan.info(g)[0] for g in range(G)],
                        "active_points": active, "l2": "flushed between timed steps (256 MiB)",
-                       "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU"},
+                       "parallelism": (f"mesh partition x{ws} (owner {part['owner']}, donor data over NCCL)" if part
+                                       else (f"replicas x{ws}" if ws > 1 else "1 GPU"))},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches * args.steps), "launches_per_step": launches,
             "clocks": clk, "bootstrap_ms": boot_ms, "mrab_vs_srab": srab,
@@ -488,6 +496,9 @@ def main():
     ap.add_argument("--no-srab", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--dist", action="store_true",
+                    help="N > 1: partition the meshes of ONE problem over the ranks (strong scaling) "
+                         "instead of independent replicas")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

@@ -1976,12 +1976,14 @@ static mrab_status var_macro_step(mrab_ctx* c, double H) {
         c->var_mode = true;
     }
     c->h_cur = H / P.S;
+    c->launch_counter = 0;
     if (c->dist) {
         issue_macro_step_dist(c);
         if (!c->dist->err.empty()) return fail(MRAB_E_CUDA, "exchange: " + c->dist->err);
     } else {
         issue_macro_step(c);
     }
+    c->launches_last = c->launch_counter;
     CK(cudaGetLastError());
     for (size_t g = 0; g < P.meshes.size(); ++g)
         for (int k = 0; k < P.history_m; ++k) c->ring_t[g][k] -= H;
@@ -2002,7 +2004,9 @@ mrab_status mrab_step(mrab_ctx* c, int n_macro) {
             // multi-GPU: direct launches (the exchange sits between them)
             if (c->scheme > 0) return fail(MRAB_E_INVALID, "multi-GPU contexts run the fastest-first scheme");
             c->scheme = 0;
+            c->launch_counter = 0;
             issue_macro_step_dist(c);
+            c->launches_last = c->launch_counter;
             CK(cudaGetLastError());
             if (!c->dist->err.empty()) return fail(MRAB_E_CUDA, "exchange: " + c->dist->err);
             c->macro++;
@@ -2084,8 +2088,10 @@ mrab_status mrab_step_scheme(mrab_ctx* c, int n_macro, int scheme) {
             if (c->scheme >= 0 && c->scheme != scheme)
                 return fail(MRAB_E_INVALID, "the MRAB scheme of a context is fixed by its first MRAB step");
             c->scheme = scheme;
+            c->launch_counter = 0;
             mrab_status st = issue_macro_step_sf(c, scheme == MRAB_SCHEME_SLOWEST_FIRST_REEXTRAP);
             if (st != MRAB_OK) return st;
+            c->launches_last = c->launch_counter;
         }
         c->macro++;
         c->macro_fixed++;
