@@ -1124,7 +1124,7 @@ __device__ __forceinline__ void sat_point_fv(const DevMesh& m, const double* __r
 namespace {
 constexpr int REG3 = 14 * 8 * 8;                      // extended region (any direction)
 constexpr int KR3 = (REG3 + NT3 - 1) / NT3;           // region points per thread (4)
-constexpr size_t SMEM3 = sizeof(double) * 5 * (REG3 + T3N) + sizeof(uint16_t) * T3N;
+constexpr size_t SMEM3 = sizeof(double) * 5 * REG3 + sizeof(uint16_t) * T3N;
 }  // namespace
 
 // 3-D tile order: CTAs walk 4 x 4 x 4 blocks of 8^3 tiles (a 1-D grid), so that tiles sharing
@@ -1151,9 +1151,11 @@ __global__ void __launch_bounds__(NT3, 2) k_rhs3d(DevMesh m, const double* __res
                                                  const double* __restrict__ FV, Gas g, Epilogue ep,
                                                  const double* __restrict__ FH = nullptr) {
     constexpr int NC = 5;
-    extern __shared__ __align__(16) double fb[];        // Fhat [NC][REG3], then Racc [NC][T3N]
-    double* racc = fb + NC * REG3;
-    uint16_t* sc = reinterpret_cast<uint16_t*>(racc + NC * T3N);
+    extern __shared__ __align__(16) double fb[];        // Fhat [NC][REG3], then the class codes
+    uint16_t* sc = reinterpret_cast<uint16_t*>(fb + NC * REG3);
+    // divergence accumulators of this thread's PPT3 points (registers: the same thread owns
+    // the same points in every direction and in the epilogue)
+    double racc[PPT3][NC];
     const int n0 = m.n[0], n1 = m.n[1], n2 = m.n[2];
     const int64_t N = m.npts;
     const int64_t s1 = n0, s2 = (int64_t)n0 * n1;
@@ -1173,7 +1175,7 @@ __global__ void __launch_bounds__(NT3, 2) k_rhs3d(DevMesh m, const double* __res
         const bool live = gi < n0 && gj < n1 && gk < n2;
         clsv[s] = live ? m.cls[gi + s1 * gj + s2 * gk] : 0u;
 #pragma unroll
-        for (int c = 0; c < NC; ++c) racc[c * T3N + t] = 0.0;
+        for (int c = 0; c < NC; ++c) racc[s][c] = 0.0;
     }
     // PRE: the next direction's region loads are issued before the current direction's
     // stencil, so the three passes' memory round trips overlap the arithmetic
@@ -1295,7 +1297,9 @@ __global__ void __launch_bounds__(NT3, 2) k_rhs3d(DevMesh m, const double* __res
         if (PRE && kap < 2) pre_load(kap + 1, lqp[(kap + 1) & 1]);
         // ---- D_kappa of the staged fluxes at the tile points
         const int sk = kap == 0 ? 1 : (kap == 1 ? RX : RX * RY);
-        for (int t = tid; t < T3N; t += NT3) {
+#pragma unroll
+        for (int s = 0; s < PPT3; ++s) {
+            const int t = tid + s * NT3;
             const unsigned code = sc[t];
             if (!code) continue;
             const int x = t & 7, y = (t >> 3) & 7, z = t >> 6;
@@ -1305,7 +1309,7 @@ __global__ void __launch_bounds__(NT3, 2) k_rhs3d(DevMesh m, const double* __res
 #pragma unroll
                 for (int c = 0; c < NC; ++c) {
                     const double* f = fb + c * REG3;
-                    racc[c * T3N + t] += (2.0 / 3.0) * (f[rr + sk] - f[rr - sk]) - (1.0 / 12.0) * (f[rr + 2 * sk] - f[rr - 2 * sk]);
+                    racc[s][c] += (2.0 / 3.0) * (f[rr + sk] - f[rr - sk]) - (1.0 / 12.0) * (f[rr + 2 * sk] - f[rr - 2 * sk]);
                 }
             } else {
                 const int ns = c_nst[cl];
@@ -1317,7 +1321,7 @@ __global__ void __launch_bounds__(NT3, 2) k_rhs3d(DevMesh m, const double* __res
                     for (int c = 0; c < NC; ++c) acc[c] += cf * fb[c * REG3 + o];
                 }
 #pragma unroll
-                for (int c = 0; c < NC; ++c) racc[c * T3N + t] += acc[c];
+                for (int c = 0; c < NC; ++c) racc[s][c] += acc[c];
             }
         }
         __syncthreads();
@@ -1370,7 +1374,7 @@ __global__ void __launch_bounds__(NT3, 2) k_rhs3d(DevMesh m, const double* __res
         if (code) {
             const double Jp = CART ? m.cJ : __ldg(m.J + p);
 #pragma unroll
-            for (int c = 0; c < NC; ++c) Rs[c] = -Jp * racc[c * T3N + t];
+            for (int c = 0; c < NC; ++c) Rs[c] = -Jp * racc[s][c];
             bool sat = false;
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
