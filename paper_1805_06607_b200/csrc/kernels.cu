@@ -1398,6 +1398,233 @@ __global__ void __launch_bounds__(NT3, 2) k_rhs3d(DevMesh m, const double* __res
 }
 
 // ------------------------------------------------------------------------------------
+// k_div3w: pass 2 of the two-pass 3-D RHS on 16 x 8 x 4 tiles.  Same arithmetic as
+// k_rhs3d<PRE> (the two are interchangeable, Options::div_wide), different tile: the L1 data
+// pipe is the busiest unit of pass 2 (ncu: 71 % of peak), and with 8-wide tiles every global
+// warp access touches four 128-byte lines (64-byte rows).  Rows of 16 doubles are whole lines:
+// the region loads touch ~38 % fewer lines and the epilogue loads and stores half as many.
+// One staging buffer in registers (the next direction's region loads are issued before the
+// current direction's stencils and stored after them), accumulators in registers.
+// ------------------------------------------------------------------------------------
+namespace w3 {
+constexpr int WX = 16, WY = 8, WZ = 4, WN = WX * WY * WZ, NT = 256, PPT = WN / NT;
+constexpr int REGW = WX * WY * (WZ + 6);                       // largest extended region (z)
+constexpr size_t SMEM = sizeof(double) * 5 * REGW + sizeof(uint16_t) * WN;
+template <int KK>
+struct Reg {
+    static constexpr int ex = KK == 0 ? 3 : 0, ey = KK == 1 ? 3 : 0, ez = KK == 2 ? 3 : 0;
+    static constexpr int RX = WX + 2 * ex, RY = WY + 2 * ey, RZ = WZ + 2 * ez, N = RX * RY * RZ;
+    static constexpr int KR = (N + NT - 1) / NT;               // region points per thread: 3, 4, 5
+    static constexpr int sk = KK == 0 ? 1 : (KK == 1 ? RX : RX * RY);
+};
+constexpr int KRMAX = 5;
+}  // namespace w3
+
+// tile order: blocks of 2 x 4 x 8 tiles (32^3 points), as tile3_blocked
+__device__ __forceinline__ bool tilew_blocked(const DevMesh& m, int& bx, int& by, int& bz) {
+    const int tx = (m.n[0] + w3::WX - 1) / w3::WX, ty = (m.n[1] + w3::WY - 1) / w3::WY,
+              tz = (m.n[2] + w3::WZ - 1) / w3::WZ;
+    const int sx = (tx + 1) / 2, sy = (ty + 3) / 4;
+    const int b = blockIdx.x, loc = b & 63, sup = b >> 6;
+    bx = (sup % sx) * 2 + (loc & 1);
+    by = ((sup / sx) % sy) * 4 + ((loc >> 1) & 3);
+    bz = (sup / (sx * sy)) * 8 + (loc >> 3);
+    return bx < tx && by < ty && bz < tz;
+}
+static inline unsigned tilew_blocks(const int* n) {
+    const int tx = (n[0] + w3::WX - 1) / w3::WX, ty = (n[1] + w3::WY - 1) / w3::WY, tz = (n[2] + w3::WZ - 1) / w3::WZ;
+    return (unsigned)(((tx + 1) / 2) * ((ty + 3) / 4) * ((tz + 7) / 8) * 64);
+}
+
+template <int KK>
+__device__ __forceinline__ void w3_load(const DevMesh& m, const double* __restrict__ FH, int i0, int j0, int k0,
+                                        double (&lq)[w3::KRMAX][5]) {
+    using R = w3::Reg<KK>;
+    const int64_t N = m.npts, s1 = m.n[0], s2 = (int64_t)m.n[0] * m.n[1];
+#pragma unroll
+    for (int r = 0; r < R::KR; ++r) {
+        const int t = threadIdx.x + r * w3::NT;
+        if (R::N % w3::NT != 0 && t >= R::N) break;
+        const int x = t % R::RX, y = (t / R::RX) % R::RY, z = t / (R::RX * R::RY);
+        int gg[3] = {i0 - R::ex + x, j0 - R::ey + y, k0 - R::ez + z};
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const int n = m.n[k];
+            if (gg[k] < 0) gg[k] = m.periodic[k] ? gg[k] + n : 0;
+            else if (gg[k] >= n) gg[k] = m.periodic[k] ? gg[k] - n : n - 1;
+        }
+        const int64_t q = gg[0] + s1 * gg[1] + s2 * gg[2];
+#pragma unroll
+        for (int c = 0; c < 5; ++c) lq[r][c] = __ldg(FH + (int64_t)(KK * 5 + c) * N + q);
+    }
+}
+
+template <int KK>
+__device__ __forceinline__ void w3_store(double* __restrict__ fb, const double (&lq)[w3::KRMAX][5]) {
+    using R = w3::Reg<KK>;
+#pragma unroll
+    for (int r = 0; r < R::KR; ++r) {
+        const int t = threadIdx.x + r * w3::NT;
+        if (R::N % w3::NT != 0 && t >= R::N) break;
+#pragma unroll
+        for (int c = 0; c < 5; ++c) fb[c * w3::REGW + t] = lq[r][c];
+    }
+}
+
+template <int KK>
+__device__ __forceinline__ void w3_div(const double* __restrict__ fb, const uint16_t* __restrict__ sc,
+                                       double (&racc)[w3::PPT][5]) {
+    using R = w3::Reg<KK>;
+#pragma unroll
+    for (int s = 0; s < w3::PPT; ++s) {
+        const int t = threadIdx.x + s * w3::NT;
+        const unsigned code = sc[t];
+        if (!code) continue;
+        const int x = t & 15, y = (t >> 4) & 7, z = t >> 7;
+        const int rr = (x + R::ex) + R::RX * ((y + R::ey) + R::RY * (z + R::ez));
+        const int cl = (code >> (4 * KK)) & 15;
+        if (cl == CLS_INT) {
+#pragma unroll
+            for (int c = 0; c < 5; ++c) {
+                const double* f = fb + c * w3::REGW;
+                racc[s][c] += (2.0 / 3.0) * (f[rr + R::sk] - f[rr - R::sk]) - (1.0 / 12.0) * (f[rr + 2 * R::sk] - f[rr - 2 * R::sk]);
+            }
+        } else {
+            const int ns = c_nst[cl];
+            double acc[5] = {0, 0, 0, 0, 0};
+            for (int tt = 0; tt < ns; ++tt) {
+                const double cf = c_cf[cl][tt];
+                const int o = rr + c_off[cl][tt] * R::sk;
+#pragma unroll
+                for (int c = 0; c < 5; ++c) acc[c] += cf * fb[c * w3::REGW + o];
+            }
+#pragma unroll
+            for (int c = 0; c < 5; ++c) racc[s][c] += acc[c];
+        }
+    }
+}
+
+template <bool VISC, bool CART>
+__global__ void __launch_bounds__(w3::NT, 2) k_div3w(DevMesh m, const double* __restrict__ Q,
+                                                    const double* __restrict__ FV, Gas g, Epilogue ep,
+                                                    const double* __restrict__ FH) {
+    using namespace w3;
+    constexpr int NC = 5;
+    extern __shared__ __align__(16) double fb[];        // Fhat [NC][REGW], then the class codes
+    uint16_t* sc = reinterpret_cast<uint16_t*>(fb + NC * REGW);
+    const int n0 = m.n[0], n1 = m.n[1], n2 = m.n[2];
+    const int64_t N = m.npts;
+    const int64_t s1 = n0, s2 = (int64_t)n0 * n1;
+    int tbx, tby, tbz;
+    if (!tilew_blocked(m, tbx, tby, tbz)) return;
+    const int i0 = tbx * WX, j0 = tby * WY, k0 = tbz * WZ;
+    const int tid = threadIdx.x;
+    double racc[PPT][NC];
+    double lq[KRMAX][NC];
+    w3_load<0>(m, FH, i0, j0, k0, lq);
+#pragma unroll
+    for (int s = 0; s < PPT; ++s) {
+        const int t = tid + s * NT;
+        const int gi = i0 + (t & 15), gj = j0 + ((t >> 4) & 7), gk = k0 + (t >> 7);
+        const bool live = gi < n0 && gj < n1 && gk < n2;
+        sc[t] = live ? m.cls[gi + s1 * gj + s2 * gk] : (uint16_t)0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) racc[s][c] = 0.0;
+    }
+    w3_store<0>(fb, lq);
+    __syncthreads();
+    w3_load<1>(m, FH, i0, j0, k0, lq);
+    w3_div<0>(fb, sc, racc);
+    __syncthreads();
+    w3_store<1>(fb, lq);
+    __syncthreads();
+    w3_load<2>(m, FH, i0, j0, k0, lq);
+    w3_div<1>(fb, sc, racc);
+    __syncthreads();
+    w3_store<2>(fb, lq);
+    __syncthreads();
+    // the epilogue inputs of this thread's points, in flight during the last stencil
+    double yb[PPT][NC];
+    int64_t pp[PPT];
+    bool livep[PPT];
+#pragma unroll
+    for (int s = 0; s < PPT; ++s) {
+        const int t = tid + s * NT;
+        const int gi = i0 + (t & 15), gj = j0 + ((t >> 4) & 7), gk = k0 + (t >> 7);
+        livep[s] = gi < n0 && gj < n1 && gk < n2;
+        pp[s] = livep[s] ? gi + s1 * gj + s2 * gk : 0;
+        const int64_t p = pp[s];
+        if (ep.y_out && ep.nsrc == 2) {
+            double v[3][NC];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                v[0][c] = __ldg(ep.base + c * N + p);
+                v[1][c] = __ldg(ep.src[0] + c * N + p);
+                v[2][c] = __ldg(ep.src[1] + c * N + p);
+            }
+#pragma unroll
+            for (int c = 0; c < NC; ++c) yb[s][c] = v[0][c] + ep.csrc[0] * v[1][c] + ep.csrc[1] * v[2][c];
+        } else if (ep.y_out) {
+            // all history loads issued together (unused slots re-read `base` with weight 0)
+            const double* sp[4];
+            double cw[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                sp[k] = k < ep.nsrc ? ep.src[k] : ep.base;
+                cw[k] = k < ep.nsrc ? ep.csrc[k] : 0.0;
+            }
+            double v[5][NC];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                v[0][c] = __ldg(ep.base + c * N + p);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) v[1 + k][c] = __ldg(sp[k] + c * N + p);
+            }
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+                yb[s][c] = v[0][c] + cw[0] * v[1][c] + cw[1] * v[2][c] + cw[2] * v[3][c] + cw[3] * v[4][c];
+            for (int k = 4; k < ep.nsrc; ++k)
+#pragma unroll
+                for (int c = 0; c < NC; ++c) yb[s][c] += ep.csrc[k] * __ldg(ep.src[k] + c * N + p);
+        }
+    }
+    w3_div<2>(fb, sc, racc);
+    // ---- SAT and epilogue
+#pragma unroll
+    for (int s = 0; s < PPT; ++s) {
+        if (!livep[s]) continue;
+        const int t = tid + s * NT;
+        const int gi = i0 + (t & 15), gj = j0 + ((t >> 4) & 7), gk = k0 + (t >> 7);
+        const int64_t p = pp[s];
+        const unsigned code = sc[t];
+        double Rs[NC] = {0, 0, 0, 0, 0};
+        if (code) {
+            const double Jp = CART ? m.cJ : __ldg(m.J + p);
+#pragma unroll
+            for (int c = 0; c < NC; ++c) Rs[c] = -Jp * racc[s][c];
+            bool sat = false;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const int cl = (code >> (4 * k)) & 15;
+                sat = sat || cl == CLS_L0 || cl == CLS_R0;
+            }
+            if (sat) {
+                const int idx[3] = {gi, gj, gk};
+                sat_point_fv<3, VISC, CART>(m, Q, FV, g, p, idx, code, Jp, Rs);
+            }
+        }
+        if (ep.r_out) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) ep.r_out[c * N + p] = Rs[c];
+        }
+        if (ep.y_out) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) ep.y_out[c * N + p] = yb[s][c] + ep.c_new * Rs[c];
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
 // 3-D RHS in two passes (default; MRAB_3D_SPLIT=0 restores k_visc3d_x + k_rhs3d):
 //   k_flux3d  per tile: the cross-shaped state region staged by cp.async in one round trip
 //             (as k_visc3d_x), primitives in place, D1 gradients at the tile points, then the
@@ -1936,7 +2163,21 @@ void launch_flux3d(const DevMesh& m, const double* Q, const Gas& gas, cudaStream
 }
 
 template <bool VISC, bool CART>
+static void launch_div3w(const DevMesh& m, const double* Q, const Gas& gas, const Epilogue& ep, cudaStream_t st) {
+    static bool init = false;
+    if (!init) {
+        cudaFuncSetAttribute(k_div3w<VISC, CART>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w3::SMEM);
+        init = true;
+    }
+    launch_k(k_div3w<VISC, CART>, dim3(tilew_blocks(m.n)), dim3(w3::NT), w3::SMEM, st, m, Q, (const double*)m.fv, gas, ep, m.fh);
+}
+
+template <bool VISC, bool CART>
 static void launch_div3d(const DevMesh& m, const double* Q, const Gas& gas, const Epilogue& ep, cudaStream_t st) {
+    if (opts().div_wide) {
+        launch_div3w<VISC, CART>(m, Q, gas, ep, st);
+        return;
+    }
     static bool init = false;
     if (!init) {
         cudaFuncSetAttribute(k_rhs3d<VISC, CART, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM3);

@@ -1,6 +1,7 @@
 """GPU parity of the non-default kernel paths (selected by the MRAB_* switches, read into the
 plan's Options at mrab_plan_create; each case runs in a subprocess): the one-pass fused 3-D
-RHS (k_rhs3z: z-marching tiles, TMA-staged planes), the per-receiver 3-D gather, the 2-D general tile path for every tile (no lean path), and the serial
+RHS (k_rhs3z: z-marching tiles, TMA-staged planes), the per-receiver 3-D gather, the 8^3-tile
+divergence pass (k_rhs3d<PRE>; the default is k_div3w on 16 x 8 x 4 tiles), the 3-D task-flow schedule, the 2-D general tile path for every tile (no lean path), and the serial
 (non-overlapped) 2-D schedule with uncapped curvilinear tiles.  Each must match the oracle like the
 default path (states after N macro steps to 1e-10, RHS to 1e-10)."""
 import os
@@ -42,6 +43,9 @@ CASES = [
     (4, {"MRAB_3D_FUSED": "1"}),
     (5, {"MRAB_3D_FUSED": "1"}),
     (5, {"MRAB_INTERP_BOX": "0"}),
+    (4, {"MRAB_DIV_WIDE": "0"}),
+    (5, {"MRAB_DIV_WIDE": "0"}),
+    (5, {"MRAB_OVERLAP3D": "1"}),
     (3, {"MRAB_LEAN": "0"}),
     (3, {"MRAB_TILE_FLAGS": "0"}),
     (2, {"MRAB_OVERLAP": "0", "MRAB_CURV_HALF": "0"}),
