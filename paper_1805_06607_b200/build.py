@@ -13,7 +13,9 @@ LIB = os.path.join(LIBDIR, "libmrab.so")
 SOURCES = ["mrab_api.cu", "kernels.cu", "kernels2d.cu", "host_setup.cpp", "dist.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-FLAGS = [*(["-DMRAB_Z3_PROF"] if os.environ.get("MRAB_Z3_PROF") else []), "-O3", "-std=c++17", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
+FLAGS = [*(["-DMRAB_Z3_PROF"] if os.environ.get("MRAB_Z3_PROF") else []),
+         *([f"-DMRAB_W3_MINB={os.environ['MRAB_W3_MINB']}"] if os.environ.get("MRAB_W3_MINB") else []),
+         *([f"-DMRAB_F3_MINB={os.environ['MRAB_F3_MINB']}"] if os.environ.get("MRAB_F3_MINB") else []), "-O3", "-std=c++17", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
          "-Xcompiler", "-fPIC,-fopenmp,-O3", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 
 

@@ -38,6 +38,7 @@ Options read_options() {
     o.z3_fused = (int)env_or("MRAB_3D_FUSED", o.z3_fused);
     o.overlap3d = (int)env_or("MRAB_OVERLAP3D", o.overlap3d);
     o.div_wide = (int)env_or("MRAB_DIV_WIDE", o.div_wide);
+    o.flux_wide = (int)env_or("MRAB_FLUX_WIDE", o.flux_wide);
     return o;
 }
 const Options& opts() { return g_opt; }

@@ -1406,6 +1406,12 @@ __global__ void __launch_bounds__(NT3, 2) k_rhs3d(DevMesh m, const double* __res
 // One staging buffer in registers (the next direction's region loads are issued before the
 // current direction's stencils and stored after them), accumulators in registers.
 // ------------------------------------------------------------------------------------
+#ifndef MRAB_W3_MINB
+#define MRAB_W3_MINB 2
+#endif
+#ifndef MRAB_F3_MINB
+#define MRAB_F3_MINB 3
+#endif
 namespace w3 {
 constexpr int WX = 16, WY = 8, WZ = 4, WN = WX * WY * WZ, NT = 256, PPT = WN / NT;
 constexpr int REGW = WX * WY * (WZ + 6);                       // largest extended region (z)
@@ -1505,7 +1511,7 @@ __device__ __forceinline__ void w3_div(const double* __restrict__ fb, const uint
 }
 
 template <bool VISC, bool CART>
-__global__ void __launch_bounds__(w3::NT, 2) k_div3w(DevMesh m, const double* __restrict__ Q,
+__global__ void __launch_bounds__(w3::NT, MRAB_W3_MINB) k_div3w(DevMesh m, const double* __restrict__ Q,
                                                     const double* __restrict__ FV, Gas g, Epilogue ep,
                                                     const double* __restrict__ FH) {
     using namespace w3;
@@ -1767,6 +1773,226 @@ __global__ void __launch_bounds__(NT3, 2) k_flux3d(DevMesh m, const double* __re
                     for (int j = 0; j < 4; ++j) FV[(int64_t)(i * 4 + j) * N + p] = fv[i][j];
         }
         // Cartesian fluxes F_i = F^I_i - F^V_i, then Fhat_kappa
+        double F[3][5];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const double mi = r * u[i];
+            F[i][0] = mi;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) F[i][1 + j] = mi * u[j] + (i == j ? pr : 0.0) - fv[i][j];
+            F[i][4] = (E + pr) * u[i] - fv[i][3];
+        }
+#pragma unroll
+        for (int kap = 0; kap < 3; ++kap)
+#pragma unroll
+            for (int c = 0; c < 5; ++c) {
+                double fh;
+                if (CART) fh = m.cM[kap] * F[kap][c];
+                else fh = Mp[kap][0] * F[0][c] + Mp[kap][1] * F[1][c] + Mp[kap][2] * F[2][c];
+                FH[(int64_t)(kap * 5 + c) * N + p] = fh;
+            }
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// k_flux3w: pass 1 of the two-pass 3-D RHS on 16 x 8 x 4 tiles (same arithmetic as k_flux3d;
+// Options::flux_wide).  The L1 data pipe is the busiest unit of pass 1 too (ncu: 72 % of peak,
+// 28 % of its shared-memory wavefronts bank-conflict replays).  Here the state of the
+// cross-shaped region (tile + 3 on each face: 1856 points) is loaded through registers, turned
+// into (u, v, w, T) there and stored once (rho only for the tile's own points): no cp.async
+// write plus in-place conversion pass (-30 % shared-memory accesses per point), and rows of 16
+// doubles are whole 128-byte lines for the loads and for the 15 (+12) flux stores.
+// Region index of tile-relative (x, y, z): the tile x + 16 y + 128 z, then the 3-deep face slabs
+// x-, x+ (3 fastest), y-, y+ and z-, z+ (x fastest).
+// ------------------------------------------------------------------------------------
+namespace f3 {
+constexpr int WX = 16, WY = 8, WZ = 4, WN = 512, NT = 256, PPT = 2;
+constexpr int OXM = WN, OXP = OXM + 96, OYM = OXP + 96, OYP = OYM + 192, OZM = OYP + 192, OZP = OZM + 384;
+constexpr int NREG = OZP + 384;                                   // 1856
+constexpr int KR = (NREG + NT - 1) / NT;                          // 8 (7.25)
+constexpr size_t SMEM = sizeof(double) * (4 * NREG + WN) + sizeof(uint16_t) * WN;
+__device__ __forceinline__ int idx(int x, int y, int z) {
+    if (x < 0) return OXM + (x + 3) + 3 * (y + 8 * z);
+    if (x >= WX) return OXP + (x - WX) + 3 * (y + 8 * z);
+    if (y < 0) return OYM + x + 16 * ((y + 3) + 3 * z);
+    if (y >= WY) return OYP + x + 16 * ((y - WY) + 3 * z);
+    if (z < 0) return OZM + x + 16 * y + 128 * (z + 3);
+    if (z >= WZ) return OZP + x + 16 * y + 128 * (z - WZ);
+    return x + 16 * y + 128 * z;
+}
+__device__ __forceinline__ void xyz(int t, int& x, int& y, int& z) {
+    if (t < WN) {
+        x = t & 15; y = (t >> 4) & 7; z = t >> 7;
+    } else if (t < OYM) {
+        const int w = t < OXP ? t - OXM : t - OXP;
+        x = (t < OXP ? -3 : WX) + w % 3;
+        y = (w / 3) & 7;
+        z = w / 24;
+    } else if (t < OZM) {
+        const int w = t < OYP ? t - OYM : t - OYP;
+        x = w & 15;
+        y = (t < OYP ? -3 : WY) + (w >> 4) % 3;
+        z = (w >> 4) / 3;
+    } else {
+        const int w = t < OZP ? t - OZM : t - OZP;
+        x = w & 15;
+        y = (w >> 4) & 7;
+        z = (t < OZP ? -3 : WZ) + (w >> 7);
+    }
+}
+}  // namespace f3
+
+template <bool VISC, bool CART>
+__global__ void __launch_bounds__(f3::NT, MRAB_F3_MINB) k_flux3w(DevMesh m, const double* __restrict__ Q,
+                                                     double* __restrict__ FH, double* __restrict__ FV,
+                                                     const uint8_t* __restrict__ fvtile, Gas g) {
+    using namespace f3;
+    extern __shared__ __align__(16) double sm[];   // [4][NREG]: u, v, w, T; then rho [WN]
+    double* pf = sm;
+    double* rh = sm + 4 * NREG;
+    uint16_t* sc = reinterpret_cast<uint16_t*>(rh + WN);
+    const int n0 = m.n[0], n1 = m.n[1], n2 = m.n[2];
+    const int64_t N = m.npts;
+    const int64_t s1 = n0, s2 = (int64_t)n0 * n1;
+    int tbx, tby, tbz;
+    if (!tilew_blocked(m, tbx, tby, tbz)) return;
+    const int i0 = tbx * WX, j0 = tby * WY, k0 = tbz * WZ;
+    const int tid = threadIdx.x;
+    const int per0 = m.periodic[0], per1 = m.periodic[1], per2 = m.periodic[2];
+    // F^V is written where the 8^3 flag tiles under this tile ask for it (SAT points, donor stencils)
+    bool wfv = false;
+    if (VISC) {
+        const int ntx = (n0 + 7) / 8, nty = (n1 + 7) / 8;
+        const int fz = (k0 >> 3), fy = (j0 >> 3), fx = (i0 >> 3);
+        wfv = fvtile[fx + ntx * (fy + nty * fz)] || (fx + 1 < ntx && fvtile[fx + 1 + ntx * (fy + nty * fz)]);
+    }
+    const int nreg = VISC ? NREG : WN;   // Euler: no gradients, the tile itself suffices
+    // ---- region state through registers -> primitives in shared memory (two batches)
+#pragma unroll
+    for (int b0 = 0; b0 < KR; b0 += 4) {
+        double q[4][5];
+        int tt[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int t = tid + (b0 + r) * NT;
+            tt[r] = t < nreg ? t : -1;
+            if (tt[r] < 0) continue;
+            int x, y, z;
+            xyz(t, x, y, z);
+            int gi = i0 + x, gj = j0 + y, gk = k0 + z;
+            if (gi < 0) gi = per0 ? gi + n0 : 0; else if (gi >= n0) gi = per0 ? gi - n0 : n0 - 1;
+            if (gj < 0) gj = per1 ? gj + n1 : 0; else if (gj >= n1) gj = per1 ? gj - n1 : n1 - 1;
+            if (gk < 0) gk = per2 ? gk + n2 : 0; else if (gk >= n2) gk = per2 ? gk - n2 : n2 - 1;
+            const int64_t p = gi + s1 * gj + s2 * gk;
+#pragma unroll
+            for (int c = 0; c < 5; ++c) q[r][c] = __ldg(Q + c * N + p);
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            if (tt[r] < 0) continue;
+            const int t = tt[r];
+            const double ir = rcp64(q[r][0]);
+            const double u = q[r][1] * ir, v = q[r][2] * ir, w = q[r][3] * ir;
+            pf[t] = u;
+            pf[NREG + t] = v;
+            pf[2 * NREG + t] = w;
+            pf[3 * NREG + t] = g.gamma * g.gm1 * (q[r][4] - 0.5 * (q[r][1] * u + q[r][2] * v + q[r][3] * w)) * ir;
+            if (t < WN) rh[t] = q[r][0];
+        }
+    }
+#pragma unroll
+    for (int s = 0; s < PPT; ++s) {
+        const int t = tid + s * NT;
+        const int gi = i0 + (t & 15), gj = j0 + ((t >> 4) & 7), gk = k0 + (t >> 7);
+        const bool live = gi < n0 && gj < n1 && gk < n2;
+        sc[t] = live ? m.cls[gi + s1 * gj + s2 * gk] : (uint16_t)0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < PPT; ++s) {
+        const int t = tid + s * NT;
+        const int x = t & 15, y = (t >> 4) & 7, z = t >> 7;
+        if (i0 + x >= n0 || j0 + y >= n1 || k0 + z >= n2) continue;
+        const int64_t p = (i0 + x) + s1 * (j0 + y) + s2 * (k0 + z);
+        const unsigned code = sc[t];
+        if (!code) {
+#pragma unroll
+            for (int c = 0; c < 15; ++c) FH[(int64_t)c * N + p] = 0.0;
+            continue;
+        }
+        const double r = rh[t];
+        const double u[3] = {pf[t], pf[NREG + t], pf[2 * NREG + t]};
+        const double T = pf[3 * NREG + t];
+        const double pr = r * T * g.igamma;
+        const double E = pr * g.igm1 + 0.5 * r * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+        double fv[3][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}, {0, 0, 0, 0}};
+        double Jp = 0.0, Mp[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+        if (!CART) {
+            Jp = __ldg(m.J + p);
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+#pragma unroll
+                for (int i = 0; i < 3; ++i) Mp[k][i] = __ldg(m.M + (k * 3 + i) * N + p);
+        }
+        if (VISC) {
+            double d[3][4];   // d[kappa][u, v, w, T]
+#pragma unroll
+            for (int kap = 0; kap < 3; ++kap) {
+                const int cl = (code >> (4 * kap)) & 15;
+                auto at = [&](int o) {
+                    return kap == 0 ? idx(x + o, y, z) : (kap == 1 ? idx(x, y + o, z) : idx(x, y, z + o));
+                };
+                if (cl == CLS_INT) {
+                    const int a1 = at(1), b1 = at(-1), a2 = at(2), b2 = at(-2);
+#pragma unroll
+                    for (int f = 0; f < 4; ++f) {
+                        const double* a = pf + f * NREG;
+                        d[kap][f] = (2.0 / 3.0) * (a[a1] - a[b1]) - (1.0 / 12.0) * (a[a2] - a[b2]);
+                    }
+                } else {
+#pragma unroll
+                    for (int f = 0; f < 4; ++f) d[kap][f] = 0.0;
+                    const int ns = c_nst[cl];
+                    for (int tt2 = 0; tt2 < ns; ++tt2) {
+                        const double cf = c_cf[cl][tt2];
+                        const int o = at(c_off[cl][tt2]);
+#pragma unroll
+                        for (int f = 0; f < 4; ++f) d[kap][f] += cf * pf[f * NREG + o];
+                    }
+                }
+            }
+            double gr[4][3];
+#pragma unroll
+            for (int f = 0; f < 4; ++f)
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    if (CART) {
+                        gr[f][i] = m.cJ * (m.cM[i] * d[i][f]);
+                    } else {
+                        double acc = 0.0;
+#pragma unroll
+                        for (int k = 0; k < 3; ++k) acc += Mp[k][i] * d[k][f];
+                        gr[f][i] = Jp * acc;
+                    }
+                }
+            const double div = gr[0][0] + gr[1][1] + gr[2][2];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                double e = 0.0;
+#pragma unroll
+                for (int j = 0; j < 3; ++j) {
+                    const double tau = (gr[i][j] + gr[j][i] - (i == j ? (2.0 / 3.0) * div : 0.0)) * g.iRe;
+                    fv[i][j] = tau;
+                    e += u[j] * tau;
+                }
+                fv[i][3] = e + g.kT * gr[3][i];
+            }
+            if (wfv)
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) FV[(int64_t)(i * 4 + j) * N + p] = fv[i][j];
+        }
         double F[3][5];
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
@@ -2143,6 +2369,26 @@ static void launch_z3(const DevMesh& m, const double* Q, const Gas& gas, const E
 }
 
 void launch_flux3d(const DevMesh& m, const double* Q, const Gas& gas, cudaStream_t st) {
+    if (opts().flux_wide) {
+        static bool initw = false;
+        if (!initw) {
+            cudaFuncSetAttribute(k_flux3w<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3::SMEM);
+            cudaFuncSetAttribute(k_flux3w<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3::SMEM);
+            cudaFuncSetAttribute(k_flux3w<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3::SMEM);
+            cudaFuncSetAttribute(k_flux3w<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3::SMEM);
+            initw = true;
+        }
+        const dim3 gw(tilew_blocks(m.n));
+        double* FHw = const_cast<double*>(m.fh);
+        if (gas.viscous) {
+            if (m.cart) launch_k(k_flux3w<true, true>, gw, dim3(f3::NT), f3::SMEM, st, m, Q, FHw, m.fv, m.fvtile, gas);
+            else launch_k(k_flux3w<true, false>, gw, dim3(f3::NT), f3::SMEM, st, m, Q, FHw, m.fv, m.fvtile, gas);
+        } else {
+            if (m.cart) launch_k(k_flux3w<false, true>, gw, dim3(f3::NT), f3::SMEM, st, m, Q, FHw, m.fv, m.fvtile, gas);
+            else launch_k(k_flux3w<false, false>, gw, dim3(f3::NT), f3::SMEM, st, m, Q, FHw, m.fv, m.fvtile, gas);
+        }
+        return;
+    }
     static bool init = false;
     if (!init) {
         cudaFuncSetAttribute(k_flux3d<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEMX);
