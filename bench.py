@@ -383,7 +383,7 @@ def run_gpu(args):
             "kernel": (f"k_rhs2d (fused RHS+SAT+AB) on mesh {gdom} ({p.meshes[gdom].name})" if p.dim == 2 else
                        (f"k_rhs3z (fused one-pass RHS + SAT + AB, z-marching) on mesh {gdom} ({p.meshes[gdom].name})"
                         if os.environ.get("MRAB_3D_FUSED", "0") not in ("", "0") else
-                        f"k_flux3d + k_rhs3d (RHS in two passes, SAT, AB) on mesh {gdom} ({p.meshes[gdom].name})")),
+                        f"k_flux3w + k_div3w (RHS in two passes on 16x8x4 tiles, SAT, AB) on mesh {gdom} ({p.meshes[gdom].name})")),
             "algorithmic_bytes_per_launch": by, "ms_per_launch": ms, "peak_source": peak_src,
             "kernel_ms_per_step_cold": kernel_times, "other_meshes": others,
             "fp64_pipe_pct_ncu": fp64_pct, "fp64_peak_tflops": _fp64_peak()[0],

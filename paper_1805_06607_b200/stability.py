@@ -56,6 +56,54 @@ class StepMap:
         self.ctx.step(1)
         return self.read()
 
+    # ---- device-resident variant: the integrator vector stays on the GPU (torch tensors), the
+    # accessors copy device to device, so forming a column costs no host round trip
+    def read_device(self, out=None):
+        import torch
+        if out is None:
+            out = torch.empty(self.dim, dtype=torch.float64, device="cuda")
+        o = 0
+        for g, n in enumerate(self.sizes):
+            self.ctx.get_state(g, out=out[o:o + n])
+            o += n
+            for k in range(self.m - 1):
+                self.ctx.get_history(g, k, out=out[o:o + n])
+                o += n
+        return out
+
+    def write_device(self, phi):
+        o = 0
+        for g, n in enumerate(self.sizes):
+            self.ctx.set_state(g, phi[o:o + n])
+            o += n
+            for k in range(self.m - 1):
+                self.ctx.set_history(g, k, phi[o:o + n])
+                o += n
+
+    def apply_device(self, phi, out=None):
+        self.write_device(phi)
+        self.ctx.step(1)
+        return self.read_device(out)
+
+
+def step_matrix_device(smap: StepMap, phi0, eps=EPS, cols=None):
+    """G_eps (eq:sm_form) with every vector resident on the GPU: phi0 is perturbed on the
+    device, written into the context by device-to-device copies, stepped, read back on the
+    device and differenced there; the matrix is returned as a CUDA tensor (columns `cols`)."""
+    import torch
+    phi0 = torch.as_tensor(phi0, dtype=torch.float64, device="cuda")
+    base = smap.apply_device(phi0).clone()
+    cols = list(range(phi0.numel())) if cols is None else list(cols)
+    G = torch.empty((base.numel(), len(cols)), dtype=torch.float64, device="cuda")
+    ph = phi0.clone()
+    buf = torch.empty_like(base)
+    for c, j in enumerate(cols):
+        ph[j] += eps
+        smap.apply_device(ph, out=buf)
+        G[:, c] = (buf - base) / eps
+        ph[j] = phi0[j]
+    return G
+
 
 class RKMap:
     """phi -> phi' = one step of size h of the reference Runge-Kutta integrator (classical RK4

@@ -130,3 +130,14 @@ def test_arnoldi_matches_dense_rho():
     assert arn <= dense * (1 + 1e-5), (arn, dense, nmv)
     assert dense - 5e-3 <= gr <= dense * (1 + 2e-4), (gr, dense)
     ctx.close()
+
+
+def test_device_resident_step_matrix_equals_host(setup):
+    """step_matrix_device keeps every integrator vector on the GPU (device-to-device accessor
+    copies, differences in torch): its columns equal the host-round-trip ones to the last bit or
+    two (torch divides by eps through a reciprocal multiply; the stepped vectors are identical)."""
+    p, st, smap, phi0 = setup
+    cols = [0, 7, 300, 1111, 2222, 4439]
+    Gh = stability.step_matrix(smap, phi0, cols=cols)
+    Gd = stability.step_matrix_device(smap, phi0, cols=cols).cpu().numpy()
+    assert np.allclose(Gh, Gd, rtol=5e-16, atol=0.0)
