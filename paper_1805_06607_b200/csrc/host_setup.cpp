@@ -39,6 +39,7 @@ Options read_options() {
     o.overlap3d = (int)env_or("MRAB_OVERLAP3D", o.overlap3d);
     o.div_wide = (int)env_or("MRAB_DIV_WIDE", o.div_wide);
     o.flux_wide = (int)env_or("MRAB_FLUX_WIDE", o.flux_wide);
+    o.flux_sym = (int)env_or("MRAB_FLUX_SYM", o.flux_sym);
     return o;
 }
 const Options& opts() { return g_opt; }

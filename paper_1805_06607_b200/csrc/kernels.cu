@@ -1413,8 +1413,14 @@ __global__ void __launch_bounds__(NT3, 2) k_rhs3d(DevMesh m, const double* __res
 #define MRAB_F3_MINB 3
 #endif
 namespace w3 {
-constexpr int WX = 16, WY = 8, WZ = 4, WN = WX * WY * WZ, NT = 256, PPT = WN / NT;
-constexpr int REGW = WX * WY * (WZ + 6);                       // largest extended region (z)
+#ifndef MRAB_W3_WY
+#define MRAB_W3_WY 8
+#endif
+constexpr int WX = 16, WY = MRAB_W3_WY, WZ = 4, WN = WX * WY * WZ, NT = 256, PPT = WN / NT;
+constexpr int YSH = WY == 8 ? 3 : 2;                           // log2(WY)
+constexpr int cmax(int a, int b) { return a > b ? a : b; }
+// largest extended region (y or z)
+constexpr int REGW = cmax(WX * WY * (WZ + 6), WX * (WY + 6) * WZ);
 constexpr size_t SMEM = sizeof(double) * 5 * REGW + sizeof(uint16_t) * WN;
 template <int KK>
 struct Reg {
@@ -1423,13 +1429,14 @@ struct Reg {
     static constexpr int KR = (N + NT - 1) / NT;               // region points per thread: 3, 4, 5
     static constexpr int sk = KK == 0 ? 1 : (KK == 1 ? RX : RX * RY);
 };
-constexpr int KRMAX = 5;
+constexpr int KRMAX = (REGW + NT - 1) / NT;
 }  // namespace w3
 
 // tile order: blocks of 2 x 4 x 8 tiles (32^3 points), as tile3_blocked
+template <int TWX, int TWY, int TWZ>
 __device__ __forceinline__ bool tilew_blocked(const DevMesh& m, int& bx, int& by, int& bz) {
-    const int tx = (m.n[0] + w3::WX - 1) / w3::WX, ty = (m.n[1] + w3::WY - 1) / w3::WY,
-              tz = (m.n[2] + w3::WZ - 1) / w3::WZ;
+    const int tx = (m.n[0] + TWX - 1) / TWX, ty = (m.n[1] + TWY - 1) / TWY,
+              tz = (m.n[2] + TWZ - 1) / TWZ;
     const int sx = (tx + 1) / 2, sy = (ty + 3) / 4;
     const int b = blockIdx.x, loc = b & 63, sup = b >> 6;
     bx = (sup % sx) * 2 + (loc & 1);
@@ -1437,12 +1444,21 @@ __device__ __forceinline__ bool tilew_blocked(const DevMesh& m, int& bx, int& by
     bz = (sup / (sx * sy)) * 8 + (loc >> 3);
     return bx < tx && by < ty && bz < tz;
 }
+template <int TWX, int TWY, int TWZ>
 static inline unsigned tilew_blocks(const int* n) {
-    const int tx = (n[0] + w3::WX - 1) / w3::WX, ty = (n[1] + w3::WY - 1) / w3::WY, tz = (n[2] + w3::WZ - 1) / w3::WZ;
+    const int tx = (n[0] + TWX - 1) / TWX, ty = (n[1] + TWY - 1) / TWY, tz = (n[2] + TWZ - 1) / TWZ;
     return (unsigned)(((tx + 1) / 2) * ((ty + 3) / 4) * ((tz + 7) / 8) * 64);
 }
 
-template <int KK>
+// Cartesian meshes store the Cartesian fluxes F_i (unscaled) once: the momentum-flux tensor
+// rho u_i u_j + p delta_ij - tau_ij is symmetric, so 12 values per point instead of the 15
+// contravariant ones (SYM; both wide passes on).  Slot of component c of direction kk:
+// mass 0..2, momentum tensor 3..8 (00 01 02 11 12 22), energy 9..11.
+__host__ __device__ constexpr int sym_slot(int kk, int c) {
+    return c == 0 ? kk : (c == 4 ? 9 + kk : (kk == 0 ? 3 + (c - 1) : (kk == 1 ? (c == 1 ? 4 : 5 + (c - 1)) : (c == 1 ? 5 : (c == 2 ? 7 : 8)))));
+}
+
+template <int KK, bool SYM>
 __device__ __forceinline__ void w3_load(const DevMesh& m, const double* __restrict__ FH, int i0, int j0, int k0,
                                         double (&lq)[w3::KRMAX][5]) {
     using R = w3::Reg<KK>;
@@ -1461,7 +1477,7 @@ __device__ __forceinline__ void w3_load(const DevMesh& m, const double* __restri
         }
         const int64_t q = gg[0] + s1 * gg[1] + s2 * gg[2];
 #pragma unroll
-        for (int c = 0; c < 5; ++c) lq[r][c] = __ldg(FH + (int64_t)(KK * 5 + c) * N + q);
+        for (int c = 0; c < 5; ++c) lq[r][c] = __ldg(FH + (int64_t)(SYM ? sym_slot(KK, c) : KK * 5 + c) * N + q);
     }
 }
 
@@ -1477,23 +1493,24 @@ __device__ __forceinline__ void w3_store(double* __restrict__ fb, const double (
     }
 }
 
+// scale: 1, or (SYM) the constant metric M_kk the stored Cartesian flux is multiplied by
 template <int KK>
 __device__ __forceinline__ void w3_div(const double* __restrict__ fb, const uint16_t* __restrict__ sc,
-                                       double (&racc)[w3::PPT][5]) {
+                                       double (&racc)[w3::PPT][5], double scale) {
     using R = w3::Reg<KK>;
 #pragma unroll
     for (int s = 0; s < w3::PPT; ++s) {
         const int t = threadIdx.x + s * w3::NT;
         const unsigned code = sc[t];
         if (!code) continue;
-        const int x = t & 15, y = (t >> 4) & 7, z = t >> 7;
+        const int x = t & 15, y = (t >> 4) & (w3::WY - 1), z = t >> (4 + w3::YSH);
         const int rr = (x + R::ex) + R::RX * ((y + R::ey) + R::RY * (z + R::ez));
         const int cl = (code >> (4 * KK)) & 15;
         if (cl == CLS_INT) {
 #pragma unroll
             for (int c = 0; c < 5; ++c) {
                 const double* f = fb + c * w3::REGW;
-                racc[s][c] += (2.0 / 3.0) * (f[rr + R::sk] - f[rr - R::sk]) - (1.0 / 12.0) * (f[rr + 2 * R::sk] - f[rr - 2 * R::sk]);
+                racc[s][c] += scale * ((2.0 / 3.0) * (f[rr + R::sk] - f[rr - R::sk]) - (1.0 / 12.0) * (f[rr + 2 * R::sk] - f[rr - 2 * R::sk]));
             }
         } else {
             const int ns = c_nst[cl];
@@ -1505,12 +1522,12 @@ __device__ __forceinline__ void w3_div(const double* __restrict__ fb, const uint
                 for (int c = 0; c < 5; ++c) acc[c] += cf * fb[c * w3::REGW + o];
             }
 #pragma unroll
-            for (int c = 0; c < 5; ++c) racc[s][c] += acc[c];
+            for (int c = 0; c < 5; ++c) racc[s][c] += scale * acc[c];
         }
     }
 }
 
-template <bool VISC, bool CART>
+template <bool VISC, bool CART, bool SYM = false>
 __global__ void __launch_bounds__(w3::NT, MRAB_W3_MINB) k_div3w(DevMesh m, const double* __restrict__ Q,
                                                     const double* __restrict__ FV, Gas g, Epilogue ep,
                                                     const double* __restrict__ FH) {
@@ -1522,16 +1539,16 @@ __global__ void __launch_bounds__(w3::NT, MRAB_W3_MINB) k_div3w(DevMesh m, const
     const int64_t N = m.npts;
     const int64_t s1 = n0, s2 = (int64_t)n0 * n1;
     int tbx, tby, tbz;
-    if (!tilew_blocked(m, tbx, tby, tbz)) return;
+    if (!tilew_blocked<WX, WY, WZ>(m, tbx, tby, tbz)) return;
     const int i0 = tbx * WX, j0 = tby * WY, k0 = tbz * WZ;
     const int tid = threadIdx.x;
     double racc[PPT][NC];
     double lq[KRMAX][NC];
-    w3_load<0>(m, FH, i0, j0, k0, lq);
+    w3_load<0, SYM>(m, FH, i0, j0, k0, lq);
 #pragma unroll
     for (int s = 0; s < PPT; ++s) {
         const int t = tid + s * NT;
-        const int gi = i0 + (t & 15), gj = j0 + ((t >> 4) & 7), gk = k0 + (t >> 7);
+        const int gi = i0 + (t & 15), gj = j0 + ((t >> 4) & (WY - 1)), gk = k0 + (t >> (4 + YSH));
         const bool live = gi < n0 && gj < n1 && gk < n2;
         sc[t] = live ? m.cls[gi + s1 * gj + s2 * gk] : (uint16_t)0;
 #pragma unroll
@@ -1539,13 +1556,13 @@ __global__ void __launch_bounds__(w3::NT, MRAB_W3_MINB) k_div3w(DevMesh m, const
     }
     w3_store<0>(fb, lq);
     __syncthreads();
-    w3_load<1>(m, FH, i0, j0, k0, lq);
-    w3_div<0>(fb, sc, racc);
+    w3_load<1, SYM>(m, FH, i0, j0, k0, lq);
+    w3_div<0>(fb, sc, racc, SYM ? m.cM[0] : 1.0);
     __syncthreads();
     w3_store<1>(fb, lq);
     __syncthreads();
-    w3_load<2>(m, FH, i0, j0, k0, lq);
-    w3_div<1>(fb, sc, racc);
+    w3_load<2, SYM>(m, FH, i0, j0, k0, lq);
+    w3_div<1>(fb, sc, racc, SYM ? m.cM[1] : 1.0);
     __syncthreads();
     w3_store<2>(fb, lq);
     __syncthreads();
@@ -1556,7 +1573,7 @@ __global__ void __launch_bounds__(w3::NT, MRAB_W3_MINB) k_div3w(DevMesh m, const
 #pragma unroll
     for (int s = 0; s < PPT; ++s) {
         const int t = tid + s * NT;
-        const int gi = i0 + (t & 15), gj = j0 + ((t >> 4) & 7), gk = k0 + (t >> 7);
+        const int gi = i0 + (t & 15), gj = j0 + ((t >> 4) & (WY - 1)), gk = k0 + (t >> (4 + YSH));
         livep[s] = gi < n0 && gj < n1 && gk < n2;
         pp[s] = livep[s] ? gi + s1 * gj + s2 * gk : 0;
         const int64_t p = pp[s];
@@ -1594,13 +1611,13 @@ __global__ void __launch_bounds__(w3::NT, MRAB_W3_MINB) k_div3w(DevMesh m, const
                 for (int c = 0; c < NC; ++c) yb[s][c] += ep.csrc[k] * __ldg(ep.src[k] + c * N + p);
         }
     }
-    w3_div<2>(fb, sc, racc);
+    w3_div<2>(fb, sc, racc, SYM ? m.cM[2] : 1.0);
     // ---- SAT and epilogue
 #pragma unroll
     for (int s = 0; s < PPT; ++s) {
         if (!livep[s]) continue;
         const int t = tid + s * NT;
-        const int gi = i0 + (t & 15), gj = j0 + ((t >> 4) & 7), gk = k0 + (t >> 7);
+        const int gi = i0 + (t & 15), gj = j0 + ((t >> 4) & (WY - 1)), gk = k0 + (t >> (4 + YSH));
         const int64_t p = pp[s];
         const unsigned code = sc[t];
         double Rs[NC] = {0, 0, 0, 0, 0};
@@ -1842,7 +1859,7 @@ __device__ __forceinline__ void xyz(int t, int& x, int& y, int& z) {
 }
 }  // namespace f3
 
-template <bool VISC, bool CART>
+template <bool VISC, bool CART, bool SYM = false>
 __global__ void __launch_bounds__(f3::NT, MRAB_F3_MINB) k_flux3w(DevMesh m, const double* __restrict__ Q,
                                                      double* __restrict__ FH, double* __restrict__ FV,
                                                      const uint8_t* __restrict__ fvtile, Gas g) {
@@ -1855,7 +1872,7 @@ __global__ void __launch_bounds__(f3::NT, MRAB_F3_MINB) k_flux3w(DevMesh m, cons
     const int64_t N = m.npts;
     const int64_t s1 = n0, s2 = (int64_t)n0 * n1;
     int tbx, tby, tbz;
-    if (!tilew_blocked(m, tbx, tby, tbz)) return;
+    if (!tilew_blocked<WX, WY, WZ>(m, tbx, tby, tbz)) return;
     const int i0 = tbx * WX, j0 = tby * WY, k0 = tbz * WZ;
     const int tid = threadIdx.x;
     const int per0 = m.periodic[0], per1 = m.periodic[1], per2 = m.periodic[2];
@@ -1917,7 +1934,7 @@ __global__ void __launch_bounds__(f3::NT, MRAB_F3_MINB) k_flux3w(DevMesh m, cons
         const unsigned code = sc[t];
         if (!code) {
 #pragma unroll
-            for (int c = 0; c < 15; ++c) FH[(int64_t)c * N + p] = 0.0;
+            for (int c = 0; c < (SYM ? 12 : 15); ++c) FH[(int64_t)c * N + p] = 0.0;
             continue;
         }
         const double r = rh[t];
@@ -2001,6 +2018,17 @@ __global__ void __launch_bounds__(f3::NT, MRAB_F3_MINB) k_flux3w(DevMesh m, cons
 #pragma unroll
             for (int j = 0; j < 3; ++j) F[i][1 + j] = mi * u[j] + (i == j ? pr : 0.0) - fv[i][j];
             F[i][4] = (E + pr) * u[i] - fv[i][3];
+        }
+        if (SYM) {
+            // the Cartesian fluxes once (the momentum tensor is symmetric): 12 values
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                FH[(int64_t)i * N + p] = F[i][0];
+                FH[(int64_t)(9 + i) * N + p] = F[i][4];
+#pragma unroll
+                for (int j = i; j < 3; ++j) FH[(int64_t)sym_slot(i, 1 + j) * N + p] = F[i][1 + j];
+            }
+            continue;
         }
 #pragma unroll
         for (int kap = 0; kap < 3; ++kap)
@@ -2368,6 +2396,9 @@ static void launch_z3(const DevMesh& m, const double* Q, const Gas& gas, const E
     cudaLaunchKernelEx(&cfg, k_rhs3z<VISC, CART>, m, Q, gas, ep, maps);
 }
 
+// Cartesian meshes: 12-value symmetric flux storage, when both passes run the wide kernels
+static bool sym_storage() { return opts().flux_wide && opts().div_wide && opts().flux_sym; }
+
 void launch_flux3d(const DevMesh& m, const double* Q, const Gas& gas, cudaStream_t st) {
     if (opts().flux_wide) {
         static bool initw = false;
@@ -2376,15 +2407,20 @@ void launch_flux3d(const DevMesh& m, const double* Q, const Gas& gas, cudaStream
             cudaFuncSetAttribute(k_flux3w<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3::SMEM);
             cudaFuncSetAttribute(k_flux3w<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3::SMEM);
             cudaFuncSetAttribute(k_flux3w<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3::SMEM);
+            cudaFuncSetAttribute(k_flux3w<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3::SMEM);
+            cudaFuncSetAttribute(k_flux3w<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f3::SMEM);
             initw = true;
         }
-        const dim3 gw(tilew_blocks(m.n));
+        const dim3 gw(tilew_blocks<f3::WX, f3::WY, f3::WZ>(m.n));
         double* FHw = const_cast<double*>(m.fh);
+        const bool sym = m.cart && sym_storage();
         if (gas.viscous) {
-            if (m.cart) launch_k(k_flux3w<true, true>, gw, dim3(f3::NT), f3::SMEM, st, m, Q, FHw, m.fv, m.fvtile, gas);
+            if (sym) launch_k(k_flux3w<true, true, true>, gw, dim3(f3::NT), f3::SMEM, st, m, Q, FHw, m.fv, m.fvtile, gas);
+            else if (m.cart) launch_k(k_flux3w<true, true>, gw, dim3(f3::NT), f3::SMEM, st, m, Q, FHw, m.fv, m.fvtile, gas);
             else launch_k(k_flux3w<true, false>, gw, dim3(f3::NT), f3::SMEM, st, m, Q, FHw, m.fv, m.fvtile, gas);
         } else {
-            if (m.cart) launch_k(k_flux3w<false, true>, gw, dim3(f3::NT), f3::SMEM, st, m, Q, FHw, m.fv, m.fvtile, gas);
+            if (sym) launch_k(k_flux3w<false, true, true>, gw, dim3(f3::NT), f3::SMEM, st, m, Q, FHw, m.fv, m.fvtile, gas);
+            else if (m.cart) launch_k(k_flux3w<false, true>, gw, dim3(f3::NT), f3::SMEM, st, m, Q, FHw, m.fv, m.fvtile, gas);
             else launch_k(k_flux3w<false, false>, gw, dim3(f3::NT), f3::SMEM, st, m, Q, FHw, m.fv, m.fvtile, gas);
         }
         return;
@@ -2412,10 +2448,15 @@ template <bool VISC, bool CART>
 static void launch_div3w(const DevMesh& m, const double* Q, const Gas& gas, const Epilogue& ep, cudaStream_t st) {
     static bool init = false;
     if (!init) {
-        cudaFuncSetAttribute(k_div3w<VISC, CART>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w3::SMEM);
+        cudaFuncSetAttribute(k_div3w<VISC, CART, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w3::SMEM);
+        cudaFuncSetAttribute(k_div3w<VISC, CART, CART>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w3::SMEM);
         init = true;
     }
-    launch_k(k_div3w<VISC, CART>, dim3(tilew_blocks(m.n)), dim3(w3::NT), w3::SMEM, st, m, Q, (const double*)m.fv, gas, ep, m.fh);
+    const dim3 grid(tilew_blocks<w3::WX, w3::WY, w3::WZ>(m.n));
+    if (CART && sym_storage())
+        launch_k(k_div3w<VISC, CART, CART>, grid, dim3(w3::NT), w3::SMEM, st, m, Q, (const double*)m.fv, gas, ep, m.fh);
+    else
+        launch_k(k_div3w<VISC, CART, false>, grid, dim3(w3::NT), w3::SMEM, st, m, Q, (const double*)m.fv, gas, ep, m.fh);
 }
 
 template <bool VISC, bool CART>

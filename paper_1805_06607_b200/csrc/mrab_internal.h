@@ -36,6 +36,7 @@ struct Options {
     int z3_fused = 0;         // MRAB_3D_FUSED: 3-D RHS in one pass (k_rhs3z) instead of two
     int div_wide = 1;         // MRAB_DIV_WIDE: 3-D pass 2 on 16 x 8 x 4 tiles (k_div3w) instead of 8^3
     int flux_wide = 1;        // MRAB_FLUX_WIDE: 3-D pass 1 on 16 x 8 x 4 tiles (k_flux3w) instead of 8^3
+    int flux_sym = 1;         // MRAB_FLUX_SYM: Cartesian 3-D meshes store 12 symmetric flux values, not 15
     int overlap3d = 0;        // MRAB_OVERLAP3D: 3-D multi-stream task-flow schedule (measured slower
                               // than the serial launch order on one GPU: the large kernels only
                               // share the memory system)

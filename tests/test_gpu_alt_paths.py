@@ -44,6 +44,9 @@ CASES = [
     (5, {"MRAB_3D_FUSED": "1"}),
     (5, {"MRAB_INTERP_BOX": "0"}),
     (4, {"MRAB_DIV_WIDE": "0"}),
+    (4, {"MRAB_FLUX_WIDE": "0"}),
+    (4, {"MRAB_FLUX_SYM": "0"}),
+    (5, {"MRAB_FLUX_WIDE": "0", "MRAB_DIV_WIDE": "0"}),
     (5, {"MRAB_DIV_WIDE": "0"}),
     (5, {"MRAB_OVERLAP3D": "1"}),
     (3, {"MRAB_LEAN": "0"}),
