@@ -1877,11 +1877,13 @@ __global__ void __launch_bounds__(f3::NT, MRAB_F3_MINB) k_flux3w(DevMesh m, cons
     const int tid = threadIdx.x;
     const int per0 = m.periodic[0], per1 = m.periodic[1], per2 = m.periodic[2];
     // F^V is written where the 8^3 flag tiles under this tile ask for it (SAT points, donor stencils)
-    bool wfv = false;
+    // (flag bit 0: donor stencils, every point of the tile; bit 1: SAT points, those only)
+    unsigned wfv = 0;
     if (VISC) {
         const int ntx = (n0 + 7) / 8, nty = (n1 + 7) / 8;
         const int fz = (k0 >> 3), fy = (j0 >> 3), fx = (i0 >> 3);
-        wfv = fvtile[fx + ntx * (fy + nty * fz)] || (fx + 1 < ntx && fvtile[fx + 1 + ntx * (fy + nty * fz)]);
+        wfv = fvtile[fx + ntx * (fy + nty * fz)];
+        if (fx + 1 < ntx) wfv |= fvtile[fx + 1 + ntx * (fy + nty * fz)];
     }
     const int nreg = VISC ? NREG : WN;   // Euler: no gradients, the tile itself suffices
     // ---- region state through registers -> primitives in shared memory (two batches)
@@ -2004,7 +2006,15 @@ __global__ void __launch_bounds__(f3::NT, MRAB_F3_MINB) k_flux3w(DevMesh m, cons
                 }
                 fv[i][3] = e + g.kT * gr[3][i];
             }
-            if (wfv)
+            bool w = (wfv & 1u) != 0;
+            if (!w && (wfv & 2u)) {
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    const int cl = (code >> (4 * k)) & 15;
+                    w = w || cl == CLS_L0 || cl == CLS_R0;
+                }
+            }
+            if (w)
 #pragma unroll
                 for (int i = 0; i < 3; ++i)
 #pragma unroll

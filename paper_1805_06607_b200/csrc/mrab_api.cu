@@ -1798,8 +1798,9 @@ mrab_status mrab_create(const mrab_plan* plan, const double* const* q0, void* d_
                         }
                         if (need) st[(size_t)(i / 8) + tx * ((size_t)(jj / 8) + (size_t)ty * (k / 8))] = 1;
                     }
-            // ... and the donor-stencil tiles (the gathers read F^V there at stepping times)
-            for (size_t t = 0; t < st.size(); ++t) st[t] = st[t] || fl[t];
+            // ... and the donor-stencil tiles (the gathers read F^V there at stepping times):
+            // bit 0 = donor stencils (every point of the tile), bit 1 = SAT points (those only)
+            for (size_t t = 0; t < st.size(); ++t) st[t] = (uint8_t)((fl[t] ? 1 : 0) | (st[t] ? 2 : 0));
             CK(cudaMemcpy(D.fvtile, st.data(), st.size(), cudaMemcpyHostToDevice));
         }
         CK(cudaMemcpy(D.recv_slot, m.recv_slot.data(), N * sizeof(int32_t), cudaMemcpyHostToDevice));
