@@ -109,3 +109,34 @@ def test_nccl_transport_single_rank():
     ref, _ = _run_ranks(p, 1, [0, 0], 3)
     for a, b in zip(got, ref):
         assert np.array_equal(a, b)
+
+
+def test_attach_nccl_binding_world_of_one():
+    """The Python path bench.py --dist takes (torch.distributed NCCL group, unique id drawn on
+    rank 0 and broadcast, mrab_dist_attach on every rank) in a one-rank job."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r"""
+import sys, numpy as np, torch, torch.distributed as dist
+sys.path.insert(0, %r)
+import synth
+from paper_1805_06607_b200 import mrab
+torch.cuda.set_device(0)
+dist.init_process_group("nccl", device_id=torch.device("cuda", 0))
+p = synth.make_config(1, "test")
+plan = mrab.Plan(p)
+owner, load = mrab.partition(plan, dist.get_world_size())
+ctx = mrab.Context(plan, p.q0)
+ctx.attach_nccl(dist, owner)
+ctx.step(p.history_m - 1 + 2)
+q = ctx.get_state(0)[0]
+assert np.all(np.isfinite(q))
+print("ok", owner, ctx.dist_stats())
+ctx.close()
+dist.destroy_process_group()
+""" % root
+    env = dict(os.environ, RANK="0", LOCAL_RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1", MASTER_PORT="29533")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok [0, 0]" in r.stdout, (r.stdout[-2000:], r.stderr[-3000:])
