@@ -16,7 +16,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [*(["-DMRAB_Z3_PROF"] if os.environ.get("MRAB_Z3_PROF") else []),
          *([f"-DMRAB_W3_MINB={os.environ['MRAB_W3_MINB']}"] if os.environ.get("MRAB_W3_MINB") else []),
          *([f"-DMRAB_F3_MINB={os.environ['MRAB_F3_MINB']}"] if os.environ.get("MRAB_F3_MINB") else []),
-         *([f"-DMRAB_W3_WY={os.environ['MRAB_W3_WY']}"] if os.environ.get("MRAB_W3_WY") else []), "-O3", "-std=c++17", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
+         *([f"-DMRAB_W3_WY={os.environ['MRAB_W3_WY']}"] if os.environ.get("MRAB_W3_WY") else []),
+         *([f"-DMRAB_W3_WX={os.environ['MRAB_W3_WX']}"] if os.environ.get("MRAB_W3_WX") else []), "-O3", "-std=c++17", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
          "-Xcompiler", "-fPIC,-fopenmp,-O3", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 
 

@@ -1416,8 +1416,12 @@ namespace w3 {
 #ifndef MRAB_W3_WY
 #define MRAB_W3_WY 8
 #endif
-constexpr int WX = 16, WY = MRAB_W3_WY, WZ = 4, WN = WX * WY * WZ, NT = 256, PPT = WN / NT;
-constexpr int YSH = WY == 8 ? 3 : 2;                           // log2(WY)
+#ifndef MRAB_W3_WX
+#define MRAB_W3_WX 16
+#endif
+constexpr int WX = MRAB_W3_WX, WY = MRAB_W3_WY, WZ = 4, WN = WX * WY * WZ, NT = 256, PPT = WN / NT;
+constexpr int XSH = WX == 32 ? 5 : 4;                          // log2(WX)
+constexpr int YSH = WY == 8 ? 3 : (WY == 4 ? 2 : 1);           // log2(WY)
 constexpr int cmax(int a, int b) { return a > b ? a : b; }
 // largest extended region (y or z)
 constexpr int REGW = cmax(WX * WY * (WZ + 6), WX * (WY + 6) * WZ);
@@ -1503,7 +1507,7 @@ __device__ __forceinline__ void w3_div(const double* __restrict__ fb, const uint
         const int t = threadIdx.x + s * w3::NT;
         const unsigned code = sc[t];
         if (!code) continue;
-        const int x = t & 15, y = (t >> 4) & (w3::WY - 1), z = t >> (4 + w3::YSH);
+        const int x = t & (w3::WX - 1), y = (t >> w3::XSH) & (w3::WY - 1), z = t >> (w3::XSH + w3::YSH);
         const int rr = (x + R::ex) + R::RX * ((y + R::ey) + R::RY * (z + R::ez));
         const int cl = (code >> (4 * KK)) & 15;
         if (cl == CLS_INT) {
@@ -1548,7 +1552,7 @@ __global__ void __launch_bounds__(w3::NT, MRAB_W3_MINB) k_div3w(DevMesh m, const
 #pragma unroll
     for (int s = 0; s < PPT; ++s) {
         const int t = tid + s * NT;
-        const int gi = i0 + (t & 15), gj = j0 + ((t >> 4) & (WY - 1)), gk = k0 + (t >> (4 + YSH));
+        const int gi = i0 + (t & (WX - 1)), gj = j0 + ((t >> XSH) & (WY - 1)), gk = k0 + (t >> (XSH + YSH));
         const bool live = gi < n0 && gj < n1 && gk < n2;
         sc[t] = live ? m.cls[gi + s1 * gj + s2 * gk] : (uint16_t)0;
 #pragma unroll
@@ -1573,7 +1577,7 @@ __global__ void __launch_bounds__(w3::NT, MRAB_W3_MINB) k_div3w(DevMesh m, const
 #pragma unroll
     for (int s = 0; s < PPT; ++s) {
         const int t = tid + s * NT;
-        const int gi = i0 + (t & 15), gj = j0 + ((t >> 4) & (WY - 1)), gk = k0 + (t >> (4 + YSH));
+        const int gi = i0 + (t & (WX - 1)), gj = j0 + ((t >> XSH) & (WY - 1)), gk = k0 + (t >> (XSH + YSH));
         livep[s] = gi < n0 && gj < n1 && gk < n2;
         pp[s] = livep[s] ? gi + s1 * gj + s2 * gk : 0;
         const int64_t p = pp[s];
@@ -1617,7 +1621,7 @@ __global__ void __launch_bounds__(w3::NT, MRAB_W3_MINB) k_div3w(DevMesh m, const
     for (int s = 0; s < PPT; ++s) {
         if (!livep[s]) continue;
         const int t = tid + s * NT;
-        const int gi = i0 + (t & 15), gj = j0 + ((t >> 4) & (WY - 1)), gk = k0 + (t >> (4 + YSH));
+        const int gi = i0 + (t & (WX - 1)), gj = j0 + ((t >> XSH) & (WY - 1)), gk = k0 + (t >> (XSH + YSH));
         const int64_t p = pp[s];
         const unsigned code = sc[t];
         double Rs[NC] = {0, 0, 0, 0, 0};
