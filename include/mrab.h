@@ -190,6 +190,13 @@ mrab_status mrab_step(mrab_ctx* ctx, int n_macro);
  * INSUFFICIENT_HISTORY (called before the m-1 bootstrap macro steps), CUDA. */
 mrab_status mrab_step_h(mrab_ctx* ctx, int n_macro, double H);
 
+/* CFL-driven stepping: n_macro macro steps, each of size H = cfl * S_max * min_g dt_g / s_g with
+ * dt_g from the device estimate (mrab_dt) at the states the step starts from (eq:ts, P:620-643;
+ * h_i = H_i / SR), then mrab_step_h(1, H).  One 8-byte-per-mesh read back per step.
+ * *H_last (may be NULL) receives the last step taken.  Errors: as mrab_dt and mrab_step_h;
+ * NONFINITE if the estimate is not positive and finite. */
+mrab_status mrab_step_cfl(mrab_ctx* ctx, int n_macro, double cfl, double* H_last);
+
 /* MRAB evaluation order ("The order in which we evaluate and advance the solution
  * components" and "whether or not to re-extrapolate the slow state"; the paper prints steps for
  * fastest-first only, reading R-SF of DESIGN.md §2 for the other two).  mrab_step_scheme with

@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -2154,6 +2155,27 @@ mrab_status mrab_dist_stats(mrab_ctx* c, int64_t* bytes_sent, int64_t* messages)
     if (!c || !c->dist) return fail(MRAB_E_INVALID, "not a multi-GPU context");
     if (bytes_sent) *bytes_sent = c->dist->bytes_sent;
     if (messages) *messages = c->dist->messages;
+    return MRAB_OK;
+}
+
+mrab_status mrab_step_cfl(mrab_ctx* c, int n_macro, double cfl, double* H_last) {
+    if (!c || n_macro < 0 || !(cfl > 0.0)) return fail(MRAB_E_INVALID, "bad ctx / n_macro / cfl");
+    const Plan& P = *c->P;
+    const int G = (int)P.meshes.size();
+    std::vector<double> dt(G);
+    for (int it = 0; it < n_macro; ++it) {
+        mrab_status st = mrab_dt(c, dt.data());
+        if (st != MRAB_OK) return st;
+        double H = 0.0;
+        for (int g = 0; g < G; ++g) {
+            const double Hg = cfl * P.S * dt[g] / P.meshes[g].s;
+            H = g == 0 ? Hg : std::min(H, Hg);
+        }
+        if (!(H > 0.0) || !std::isfinite(H)) return fail(MRAB_E_NONFINITE, "timestep estimate is not a positive finite number");
+        st = mrab_step_h(c, 1, H);
+        if (st != MRAB_OK) return st;
+        if (H_last) *H_last = H;
+    }
     return MRAB_OK;
 }
 

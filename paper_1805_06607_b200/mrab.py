@@ -90,6 +90,7 @@ def lib():
         L.mrab_dist_attach.argtypes = [vp, C.c_int, vp, C.c_int, C.c_int, C.POINTER(C.c_int)]
         L.mrab_dist_stats.argtypes = [vp, i64p, i64p]
         L.mrab_dt.argtypes = [vp, dp]
+        L.mrab_step_cfl.argtypes = [vp, C.c_int, C.c_double, dp]
         L.mrab_get_state.argtypes = [vp, C.c_int, vp, dp]
         L.mrab_set_state.argtypes = [vp, C.c_int, vp]
         L.mrab_get_history.argtypes = [vp, C.c_int, C.c_int, vp]
@@ -105,7 +106,7 @@ def lib():
                      "mrab_step", "mrab_get_state", "mrab_set_state", "mrab_rhs",
                      "mrab_get_history", "mrab_set_history", "mrab_get_counters",
                      "mrab_launches_per_macro_step", "mrab_time_kernel", "mrab_step_h", "mrab_dt", "mrab_step_scheme", "mrab_rk_step", "mrab_partition", "mrab_dist_unique_id", "mrab_dist_attach",
-                     "mrab_dist_stats"):
+                     "mrab_dist_stats", "mrab_step_cfl"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -117,7 +118,7 @@ EXPORTED = ["mrab_ab_weights", "mrab_plan_create", "mrab_plan_destroy", "mrab_pl
             "mrab_rhs", "mrab_get_counters", "mrab_launches_per_macro_step", "mrab_time_kernel",
             "mrab_set_trace", "mrab_last_error", "mrab_get_history", "mrab_set_history",
             "mrab_overset_build", "mrab_free", "mrab_plan_get_face_flags", "mrab_step_h", "mrab_dt", "mrab_step_scheme", "mrab_rk_step", "mrab_partition", "mrab_dist_unique_id", "mrab_dist_attach",
-            "mrab_dist_stats"]
+            "mrab_dist_stats", "mrab_step_cfl"]
 
 
 def _check(st):
@@ -370,6 +371,13 @@ class Context:
     def step_h(self, H, n_macro=1):
         """n_macro MRAB macro steps of size H (variable macro step, mrab_step_h)."""
         _check(lib().mrab_step_h(self.h, int(n_macro), float(H)))
+
+    def step_cfl(self, cfl, n_macro=1):
+        """n_macro macro steps at H = cfl * S * min_g dt_g / s_g from the device estimate
+        (mrab_step_cfl); returns the last H."""
+        H = C.c_double()
+        _check(lib().mrab_step_cfl(self.h, int(n_macro), float(cfl), C.byref(H)))
+        return H.value
 
     def dt(self):
         """Per-mesh minimum of the eq:ts stable timestep at the current states (mrab_dt)."""

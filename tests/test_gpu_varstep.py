@@ -106,6 +106,25 @@ def test_cfl_driven_run():
     ctx.close()
 
 
+def test_step_cfl_matches_manual_loop():
+    """mrab_step_cfl = mrab_dt + the H formula + mrab_step_h, bit for bit."""
+    p = synth.make_config(1, "test")
+    S = p.s_max
+    a = mrab.Context(mrab.Plan(p), p.q0)
+    b = mrab.Context(mrab.Plan(p), p.q0)
+    a.step(p.history_m - 1)
+    b.step(p.history_m - 1)
+    for _ in range(3):
+        H = 0.4 * S * min(d / m.step_multiple for d, m in zip(a.dt(), p.meshes))
+        a.step_h(H)
+    Hb = b.step_cfl(0.4, 3)
+    assert Hb == H
+    for g in range(2):
+        assert np.array_equal(a.get_state(g)[0], b.get_state(g)[0])
+    a.close()
+    b.close()
+
+
 def test_step_h_errors():
     p = synth.make_config(1, "test")
     ctx = mrab.Context(mrab.Plan(p), p.q0)
