@@ -30,11 +30,14 @@ def rho_est(smap, phi):
     a, _ = stability.spectral_radius_arnoldi(smap, phi, k=K, restarts=2)
     return max(a, g)
 SCALE = os.environ.get("SCALE", "full")
+CFG = int(os.environ.get("CFG", "1"))                 # 1: Euler vortex pair; 2: viscous curvilinear pair
+TOL = float(os.environ.get("TOL", "1e-4"))            # bisection tolerance (1e-4)
+LO = float(os.environ.get("LO", "1e-3"))
 K = int(os.environ.get("ARNOLDI_K", "70"))
 
 
 def problem(order_n, history_m, sr):
-    p = synth.make_config(1, SCALE, order_n=order_n, history_m=history_m, sr=sr)
+    p = synth.make_config(CFG, SCALE, order_n=order_n, history_m=history_m, sr=sr)
     # steady base state: the far-field state everywhere
     q = [np.broadcast_to(np.asarray(p.q_inf).reshape((-1,) + (1,) * p.dim), x.shape).copy() for x in p.q0]
     p.q0 = q
@@ -77,16 +80,16 @@ def main():
     srs = [int(x) for x in os.environ.get("SRS", "1,2,3,4,5,6,8").split(",")]
     hi = float(os.environ.get("HI", "0.6"))
     t0 = time.time()
-    out = {"problem": f"config 1 ({SCALE}), Euler, about the uniform free stream", "eps": stability.EPS,
-           "stable_if_rho_le": ONE, "rho": f"max(converged Ritz value of restarted Arnoldi k = {K}, power-iteration growth over {ITERS} steps)", "bisection_tol": 1e-4}
-    dt_rk4 = stability.max_stable(rho_rk4, 1e-3, hi, tol=1e-4, one=ONE)
+    out = {"problem": f"config {CFG} ({SCALE}), about the uniform free stream", "eps": stability.EPS,
+           "stable_if_rho_le": ONE, "rho": f"max(converged Ritz value of restarted Arnoldi k = {K}, power-iteration growth over {ITERS} steps)", "bisection_tol": TOL}
+    dt_rk4 = stability.max_stable(rho_rk4, LO, hi, tol=TOL, one=ONE)
     out["rk4"] = dt_rk4
     rows = {}
     for name, (n, m) in (("AB3", (3, 3)), ("AB34", (3, 4))):
         base = None
         rows[name] = []
         for sr in srs:
-            dt = stability.max_stable(lambda H: rho_mrab(H, n, m, sr), 1e-3, hi, tol=1e-4, one=ONE)
+            dt = stability.max_stable(lambda H: rho_mrab(H, n, m, sr), LO, hi, tol=TOL, one=ONE)
             if sr == 1:
                 base = dt
             rows[name].append({"sr": sr, "dt": dt, "r_rk4": dt / dt_rk4, "r_srab": dt / base,
@@ -96,12 +99,12 @@ def main():
     out["seconds"] = time.time() - t0
     print("| Int. | SR | dt (AB3) | r_RK4 | r_SRAB | % | dt (AB34) | r_RK4 | r_SRAB | % |")
     print("|---|---|---|---|---|---|---|---|---|---|")
-    print(f"| RK4 | | {dt_rk4:.4f} | 1.000 | {dt_rk4 / rows['AB3'][0]['dt']:.2f} | | {dt_rk4:.4f} | 1.000 | "
+    print(f"| RK4 | | {dt_rk4:.5f} | 1.000 | {dt_rk4 / rows['AB3'][0]['dt']:.2f} | | {dt_rk4:.5f} | 1.000 | "
           f"{dt_rk4 / rows['AB34'][0]['dt']:.2f} | |")
     for a, b in zip(rows["AB3"], rows["AB34"]):
         nm = "SRAB" if a["sr"] == 1 else "MRAB"
-        print(f"| {nm} | {a['sr']} | {a['dt']:.4f} | {a['r_rk4']:.3f} | {a['r_srab']:.2f} | {a['pct']:.1f} | "
-              f"{b['dt']:.4f} | {b['r_rk4']:.3f} | {b['r_srab']:.2f} | {b['pct']:.1f} |")
+        print(f"| {nm} | {a['sr']} | {a['dt']:.5f} | {a['r_rk4']:.3f} | {a['r_srab']:.2f} | {a['pct']:.1f} | "
+              f"{b['dt']:.5f} | {b['r_rk4']:.3f} | {b['r_srab']:.2f} | {b['pct']:.1f} |")
     print(json.dumps(out))
 
 
