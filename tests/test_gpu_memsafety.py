@@ -62,4 +62,23 @@ def test_guard_bands_and_poisoned_workspace(cid, kw):
     orc = timeint.MRAB(p)
     orc.run(2)
     assert_states(gpu, orc.base, p.gamma)
+    # round-2 entry points under the same bands: timestep kernel, variable step (tile-list
+    # donor preparation), and -- two-rate problems -- a slowest-first context
+    dts = ctx.dt()
+    assert all(np.isfinite(d) and d > 0 for d in dts)
+    ctx.step_h(0.9 * p.s_max * p.h)
+    orc.macro_step_var(0.9 * p.s_max * p.h)
+    torch.cuda.synchronize()
+    assert bool(torch.all(lo == 0xFF)) and bool(torch.all(hi == 0xFF)), "write outside the workspace"
+    assert_states([ctx.get_state(g)[0] for g in range(len(p.meshes))], orc.base, p.gamma)
     ctx.close()
+    if len({m.step_multiple for m in p.meshes}) == 2 and min(m.step_multiple for m in p.meshes) == 1:
+        buf.fill_(0xFF)
+        ctx = mrab.Context(plan, p.q0, workspace=ws)
+        ctx.step(p.history_m - 1 + 2, scheme="slowest_first_reextrap")
+        torch.cuda.synchronize()
+        assert bool(torch.all(buf[:GUARD] == 0xFF)) and bool(torch.all(buf[GUARD + off + nbytes:] == 0xFF))
+        o2 = timeint.MRAB(p)
+        o2.run(2, scheme="slowest_first_reextrap")
+        assert_states([ctx.get_state(g)[0] for g in range(len(p.meshes))], o2.base, p.gamma)
+        ctx.close()
