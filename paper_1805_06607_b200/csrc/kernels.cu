@@ -2156,14 +2156,15 @@ __global__ void __launch_bounds__(128) k_interp3b(RecvList rl, DonorSet ds) {
     constexpr int NC = 5, NF = 12, NV = NC + (VISC ? NF : 0);
     extern __shared__ __align__(16) double bx[];   // [NV][IBOXN]
     const int* gi6 = rl.ginfo + 6 * blockIdx.x;
-    const int start = gi6[0], count = gi6[1], dm = gi6[2];
+    const int start = gi6[0], count = gi6[1] & 255, dm = gi6[2];
+    const int ex = (gi6[1] >> 8) & 7, ey = (gi6[1] >> 12) & 7, ez = (gi6[1] >> 16) & 7;   // 4..7
     const int ox = gi6[3], oy = gi6[4], oz = gi6[5];
     const int n0 = ds.n[dm][0], n1 = ds.n[dm][1], n2 = ds.n[dm][2];
     const int64_t N = ds.npts[dm];
     const double* __restrict__ S = ds.state[dm];
     const double* __restrict__ F = ds.fv[dm];
-    for (int t = threadIdx.x; t < IBOXN; t += blockDim.x) {
-        const int x = t % IBOX, y = (t / IBOX) % IBOX, z = t / (IBOX * IBOX);
+    for (int t = threadIdx.x; t < ex * ey * ez; t += blockDim.x) {
+        const int x = t % ex, y = (t / ex) % ey, z = t / (ex * ey);
         int i = ox + x, j = oy + y, k = oz + z;
         // the box may cross a periodic seam (bases are wrapped) or run past a face: wrap, clamp
         if (i >= n0) i -= n0;
@@ -2201,7 +2202,7 @@ __global__ void __launch_bounds__(128) k_interp3b(RecvList rl, DonorSet ds) {
             for (int a = 0; a < 16; ++a) {
                 const int a1 = a & 3, a2 = a >> 2;
                 const double W = w0 * w[4 + a1] * w[8 + a2];
-                const int e = (lx + a0) + IBOX * ((ly + a1) + IBOX * (lz + a2));
+                const int e = (lx + a0) + ex * ((ly + a1) + ey * (lz + a2));
 #pragma unroll
                 for (int c = 0; c < NV; ++c) acc[c] += W * bx[c * IBOXN + e];
             }
@@ -2244,8 +2245,19 @@ std::vector<int32_t> interp3_groups(int64_t R, const int32_t* donor, const int32
         while (j < R && j - i < 64 && keys[j].d == keys[i].d && keys[j].x == keys[i].x &&
                keys[j].y == keys[i].y && keys[j].z == keys[i].z)
             ++j;
-        info.insert(info.end(), {(int32_t)i, (int32_t)(j - i), keys[i].d, 4 * keys[i].x, 4 * keys[i].y,
-                                 4 * keys[i].z});
+        // the staged box: from the smallest stencil base of the group, as large as its stencils
+        // reach (4..7 per axis; a sheet of face receivers uses 4 or 5 along its normal).  The
+        // extents ride in the count word (bits 8-10, 12-14, 16-18).
+        int lo[3] = {1 << 30, 1 << 30, 1 << 30}, hi[3] = {0, 0, 0};
+        for (int64_t k = i; k < j; ++k)
+            for (int a = 0; a < 3; ++a) {
+                const int b = base[3 * keys[k].r + a];
+                lo[a] = std::min(lo[a], b);
+                hi[a] = std::max(hi[a], b);
+            }
+        const int32_t cnt = (int32_t)(j - i) | ((hi[0] - lo[0] + 4) << 8) | ((hi[1] - lo[1] + 4) << 12) |
+                            ((hi[2] - lo[2] + 4) << 16);
+        info.insert(info.end(), {(int32_t)i, cnt, keys[i].d, lo[0], lo[1], lo[2]});
         for (int64_t k = i; k < j; ++k) order[k] = (int32_t)keys[k].r;
         i = j;
     }
