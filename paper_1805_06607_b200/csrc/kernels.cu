@@ -2153,7 +2153,11 @@ __global__ void __launch_bounds__(128) k_interp3q(RecvList rl, DonorSet ds) {
 constexpr int IBOX = 7, IBOXN = IBOX * IBOX * IBOX;
 template <bool VISC>
 __global__ void __launch_bounds__(128) k_interp3b(RecvList rl, DonorSet ds) {
-    constexpr int NC = 5, NF = 12, NV = NC + (VISC ? NF : 0);
+    // the Cartesian viscous fluxes F^V_i = (tau_i0, tau_i1, tau_i2, e_i) hold a symmetric tau:
+    // 9 distinct values are staged and interpolated, the 12 fvhat entries filled from them
+    constexpr int NC = 5, NF = 12, NU = 9, NV = NC + (VISC ? NU : 0);
+    constexpr int USLOT[9] = {0, 1, 2, 3, 5, 6, 7, 10, 11};          // (0,0..3), (1,1..3), (2,2..3)
+    constexpr int FROM[12] = {0, 1, 2, 3, 1, 4, 5, 6, 2, 5, 7, 8};   // fv slot i*4+j -> staged value
     extern __shared__ __align__(16) double bx[];   // [NV][IBOXN]
     const int* gi6 = rl.ginfo + 6 * blockIdx.x;
     const int start = gi6[0], count = gi6[1] & 255, dm = gi6[2];
@@ -2176,7 +2180,7 @@ __global__ void __launch_bounds__(128) k_interp3b(RecvList rl, DonorSet ds) {
         const int64_t q = i + (int64_t)n0 * (j + (int64_t)n1 * k);
 #pragma unroll
         for (int c = 0; c < NV; ++c) {
-            const double* src = c < NC ? S + c * N + q : F + (int64_t)(c - NC) * N + q;
+            const double* src = c < NC ? S + c * N + q : F + (int64_t)USLOT[c < NC ? 0 : c - NC] * N + q;
             const unsigned sa = (unsigned)__cvta_generic_to_shared(bx + c * IBOXN + t);
             asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(src));
         }
@@ -2217,7 +2221,7 @@ __global__ void __launch_bounds__(128) k_interp3b(RecvList rl, DonorSet ds) {
             for (int c = 0; c < NC; ++c) rl.qhat[c * rl.n + r] = acc[c];
             if (VISC)
 #pragma unroll
-                for (int c = 0; c < NF; ++c) rl.fvhat[c * rl.n + r] = acc[NC + c];
+                for (int c = 0; c < NF; ++c) rl.fvhat[c * rl.n + r] = acc[NC + FROM[c]];
         }
     }
 }
@@ -2586,7 +2590,7 @@ void launch_combine(int nc, const DevMesh& m, const Box& box, const double* base
 void launch_interp(int viscous, const RecvList& rl, const DonorSet& ds, cudaStream_t st) {
     if (rl.n <= 0) return;
     if (rl.ginfo && rl.ngroups > 0) {
-        const size_t bytes = sizeof(double) * (viscous ? 17 : 5) * IBOXN;
+        const size_t bytes = sizeof(double) * (viscous ? 14 : 5) * IBOXN;
         static bool init = false;
         if (!init) {
             cudaFuncSetAttribute(k_interp3b<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double) * 17 * IBOXN));
