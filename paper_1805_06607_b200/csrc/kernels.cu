@@ -1144,9 +1144,9 @@ static inline unsigned tile3_blocks(const int* n) {
     return (unsigned)(((tx + 3) / 4) * ((ty + 3) / 4) * ((tz + 3) / 4) * 64);
 }
 
-// PRE: the contravariant fluxes come precomputed from k_flux3d (two-pass mode): the region
-// loads read Fhat_kappa (5 values) instead of Q and F^V (9) and no flux is formed here
-template <bool VISC, bool CART, bool PRE = false>
+// The contravariant fluxes come precomputed from the flux pass (PRE is always true: the
+// one-pass-per-direction variant that formed them here from Q and F^V was removed in round 2)
+template <bool VISC, bool CART, bool PRE = true>
 __global__ void __launch_bounds__(NT3, 2) k_rhs3d(DevMesh m, const double* __restrict__ Q,
                                                  const double* __restrict__ FV, Gas g, Epilogue ep,
                                                  const double* __restrict__ FH = nullptr) {
@@ -1199,102 +1199,26 @@ __global__ void __launch_bounds__(NT3, 2) k_rhs3d(DevMesh m, const double* __res
             for (int c = 0; c < NC; ++c) dst[r][c] = __ldg(FH + (int64_t)(kk * NC + c) * N + q);
         }
     };
-    if (PRE) pre_load(0, lqp[0]);
+    pre_load(0, lqp[0]);
     // direction loop unrolled: region extents are compile-time, so the index arithmetic is
     // constant division (it was runtime integer division, a quarter of all instructions)
 #pragma unroll
     for (int kap = 0; kap < 3; ++kap) {
         const int ex = kap == 0 ? 3 : 0, ey = kap == 1 ? 3 : 0, ez = kap == 2 ? 3 : 0;
         const int RX = T3X + 2 * ex, RY = T3Y + 2 * ey;
-        // ---- loads of all region points of this thread (independent, in flight together)
-        double lq[KR3][NC], lv[KR3][4], lm[KR3][3];
-#pragma unroll
-        for (int r = 0; r < KR3; ++r) {
-            if (PRE) break;
-            const int t = tid + r * NT3;
-            const int x = t % RX, y = (t / RX) % RY, z = t / (RX * RY);
-            int gg[3] = {i0 - ex + x, j0 - ey + y, k0 - ez + z};
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                const int n = m.n[k];
-                if (gg[k] < 0) gg[k] = m.periodic[k] ? gg[k] + n : 0;
-                else if (gg[k] >= n) gg[k] = m.periodic[k] ? gg[k] - n : n - 1;
-            }
-            const int64_t q = gg[0] + s1 * gg[1] + s2 * gg[2];
-#pragma unroll
-            for (int c = 0; c < NC; ++c) lq[r][c] = __ldg(Q + c * N + q);
-            if (VISC) {
-                if (CART) {
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) lv[r][j] = __ldg(FV + (int64_t)(kap * 4 + j) * N + q);
-                }
-            }
-            if (!CART) {
-#pragma unroll
-                for (int i = 0; i < 3; ++i) lm[r][i] = __ldg(m.M + (kap * 3 + i) * N + q);
-            }
-            (void)lv;
-            (void)lm;
-            if (!CART && VISC) {
-                // curvilinear: F^V of every Cartesian direction is needed; fetch into lv on use
-            }
-            // stash the clamped index for the curvilinear viscous path
-            lv[r][0] = CART ? lv[r][0] : __longlong_as_double((long long)q);
-        }
-        // ---- contravariant fluxes -> shared memory
+        // ---- the prefetched contravariant fluxes of this direction -> shared memory
 #pragma unroll
         for (int r = 0; r < KR3; ++r) {
             const int t = tid + r * NT3;
             if (t >= (T3X + 2 * ex) * (T3Y + 2 * ey) * (T3Z + 2 * ez)) break;
-            if (PRE) {
 #pragma unroll
-                for (int c = 0; c < NC; ++c) fb[c * REG3 + t] = lqp[kap & 1][r][c];
-                continue;
-            }
-            const double rho = lq[r][0];
-            const double ir = rcp64(rho);
-            const double u[3] = {lq[r][1] * ir, lq[r][2] * ir, lq[r][3] * ir};
-            const double E = lq[r][4];
-            const double pr = g.gm1 * (E - 0.5 * (lq[r][1] * u[0] + lq[r][2] * u[1] + lq[r][3] * u[2]));
-            double fh[NC] = {0, 0, 0, 0, 0};
-            if (CART) {
-                const int i = kap;
-                double f[NC];
-                f[0] = lq[r][1 + i];
-#pragma unroll
-                for (int j = 0; j < 3; ++j) f[1 + j] = lq[r][1 + i] * u[j] + (i == j ? pr : 0.0);
-                f[4] = (E + pr) * u[i];
-                if (VISC) {
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) f[1 + j] -= lv[r][j];
-                }
-#pragma unroll
-                for (int c = 0; c < NC; ++c) fh[c] = m.cM[kap] * f[c];
-            } else {
-                const int64_t q = (int64_t)__double_as_longlong(lv[r][0]);
-#pragma unroll
-                for (int i = 0; i < 3; ++i) {
-                    double f[NC];
-                    f[0] = lq[r][1 + i];
-#pragma unroll
-                    for (int j = 0; j < 3; ++j) f[1 + j] = lq[r][1 + i] * u[j] + (i == j ? pr : 0.0);
-                    f[4] = (E + pr) * u[i];
-                    if (VISC) {
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) f[1 + j] -= __ldg(FV + (int64_t)(i * 4 + j) * N + q);
-                    }
-#pragma unroll
-                    for (int c = 0; c < NC; ++c) fh[c] += lm[r][i] * f[c];
-                }
-            }
-#pragma unroll
-            for (int c = 0; c < NC; ++c) fb[c * REG3 + t] = fh[c];
+            for (int c = 0; c < NC; ++c) fb[c * REG3 + t] = lqp[kap & 1][r][c];
         }
         if (kap == 0)
 #pragma unroll
             for (int s = 0; s < PPT3; ++s) sc[tid + s * NT3] = (uint16_t)clsv[s];
         __syncthreads();
-        if (PRE && kap < 2) pre_load(kap + 1, lqp[(kap + 1) & 1]);
+        if (kap < 2) pre_load(kap + 1, lqp[(kap + 1) & 1]);
         // ---- D_kappa of the staged fluxes at the tile points
         const int sk = kap == 0 ? 1 : (kap == 1 ? RX : RX * RY);
 #pragma unroll
