@@ -1496,6 +1496,7 @@ __global__ void __launch_bounds__(w3::NT, MRAB_W3_MINB) k_div3w(DevMesh m, const
     __syncthreads();
     // the epilogue inputs of this thread's points, in flight during the last stencil
     double yb[PPT][NC];
+    double Jv[PPT];
     int64_t pp[PPT];
     bool livep[PPT];
 #pragma unroll
@@ -1505,6 +1506,7 @@ __global__ void __launch_bounds__(w3::NT, MRAB_W3_MINB) k_div3w(DevMesh m, const
         livep[s] = gi < n0 && gj < n1 && gk < n2;
         pp[s] = livep[s] ? gi + s1 * gj + s2 * gk : 0;
         const int64_t p = pp[s];
+        Jv[s] = CART ? m.cJ : __ldg(m.J + p);   // (with the epilogue loads, not after the last stencil)
         if (ep.y_out && ep.nsrc == 2) {
             double v[3][NC];
 #pragma unroll
@@ -1550,7 +1552,7 @@ __global__ void __launch_bounds__(w3::NT, MRAB_W3_MINB) k_div3w(DevMesh m, const
         const unsigned code = sc[t];
         double Rs[NC] = {0, 0, 0, 0, 0};
         if (code) {
-            const double Jp = CART ? m.cJ : __ldg(m.J + p);
+            const double Jp = Jv[s];
 #pragma unroll
             for (int c = 0; c < NC; ++c) Rs[c] = -Jp * racc[s][c];
             bool sat = false;
