@@ -1754,27 +1754,23 @@ __global__ void __launch_bounds__(NT3, 2) k_flux3d(DevMesh m, const double* __re
 // ------------------------------------------------------------------------------------
 namespace f3 {
 constexpr int WX = 16, WY = 8, WZ = 4, WN = 512, NT = 256, PPT = 2;
-constexpr int OXM = WN, OXP = OXM + 96, OYM = OXP + 96, OYP = OYM + 192, OZM = OYP + 192, OZP = OZM + 384;
+// rows of the tile carry their x halo (22 = 3 + 16 + 3 doubles per row): an x stencil then reads
+// one contiguous run per row, free of bank conflicts (split x slabs cost 22 % replays)
+constexpr int RW = WX + 6, NCORE = RW * WY * WZ;                 // 704
+constexpr int OYM = NCORE, OYP = OYM + 192, OZM = OYP + 192, OZP = OZM + 384;
 constexpr int NREG = OZP + 384;                                   // 1856
 constexpr int KR = (NREG + NT - 1) / NT;                          // 8 (7.25)
 constexpr size_t SMEM = sizeof(double) * (4 * NREG + WN) + sizeof(uint16_t) * WN;
 __device__ __forceinline__ int idx(int x, int y, int z) {
-    if (x < 0) return OXM + (x + 3) + 3 * (y + 8 * z);
-    if (x >= WX) return OXP + (x - WX) + 3 * (y + 8 * z);
     if (y < 0) return OYM + x + 16 * ((y + 3) + 3 * z);
     if (y >= WY) return OYP + x + 16 * ((y - WY) + 3 * z);
     if (z < 0) return OZM + x + 16 * y + 128 * (z + 3);
     if (z >= WZ) return OZP + x + 16 * y + 128 * (z - WZ);
-    return x + 16 * y + 128 * z;
+    return (x + 3) + RW * (y + WY * z);
 }
 __device__ __forceinline__ void xyz(int t, int& x, int& y, int& z) {
-    if (t < WN) {
-        x = t & 15; y = (t >> 4) & 7; z = t >> 7;
-    } else if (t < OYM) {
-        const int w = t < OXP ? t - OXM : t - OXP;
-        x = (t < OXP ? -3 : WX) + w % 3;
-        y = (w / 3) & 7;
-        z = w / 24;
+    if (t < NCORE) {
+        x = t % RW - 3; y = (t / RW) & 7; z = t / (RW * WY);
     } else if (t < OZM) {
         const int w = t < OYP ? t - OYM : t - OYP;
         x = w & 15;
@@ -1815,19 +1811,21 @@ __global__ void __launch_bounds__(f3::NT, MRAB_F3_MINB) k_flux3w(DevMesh m, cons
         wfv = fvtile[fx + ntx * (fy + nty * fz)];
         if (fx + 1 < ntx) wfv |= fvtile[fx + 1 + ntx * (fy + nty * fz)];
     }
-    const int nreg = VISC ? NREG : WN;   // Euler: no gradients, the tile itself suffices
+    const int nreg = VISC ? NREG : NCORE;   // Euler: no gradients, the tile rows suffice
     // ---- region state through registers -> primitives in shared memory (two batches)
 #pragma unroll
     for (int b0 = 0; b0 < KR; b0 += 4) {
         double q[4][5];
-        int tt[4];
+        int tt[4], tp[4];
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
             const int t = tid + (b0 + r) * NT;
             tt[r] = t < nreg ? t : -1;
+            tp[r] = -1;
             if (tt[r] < 0) continue;
             int x, y, z;
             xyz(t, x, y, z);
+            if (t < NCORE && x >= 0 && x < WX) tp[r] = x + 16 * y + 128 * z;   // a point of the tile
             int gi = i0 + x, gj = j0 + y, gk = k0 + z;
             if (gi < 0) gi = per0 ? gi + n0 : 0; else if (gi >= n0) gi = per0 ? gi - n0 : n0 - 1;
             if (gj < 0) gj = per1 ? gj + n1 : 0; else if (gj >= n1) gj = per1 ? gj - n1 : n1 - 1;
@@ -1846,7 +1844,7 @@ __global__ void __launch_bounds__(f3::NT, MRAB_F3_MINB) k_flux3w(DevMesh m, cons
             pf[NREG + t] = v;
             pf[2 * NREG + t] = w;
             pf[3 * NREG + t] = g.gamma * g.gm1 * (q[r][4] - 0.5 * (q[r][1] * u + q[r][2] * v + q[r][3] * w)) * ir;
-            if (t < WN) rh[t] = q[r][0];
+            if (tp[r] >= 0) rh[tp[r]] = q[r][0];
         }
     }
 #pragma unroll
@@ -1870,8 +1868,9 @@ __global__ void __launch_bounds__(f3::NT, MRAB_F3_MINB) k_flux3w(DevMesh m, cons
             continue;
         }
         const double r = rh[t];
-        const double u[3] = {pf[t], pf[NREG + t], pf[2 * NREG + t]};
-        const double T = pf[3 * NREG + t];
+        const int ci = idx(x, y, z);
+        const double u[3] = {pf[ci], pf[NREG + ci], pf[2 * NREG + ci]};
+        const double T = pf[3 * NREG + ci];
         const double pr = r * T * g.igamma;
         const double E = pr * g.igm1 + 0.5 * r * (u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
         double fv[3][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}, {0, 0, 0, 0}};
